@@ -1,0 +1,197 @@
+"""Generate the golden vectors of tests/golden/*.npz from the REAL reference.
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every output array below is produced by the unmodified reference package
+``femmin`` (/root/reference/pkg/src/femmin).  Inputs (trial fields) come from
+the counter-based generator in ``oracle/femmin_oracle.py`` or from the
+reference test seeds; the meshes the reference cannot build (config-3
+rectangle, config-4/5 beam) are composed from reference pieces
+(``_grid_triangles``, ``_make_mesh``, ``mark_dirichlet``) exactly as
+SURVEY.md §0.1 #3/#4 describes.  The fixtures are small (a few MB in total).
+"""
+
+import os
+import re
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import femmin  # noqa: E402
+from femmin import bench, mesh as fmesh, patches as fpatches  # noqa: E402
+from femmin.assembly import LinearLoad, energy, interpolate  # noqa: E402
+from femmin.gradients import exact_gradient, numeric_gradient  # noqa: E402
+from femmin.models import (ElasticParams, InadmissibleStateError, NeoHookean,  # noqa: E402
+                           PLaplaceParams, PLaplacian)
+
+from oracle import femmin_oracle as O  # noqa: E402  (inputs only)
+
+
+class Lame:
+    def __init__(self, C1, D1):
+        self.C1, self.D1 = C1, D1
+
+
+def _mesh_arrays(m):
+    return dict(
+        coords=m.nodes2coord, conn=m.elems2nodes, volumes=m.volumes,
+        dphi=np.stack(m.dphi), d=np.int64(m.d),
+        nodes_dirichlet=m.nodes_dirichlet, nodes_minim=m.nodes_minim,
+        dofs_dirichlet=m.dofs_dirichlet, dofs_minim=m.dofs_minim,
+        dofs_minim_local=m.dofs_minim_local)
+
+
+def _patch_arrays(p):
+    return dict(p_lengths=p.lengths, p_prefix=p.prefix, p_elems=p.elems,
+                p_slot=np.argmax(p.logical, axis=1).astype(np.int64),
+                p_indx3=fpatches.patch_prefix_indices(p, 3))
+
+
+def _evaluate(m, p, model, load, v, fd_eps):
+    J, W = energy(v, m, model, load)
+    ge = exact_gradient(v, m, p, model, load)
+    gn = numeric_gradient(v, m, p, model, load, eps=fd_eps)
+    return dict(v=v, J=np.float64(J), densities=W, g_exact=ge, g_fd=gn,
+                fd_eps=np.float64(fd_eps),
+                b=(load.b if load is not None else np.zeros(m.d * m.nn)))
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"{name}: {os.path.getsize(path) / 1e3:.0f} kB")
+
+
+def case_lshape(level, p, seed, name, fd_eps=1e-6):
+    m = bench.lshape_problem(level)
+    pt = femmin.build_patches(m)
+    model = PLaplacian(PLaplaceParams(p=p), dim=2)
+    load = LinearLoad.assemble(m, -10.0, d=1)
+    v = np.zeros(m.nn)
+    v[m.dofs_minim] = O.uniform01(seed, m.dofs_minim)
+    save(name, **_mesh_arrays(m), **_patch_arrays(pt),
+         **_evaluate(m, pt, model, load, v, fd_eps), p=np.float64(p),
+         level=np.int64(level), seed=np.int64(seed))
+
+
+def case_bar_twist():
+    m = bench.bar_problem(1)
+    pt = femmin.build_patches(m)
+    model = NeoHookean(bench.BAR_MATERIAL, dim=3)
+    v = interpolate(bench.twist_map(2 * np.pi), m, d=3)
+    out = _evaluate(m, pt, model, None, v, 1e-6)
+    # admissible random affine field + noise, as test_gradients.py:21-28
+    rng = np.random.default_rng(20240817)
+    A = np.eye(3) + 0.05 * rng.normal(size=(3, 3))
+    while np.linalg.det(A) < 0.5:
+        A = np.eye(3) + 0.05 * rng.normal(size=(3, 3))
+    v2 = interpolate(lambda x: x @ A.T, m, d=3) + 1e-6 * rng.normal(size=3 * m.nn)
+    out2 = _evaluate(m, pt, model, None, v2, 1e-6)
+    # inadmissible behaviour: collapsed field and a huge FD step at identity
+    J0, W0 = energy(np.zeros(3 * m.nn), m, model)
+    try:
+        numeric_gradient(interpolate(lambda x: x, m, d=3), m, pt, model, eps=1.0)
+        bad_dof = -1
+    except InadmissibleStateError as exc:
+        bad_dof = int(re.search(r"dof (\d+)", str(exc)).group(1))
+    save("bar1_nh", **_mesh_arrays(m), **_patch_arrays(pt), **out,
+         **{k + "_2": val for k, val in out2.items()},
+         C1=np.float64(bench.BAR_MATERIAL.C1), D1=np.float64(bench.BAR_MATERIAL.D1),
+         J_collapsed=np.float64(J0), fd_bad_dof_eps1=np.int64(bad_dof))
+
+
+def case_bar2_mesh():
+    m = bench.bar_problem(2)
+    pt = femmin.build_patches(m)
+    save("bar2_mesh", coords=m.nodes2coord, conn=m.elems2nodes, volumes=m.volumes,
+         dphi=np.stack(m.dphi), nodes_minim=m.nodes_minim, dofs_minim=m.dofs_minim,
+         p_lengths=pt.lengths, p_elems=pt.elems,
+         p_slot=np.argmax(pt.logical, axis=1).astype(np.int64))
+
+
+def case_rect(nx, ny, seed):
+    xs = np.linspace(0.0, 2.0, nx + 1)
+    ys = np.linspace(0.0, 1.0, ny + 1)
+    Y, X = np.meshgrid(ys, xs, indexing="ij")
+    coords = np.column_stack([X.ravel(), Y.ravel()])
+    tri, _, _ = fmesh._grid_triangles(nx, ny)
+    m = fmesh._make_mesh(2, -1, coords, tri)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    m = fmesh.mark_dirichlet(m, spec, d=2)
+    pt = femmin.build_patches(m)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    model = NeoHookean(ElasticParams(E=E, nu=nu), dim=2)
+    model.params = Lame(mu / 2, lam / 2)          # duck-typed D1 = lambda/2
+    load = LinearLoad.assemble(m, (0.0, -3.5e7), d=2)
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    v[m.dofs_minim] += 1e-2 * (2.0 / nx) * (2.0 * O.uniform01(seed, m.dofs_minim) - 1.0)
+    save(f"rect{nx}x{ny}_nh", **_mesh_arrays(m), **_patch_arrays(pt),
+         **_evaluate(m, pt, model, load, v, 1e-8), C1=np.float64(mu / 2),
+         D1=np.float64(lam / 2), nx=np.int64(nx), ny=np.int64(ny), seed=np.int64(seed))
+
+
+def case_beam(nx, ny, nz, seed):
+    # coordinates / connectivity from the restated generator (pinned against
+    # generate_bar_mesh_3d by test_oracle_golden), everything else reference
+    om = O.beam_mesh(nx, ny, nz, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    m = fmesh._make_mesh(3, -1, om.nodes2coord, om.elems2nodes)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    m = fmesh.mark_dirichlet(m, spec, d=3)
+    pt = femmin.build_patches(m)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    model = NeoHookean(ElasticParams(E=E, nu=nu), dim=3)
+    model.params = Lame(mu / 2, lam / 2)
+    load = LinearLoad.assemble(m, (0.0, 0.0, -2.5e7), d=3)
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    v[m.dofs_minim] += 1e-2 * (2.0 / nx) * (2.0 * O.uniform01(seed, m.dofs_minim) - 1.0)
+    save(f"beam{nx}x{ny}x{nz}_nh", **_mesh_arrays(m), **_patch_arrays(pt),
+         **_evaluate(m, pt, model, load, v, 1e-8), C1=np.float64(mu / 2),
+         D1=np.float64(lam / 2), nx=np.int64(nx), ny=np.int64(ny), nz=np.int64(nz),
+         seed=np.int64(seed))
+
+
+def case_lshape1_tests():
+    """The reference unit-test fixture lshape_problem(1) with its rng seed."""
+    m = bench.lshape_problem(1)
+    pt = femmin.build_patches(m)
+    rng = np.random.default_rng(20240817)
+    v = rng.normal(size=m.nn)
+    out = {}
+    for p in (1.5, 3.0, 4.0):
+        model = PLaplacian(PLaplaceParams(p=p), dim=2)
+        load = LinearLoad.assemble(m, -10.0, d=1)
+        r = _evaluate(m, pt, model, load, v, 1e-6)
+        out.update({f"{k}_p{p:g}": val for k, val in r.items() if k != "v"})
+    save("lshape1_plap", **_mesh_arrays(m), **_patch_arrays(pt), v=v, **out)
+
+
+def case_small_shapes():
+    """Counts and partitions of small generated meshes (mesh tests)."""
+    out = {}
+    for lvl in (0, 1, 2, 3):
+        m = fmesh.generate_lshape_mesh_2d(lvl)
+        out[f"lshape{lvl}_coords"] = m.nodes2coord
+        out[f"lshape{lvl}_conn"] = m.elems2nodes
+        out[f"lshape{lvl}_volumes"] = m.volumes
+        out[f"lshape{lvl}_dphi"] = np.stack(m.dphi)
+    save("lshape_meshes", **out)
+
+
+if __name__ == "__main__":
+    case_small_shapes()
+    case_lshape1_tests()
+    case_lshape(4, 3.0, 2109, "cfg1_lshape4_p3")
+    case_lshape(4, 1.8, 2110, "lshape4_p1.8")
+    case_bar_twist()
+    case_bar2_mesh()
+    case_rect(32, 16, 2109)
+    case_beam(8, 4, 4, 2109)
