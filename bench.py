@@ -1,0 +1,323 @@
+"""Benchmark: fused J + exact grad J on the config-4 Neo-Hookean beam.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg4] [--no-cpu-baseline]
+
+N = 1: BASELINE.json configs[3] (3D compressible Neo-Hookean, 256x128x128 Kuhn
+beam, 25,165,824 tets) — the config the north-star target (>= 60 % of the HBM
+roofline on the 3D NH exact-gradient path) is quoted on.  One step = one fused
+J + grad J evaluation of the whole mesh (energy, chain-rule gradient on all
+12.78M free dofs, consistent load), device-resident.  N > 1 (torchrun): the
+beam is split into x1-slabs, one per rank, J is all-reduced over NCCL and the
+interface-plane gradient partials are exchanged with the slab neighbours
+(strong scaling: the total mesh is fixed).
+
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the reference
+algorithm's CPU implementation (the oracle port of femmin, oracle/) on this
+host on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic bytes per element of one fused J+grad pass (SURVEY.md §8d,
+# "variant S"): int32 conn, f64 vol, f64 dphi, v and b read once per node,
+# g written once per free dof
+def algorithmic_bytes(dim, d, ne, nn, nfree_dofs):
+    per_elem = 4 * (dim + 1) + 8 + 8 * dim * (dim + 1)
+    return ne * per_elem + 8 * d * nn * 2 + 8 * nfree_dofs
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline_sample(nx=96, ny=48, nz=48, repeats=2):
+    """Reference algorithm (oracle port of femmin, numpy) on host cores: a
+    bounded sample of the same workload (3D NH Kuhn beam, same box/field)."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    from oracle import femmin_oracle as O
+    m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109)
+    P = O.build_patches(m)
+    best = float("inf")
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.energy(v, m, model, b)
+        O.exact_gradient(v, m, P, model, b)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": m.ne / best / 1e6, "unit": "Melem/s",
+            "cores": 1, "kind": "port",
+            "sample": f"beam {nx}x{ny}x{nz} ({m.ne} tets), femmin algorithm (oracle port: "
+                      f"energy + exact_gradient, numpy ufuncs single-threaded, OpenBLAS ddot "
+                      f"with {os.environ.get('OMP_NUM_THREADS')} threads), best of {repeats}",
+            "seconds_per_eval": best}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host CPU (rank 0 only)."""
+    if rank != 0:
+        return
+    nx, ny, nz = 64, 32, 32
+    from oracle import femmin_oracle as O
+    m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109)
+    P = O.build_patches(m)
+    for _ in range(args.warmup):
+        O.energy(v, m, model, b)
+        O.exact_gradient(v, m, P, model, b)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.energy(v, m, model, b)
+        O.exact_gradient(v, m, P, model, b)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = m.ne / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "J+gradJ throughput (fused J + exact gradient evals)",
+        "value": value, "unit": "Melem/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg4-type 3D Neo-Hookean Kuhn beam sample {nx}x{ny}x{nz} "
+                               f"({m.ne} tets) on [0,2]x[0,1]^2", "parallelism": "host CPU"},
+        "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": 1, "kind": "port",
+                         "sample": f"beam {nx}x{ny}x{nz}, femmin algorithm (oracle port), "
+                                   f"numpy single-threaded ufuncs"},
+        "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tile-nodes", type=int, default=0)
+    ap.add_argument("--box", type=str, default="")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2109_01158_b200 import problems
+    from paper_2109_01158_b200.parallel import SlabExchange, slab_range
+
+    tiling = None
+    if args.tile_nodes or args.box:
+        box = [int(x) for x in args.box.split(",")] if args.box else [0, 0, 0]
+        tiling = (args.tile_nodes, box + [0] * (3 - len(box)))
+
+    nx, ny, nz = 256, 128, 128
+    if args.config == "cfg4":
+        ix0, ix1 = slab_range(nx, rank, world)
+        pr = problems.beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1, tiling=tiling)
+        workload = "cfg4: 3D compressible Neo-Hookean beam [0,2]x[0,1]^2, 256x128x128 hexes x 6 " \
+                   "Kuhn tets (25,165,824 tets, 4,276,737 nodes), f=(0,0,-2.5e7), v=x on x1=0"
+        ne_total = 6 * nx * ny * nz
+    else:
+        if world > 1:
+            raise SystemExit("only cfg4 is partitioned across GPUs")
+        pr = problems.CONFIGS[args.config](tiling=tiling)
+        workload = args.config
+        ne_total = pr.ne
+    dm, model, b, v = pr.dm, pr.model, pr.b, pr.v
+    ex = SlabExchange.from_problem(pr, rank, world) if world > 1 else None
+    g = torch.empty(dm.nfree_dofs, dtype=torch.float64, device="cuda")
+    J = torch.empty(3, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dm.exact_gradient(v, model, b, g=g, J=J)
+        if ex is not None:
+            ex.reduce(g, J)
+
+    for _ in range(args.warmup):
+        step()
+    dm.check()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    # kernel events (dominant tile kernel) + step events, all on the launching stream
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for a, z in kev:
+        a.record(stream)
+        z.record(stream)
+    l0 = dm.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        dm.time_next(*kev[i])
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = dm.launches() - l0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    kms = sum(a.elapsed_time(z) for a, z in kev) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms, kms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, kms = float(tt[0]), float(tt[1])
+    dm.check()
+
+    # ---- end to end through the public device API, host buffers ----------
+    v_host = v.cpu().pin_memory()
+    g_host = torch.empty(g.shape, dtype=torch.float64).pin_memory()
+    J_host = torch.empty(3, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_step():
+        v.copy_(v_host, non_blocking=True)
+        step()
+        g_host.copy_(g, non_blocking=True)
+        J_host.copy_(J, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0])
+
+    value = ne_total / (ms * 1e-3) / 1e6
+    peak, peak_src = _peaks()
+    alg = algorithmic_bytes(dm.dim, dm.d, dm.ne, dm.nn, dm.nfree_dofs)
+    achieved = alg / (kms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(f"{args.config}_n{world}")
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_sample()
+        line = {
+            "metric": "J+gradJ throughput (fused J + exact gradient evals x elements / s)",
+            "value": value, "unit": "Melem/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (GPU-generated mesh, seeded splitmix64 field v = x + U[-a,a])",
+            "config": {"workload": workload, "elements": ne_total,
+                       "evals_per_s": 1e3 / ms,
+                       "parallelism": f"x1-slabs x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (3.3 GB per eval) larger than the 126 MB L2; no flush",
+                       "tiles": {k: dm.stats[k] for k in ("n_tiles", "redundancy",
+                                                          "max_tile_elems")}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_tile_exact<3,NH,J,G>", "kernel_ms": kms,
+                         "algorithmic_bytes_per_launch": alg,
+                         "bytes_per_elem": alg / dm.ne, "peak_source": peak_src,
+                         "frac_of_8TBs_nominal": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ne_total / (e2e_ms * 1e-3) / 1e6, "unit": "Melem/s",
+                    "h2d_bytes_per_step": int(v.numel() * 8),
+                    "d2h_bytes_per_step": int(g.numel() * 8 + 24),
+                    "api": "DeviceMesh.exact_gradient(v, model, b, g, J) with pinned host v/g/J"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+// Device-side layout of an evaluation context (the frozen Mesh + Patches of
+// mesh.py:31-53 / patches.py:22-34, re-laid out for sm_100a) and the device
+// functions shared by the evaluation kernels.
+//
+// Element records (AoS, one per element, storage order = grouped by owner tile):
+//   3D: 128 B = int32 conn[4] | f64 vol | f64 dphi[3][4] | int32 orig | pad
+//   2D:  80 B = int32 conn[3] | int32 orig | f64 vol | f64 dphi[2][3] | pad
+// One record is exactly one (3D) 128-byte line: a gather by element id costs
+// one line, and vol + dphi + conn arrive together.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "fm_common.cuh"
+
+namespace fm {
+
+constexpr int FLAG_J = 16;           // tile element contributes to J (its owner tile)
+constexpr int MAX_TILE_ELEMS = 16384; // node entries store te_local in 14 bits
+
+template <int DIM> struct RecBytes;
+template <> struct RecBytes<2> { static constexpr int value = 80; };
+template <> struct RecBytes<3> { static constexpr int value = 128; };
+
+template <int DIM> struct Elem {
+  int c[DIM + 1];
+  int orig;
+  double vol;
+  double g[DIM][DIM + 1];  // dphi[m][l]
+};
+
+// Element records are read exactly once per visit: stream them past L1.
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+template <int DIM>
+__device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64_t s,
+                                          Elem<DIM> &E) {
+  const double2 *p =
+      reinterpret_cast<const double2 *>(aos + s * (int64_t)RecBytes<DIM>::value);
+  if constexpr (DIM == 3) {
+    double2 q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = ld_stream(p + k);
+    E.c[0] = __double2loint(q[0].x);
+    E.c[1] = __double2hiint(q[0].x);
+    E.c[2] = __double2loint(q[0].y);
+    E.c[3] = __double2hiint(q[0].y);
+    E.vol = q[1].x;
+    const double f[12] = {q[1].y, q[2].x, q[2].y, q[3].x, q[3].y, q[4].x,
+                          q[4].y, q[5].x, q[5].y, q[6].x, q[6].y, q[7].x};
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+#pragma unroll
+      for (int l = 0; l < 4; ++l) E.g[m][l] = f[m * 4 + l];
+    E.orig = __double2loint(q[7].y);
+  } else {
+    double2 q[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) q[k] = ld_stream(p + k);
+    E.c[0] = __double2loint(q[0].x);
+    E.c[1] = __double2hiint(q[0].x);
+    E.c[2] = __double2loint(q[0].y);
+    E.orig = __double2hiint(q[0].y);
+    E.vol = q[1].x;
+    E.g[0][0] = q[1].y;
+    E.g[0][1] = q[2].x;
+    E.g[0][2] = q[2].y;
+    E.g[1][0] = q[3].x;
+    E.g[1][1] = q[3].y;
+    E.g[1][2] = q[4].x;
+  }
+}
+
+// Gather the d components of the field at the element's nodes (v interleaved).
+template <int DIM, int D>
+__device__ __forceinline__ void gather_v(const double *__restrict__ v, const Elem<DIM> &E,
+                                         double (&vv)[D][DIM + 1]) {
+#pragma unroll
+  for (int l = 0; l < DIM + 1; ++l) {
+    const double *p = v + (int64_t)E.c[l] * D;
+#pragma unroll
+    for (int j = 0; j < D; ++j) vv[j][l] = __ldg(p + j);
+  }
+}
+
+struct ModelArgs {
+  int kind;  // FM_MODEL_*
+  double p, C1, D1;
+  // p-Laplace exponents classified like numpy's fast scalar power
+  // (ndarray ** scalar: 0.5 -> sqrt, 1 -> copy, 2 -> square, -1 -> reciprocal)
+  double e_w, e_dw;  // p/2 and (p-2)/2
+};
+
+__device__ __forceinline__ double np_scalar_pow(double x, double e) {
+  if (e == 0.5) return sqrt(x);
+  if (e == 1.0) return x;
+  if (e == 2.0) return x * x;
+  if (e == -1.0) return 1.0 / x;
+  if (e == 0.0) return 1.0;
+  return pow(x, e);
+}
+
+// Tile tables (built by fm_ctx_create).
+struct TileArgs {
+  const uint8_t *aos;
+  const int32_t *tile_elem_ptr;   // n_tiles_all + 1
+  const int32_t *tile_elems;      // storage index per tile element
+  const uint8_t *tile_flags;      // owned-slot mask | FLAG_J
+  const int32_t *tile_node_ptr;   // n_tiles_all + 1 (orphan tiles: empty)
+  const int32_t *tile_node_rank;  // free rank per tile node
+  const int32_t *node_entry_ptr;  // per tile node + 1
+  const uint16_t *node_entries;   // te_local << 2 | slot, ascending element
+  const int32_t *free_node;       // nodes_minim (int32)
+  const int32_t *free_out;        // output offset of the node's first free dof
+  const uint8_t *free_mask;       // free components
+  const int32_t *rank_of;         // node -> free rank or -1
+};
+
+// Deterministic block sum (fixed shuffle tree + fixed warp order).
+__device__ __forceinline__ double block_sum(double x, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = x;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+}  // namespace fm
+
+// Host-side context.
+struct fm_ctx {
+  int dim = 0, d = 0, nv = 0, tile_nodes = 0;
+  int64_t nn = 0, ne = 0, nfree = 0, nfree_dofs = 0, p_total = 0;
+  int32_t n_tiles = 0, n_tiles_all = 0;
+  int64_t n_tile_elems = 0, n_node_entries = 0;
+  int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0;
+  uint8_t *aos = nullptr;
+  int32_t *tile_elem_ptr = nullptr, *tile_elems = nullptr, *tile_node_ptr = nullptr;
+  int32_t *tile_node_rank = nullptr, *node_entry_ptr = nullptr;
+  uint8_t *tile_flags = nullptr;
+  uint16_t *node_entries = nullptr;
+  int32_t *free_node = nullptr, *free_out = nullptr, *rank_of = nullptr;
+  int32_t *storage_to_orig = nullptr;
+  uint8_t *free_mask = nullptr;
+  // scratch
+  double *jpart = nullptr;        // per tile (fused) / per block (energy)
+  double *dotpart = nullptr;      // b.v partials
+  int n_dot_blocks = 0, n_energy_blocks = 0;
+  unsigned long long *status = nullptr;  // [0] exact inadmissible, [1] FD min key
+  int64_t launches = 0;
+  size_t bytes = 0;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // armed by fm_ctx_time_next
+  fm_ctx_stats stats{};
+
+  fm::TileArgs tile_args() const {
+    return fm::TileArgs{aos,          tile_elem_ptr, tile_elems, tile_flags,
+                        tile_node_ptr, tile_node_rank, node_entry_ptr, node_entries,
+                        free_node,     free_out,       free_mask,      rank_of};
+  }
+};

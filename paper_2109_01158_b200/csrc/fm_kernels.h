@@ -1,0 +1,35 @@
+// Internal launcher declarations shared between translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fm_ctx.cuh"
+
+namespace fm {
+
+cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int n_tiles, int threads,
+                              size_t smem_entries, bool wj, bool wg, const double *v,
+                              const double *b, double *g, double *jpart,
+                              unsigned long long *status, const ModelArgs &m, cudaStream_t s);
+
+cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
+                           size_t smem_entries, const double *v, const double *b, double eps,
+                           double *g, unsigned long long *badkey, const ModelArgs &m,
+                           cudaStream_t s);
+
+cudaError_t launch_energy(int dim, int model, const uint8_t *aos, int64_t ne, int nblocks,
+                          const double *v, double *part, double *dens, const ModelArgs &m,
+                          cudaStream_t s);
+
+cudaError_t launch_dot(const double *a, const double *b, int64_t n, int nblocks, double *part,
+                       cudaStream_t s);
+
+cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, double *out,
+                            cudaStream_t s);
+
+cudaError_t launch_descent(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
+                           const uint8_t *free_mask, const double *g, double alpha, double *v,
+                           cudaStream_t s);
+
+}  // namespace fm

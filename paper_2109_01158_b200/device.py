@@ -1,0 +1,213 @@
+"""Device-resident evaluation contexts (the B200 side of the drop-in boundary).
+
+``DeviceMesh`` owns one ``fm_ctx`` (include/femmin_b200.h): the frozen Mesh +
+Patches of the reference (mesh.py:31-53, patches.py:22-34) uploaded once and
+re-laid out as 128-byte element records and node tiles.  Its methods take and
+return CUDA tensors without host copies; the numpy drop-in functions in
+``assembly`` / ``gradients`` are thin wrappers that upload ``v``, call these and
+copy the result back.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import ptr, require_cuda, stream_ptr, to_dev
+
+DEFAULT_EPS = 1e-8  # gradients.py:20
+
+# ---------------------------------------------------------------------------
+# device tensors attached to host objects (Mesh / Patches / LinearLoad)
+
+_ATTACHED: dict[int, dict] = {}
+
+
+def attach(obj, **tensors):
+    key = id(obj)
+    if key not in _ATTACHED:
+        _ATTACHED[key] = {}
+        weakref.finalize(obj, _ATTACHED.pop, key, None)
+    _ATTACHED[key].update(tensors)
+
+
+def attached(obj) -> dict | None:
+    return _ATTACHED.get(id(obj))
+
+
+class DeviceMesh:
+    """One evaluation context on the current CUDA device.
+
+    Arguments are CUDA tensors in the reference layout: coords (nn, dim) f64,
+    conn (ne, dim+1) i64, volumes (ne,) f64, dphi (dim, ne, dim+1) f64,
+    nodes_minim (nfree,) i64 ascending, fixed (nn*d,) u8, and the patch CSR
+    p_prefix (nfree,) i64 inclusive, p_elems / p_slot (||T||,) i64.
+    """
+
+    def __init__(self, *, dim, d, coords, conn, volumes, dphi, nodes_minim, fixed, p_prefix,
+                 p_elems, p_slot, tiling=None):
+        self._lib = require_cuda()
+        self.dim, self.d = int(dim), int(d)
+        self.nn, self.ne = int(coords.shape[0]), int(conn.shape[0])
+        self.nfree = int(nodes_minim.shape[0])
+        desc = _lib.FmMeshDesc(self.dim, self.d, self.nn, self.ne, ptr(coords), ptr(conn),
+                               ptr(volumes), ptr(dphi), self.nfree, ptr(nodes_minim), ptr(fixed),
+                               ptr(p_prefix), ptr(p_elems), ptr(p_slot), int(p_elems.shape[0]))
+        til = None
+        if tiling is not None:
+            nt, box = tiling
+            til = _lib.FmTiling(int(nt), (C.c_int32 * 3)(*[int(b) for b in box]))
+        h = C.c_void_p()
+        _lib.check(self._lib.fm_ctx_create(C.byref(desc), C.byref(til) if til else None,
+                                           stream_ptr(), C.byref(h)), "fm_ctx_create")
+        self._h = h
+        self._fin = weakref.finalize(self, self._lib.fm_ctx_destroy, h)
+        st = _lib.FmCtxStats()
+        _lib.check(self._lib.fm_ctx_stats_get(h, C.byref(st)))
+        self.stats = {k: getattr(st, k) for k, _ in _lib.FmCtxStats._fields_}
+        self.nodes_minim = nodes_minim
+        self.nfree_dofs = self._count_free_dofs(fixed, nodes_minim)
+        self._J = torch.empty(3, dtype=torch.float64, device="cuda")
+
+    def _count_free_dofs(self, fixed, nodes_minim):
+        return int(fixed.numel() - int(fixed.sum().item()))
+
+    def close(self):
+        self._fin()
+
+    # ---- evaluation (asynchronous on the current stream) --------------------
+    def energy(self, v, model, b=None, densities=None, out=None):
+        """J (device double[3]: J, sum vol*W, b.v) of assembly.py:94-106."""
+        out = self._J if out is None else out
+        m = _model(model)
+        _lib.check(self._lib.fm_energy(self._h, C.byref(m), ptr(v), ptr(b), ptr(out),
+                                       ptr(densities), stream_ptr()), "fm_energy")
+        return out
+
+    def exact_gradient(self, v, model, b=None, g=None, J=None):
+        """gradients.py:124-149 into g (nfree_dofs,), fused with J when given."""
+        if g is None:
+            g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        m = _model(model)
+        _lib.check(self._lib.fm_grad_exact(self._h, C.byref(m), ptr(v), ptr(b), ptr(g), ptr(J),
+                                           stream_ptr()), "fm_grad_exact")
+        return g
+
+    def numeric_gradient(self, v, model, b=None, eps=DEFAULT_EPS, g=None):
+        """gradients.py:84-121 into g (nfree_dofs,)."""
+        if g is None:
+            g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        m = _model(model)
+        _lib.check(self._lib.fm_grad_fd(self._h, C.byref(m), ptr(v), ptr(b), float(eps), ptr(g),
+                                        stream_ptr()), "fm_grad_fd")
+        return g
+
+    def descent_step(self, v, g, alpha):
+        """v_free <- v_free - alpha * g (Dirichlet dofs untouched)."""
+        _lib.check(self._lib.fm_descent_step(self._h, ptr(v), ptr(g), float(alpha),
+                                             stream_ptr()))
+        return v
+
+    def check(self):
+        """Synchronise and raise InadmissibleStateError for latched conditions."""
+        idx = C.c_int64(-1)
+        _lib.check(self._lib.fm_ctx_check(self._h, stream_ptr(), C.byref(idx)))
+
+    def launches(self) -> int:
+        return int(self._lib.fm_ctx_launches(self._h))
+
+    def time_next(self, start: "torch.cuda.Event", stop: "torch.cuda.Event"):
+        """Record the two (already created) CUDA events around the next
+        dominant kernel launch of this context."""
+        _lib.check(self._lib.fm_ctx_time_next(self._h, C.c_void_p(start.cuda_event),
+                                              C.c_void_p(stop.cuda_event)))
+
+    # ---- construction from host objects --------------------------------------
+    @classmethod
+    def from_host(cls, mesh, patches=None, d=None, tiling=None) -> "DeviceMesh":
+        """Upload a (reference-compatible) Mesh + Patches; reuse device copies
+        attached by this package's generators."""
+        dev = attached(mesh) or {}
+        d = int(mesh.d if d is None else d)
+        dim = int(mesh.dim)
+        coords = dev.get("coords")
+        if coords is None:
+            coords = to_dev(np.asarray(mesh.nodes2coord, dtype=np.float64))
+        conn = dev.get("conn")
+        if conn is None:
+            conn = to_dev(np.asarray(mesh.elems2nodes, dtype=np.int64))
+        vol = dev.get("volumes")
+        if vol is None:
+            vol = to_dev(np.asarray(mesh.volumes, dtype=np.float64))
+        dphi = dev.get("dphi")
+        if dphi is None:
+            dphi = to_dev(np.stack([np.asarray(g, dtype=np.float64) for g in mesh.dphi]))
+        if d == int(mesh.d):
+            nm = dev.get("nodes_minim")
+            if nm is None:
+                nm = to_dev(np.asarray(mesh.nodes_minim, dtype=np.int64))
+            fixed = dev.get("fixed")
+            if fixed is None:
+                fx = np.zeros(mesh.nn * d, dtype=np.uint8)
+                fx[np.asarray(mesh.dofs_dirichlet, dtype=np.int64)] = 1
+                fixed = to_dev(fx)
+        else:  # component count differs from the partition: treat every dof as free
+            nm = torch.arange(mesh.nn, dtype=torch.int64, device="cuda")
+            fixed = torch.zeros(mesh.nn * d, dtype=torch.uint8, device="cuda")
+            patches = None
+        if patches is not None:
+            pdev = attached(patches) or {}
+            prefix = pdev.get("prefix")
+            if prefix is None:
+                prefix = to_dev(np.asarray(patches.prefix, dtype=np.int64))
+            elems = pdev.get("elems")
+            if elems is None:
+                elems = to_dev(np.asarray(patches.elems, dtype=np.int64))
+            slot = pdev.get("slot")
+            if slot is None:
+                s = getattr(patches, "slot", None)
+                if s is None:
+                    s = np.argmax(np.asarray(patches.logical), axis=1)
+                slot = to_dev(np.asarray(s, dtype=np.int64))
+        else:
+            from .patches import build_patches_device
+            prefix, elems, slot = build_patches_device(conn, nm, mesh.nn, dim + 1)
+        return cls(dim=dim, d=d, coords=coords, conn=conn, volumes=vol, dphi=dphi,
+                   nodes_minim=nm, fixed=fixed, p_prefix=prefix, p_elems=elems, p_slot=slot,
+                   tiling=tiling)
+
+
+def _model(model) -> _lib.FmModel:
+    if isinstance(model, _lib.FmModel):
+        return model
+    from .models import fm_model_struct
+    return fm_model_struct(model)
+
+
+# ---------------------------------------------------------------------------
+# context cache for the numpy drop-in (frozen Mesh / Patches are immutable)
+
+_CTX: dict[tuple, DeviceMesh] = {}
+
+
+def _drop(key):
+    ctx = _CTX.pop(key, None)
+    if ctx is not None:
+        ctx.close()
+
+
+def context_for(mesh, patches=None, d=None) -> DeviceMesh:
+    d = int(mesh.d if d is None else d)
+    key = (id(mesh), id(patches) if patches is not None else 0, d)
+    ctx = _CTX.get(key)
+    if ctx is None:
+        ctx = DeviceMesh.from_host(mesh, patches, d)
+        _CTX[key] = ctx
+        weakref.finalize(mesh, _drop, key)
+        if patches is not None:
+            weakref.finalize(patches, _drop, key)
+    return ctx

@@ -1,0 +1,94 @@
+"""Multi-GPU x1-slab partition of the Kuhn beam (configs 4/5).
+
+Each rank generates and evaluates its own slab of cubes ix in [ix0, ix1)
+(``problems.beam(..., ix0=, ix1=)``): elements are disjoint, the nodes of the
+interface planes x = xs[ix0] and x = xs[ix1] are shared with the neighbours.
+Because J, the consistent load b and the element contributions to grad J are
+all sums over elements, each rank's slab-local results are exact partial sums:
+
+* J       = sum over ranks of the local J (elastic part and b.v both split by
+            elements) -> all-gather of 3 doubles, summed in rank order, so every
+            rank holds the same bits;
+* grad J  = local value at interior nodes; at an interface node the sum of the
+            two neighbours' partials, exchanged as one plane buffer
+            (ny+1)(nz+1)*3 doubles per side over NCCL send/recv and added as
+            own + received (a + b == b + a, so both copies are bitwise equal).
+
+The descent update of config 5 then needs no further exchange.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def slab_range(nx: int, rank: int, world: int) -> tuple[int, int]:
+    """Cubes [ix0, ix1) of rank ``rank`` (balanced contiguous x1-slabs)."""
+    return nx * rank // world, nx * (rank + 1) // world
+
+
+def plane_nodes(ixl: int, nxl: int, ny: int, nz: int, device=None) -> torch.Tensor:
+    """Slab-local node ids of the x-plane ixl (0 <= ixl <= nxl), (iy, iz) order."""
+    k = torch.arange((ny + 1) * (nz + 1), dtype=torch.int64, device=device)
+    return ixl + (nxl + 1) * k
+
+
+def plane_dof_positions(nodes: torch.Tensor, d: int, dofs_minim: torch.Tensor) -> torch.Tensor:
+    """Positions of the nodes' d dofs (node-major) in the restricted gradient."""
+    dofs = (nodes[:, None] * d + torch.arange(d, device=nodes.device)[None]).reshape(-1)
+    pos = torch.searchsorted(dofs_minim, dofs)
+    if not torch.equal(dofs_minim[pos.clamp(max=dofs_minim.numel() - 1)], dofs):
+        raise ValueError("interface plane holds Dirichlet dofs; slabs must not cut x1 = 0")
+    return pos
+
+
+class SlabExchange:
+    """Reduction of slab-local (J, grad J) partials across the x1-slab ranks."""
+
+    def __init__(self, nx, ny, nz, ix0, ix1, d, dofs_minim, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        nxl = ix1 - ix0
+        dev = dofs_minim.device
+        self.left = (plane_dof_positions(plane_nodes(0, nxl, ny, nz, dev), d, dofs_minim)
+                     if rank > 0 else None)
+        self.right = (plane_dof_positions(plane_nodes(nxl, nxl, ny, nz, dev), d, dofs_minim)
+                      if rank < world - 1 else None)
+        n = (ny + 1) * (nz + 1) * d
+        mk = lambda: torch.empty(n, dtype=torch.float64, device=dev)  # noqa: E731
+        self.send_l, self.recv_l = mk(), mk()
+        self.send_r, self.recv_r = mk(), mk()
+        self.jall = torch.empty((world, 3), dtype=torch.float64, device=dev)
+
+    @classmethod
+    def from_problem(cls, pr, rank, world, group=None):
+        mt = pr.meta
+        return cls(mt["nx"], mt["ny"], mt["nz"], mt["ix0"], mt["ix1"], pr.dm.d,
+                   mt["dofs_minim"], rank, world, group)
+
+    def reduce(self, g: torch.Tensor, J: torch.Tensor | None = None):
+        """In place: g += neighbours' interface partials; J <- global J."""
+        ops = []
+        if self.left is not None:
+            torch.index_select(g, 0, self.left, out=self.send_l)
+            ops += [dist.P2POp(dist.isend, self.send_l, self.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, self.recv_l, self.rank - 1, self.group)]
+        if self.right is not None:
+            torch.index_select(g, 0, self.right, out=self.send_r)
+            ops += [dist.P2POp(dist.isend, self.send_r, self.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, self.recv_r, self.rank + 1, self.group)]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if self.left is not None:
+            g.index_add_(0, self.left, self.recv_l)
+        if self.right is not None:
+            g.index_add_(0, self.right, self.recv_r)
+        if J is not None:
+            dist.all_gather_into_tensor(self.jall, J.reshape(1, 3).contiguous(),
+                                        group=self.group)
+            acc = self.jall[0].clone()
+            for r in range(1, self.world):
+                acc += self.jall[r]
+            J.copy_(acc)
+        return g, J

@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's golden
+vectors and the CPU oracle (same seeded inputs).
+
+Bars: index structures and coordinates bit-exact; J within
+1e-10 relative (observed ~1e-15); exact gradient within 1e-10 of max|g|
+(norm-relative); FD gradient within a roundoff bound derived per dof from the
+direct-sum oracle (u * sum_patch vol*|W+-| / (2 eps), factor written inline).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import femmin_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2109_01158_b200 as fb  # noqa: E402
+from paper_2109_01158_b200 import problems  # noqa: E402
+
+J_TOL = 1e-10
+G_TOL = 1e-10
+FD_FACTOR = 64.0      # FD bound: 64 u * sum_patch vol*(|W+|+|W-|) / (2 eps)
+
+GOLDEN_CASES = ["cfg1_lshape4_p3", "lshape4_p1.8", "bar1_nh", "rect32x16_nh", "beam8x4x4_nh"]
+
+
+def _golden_mesh(g):
+    m = fb.Mesh(dim=int(g["coords"].shape[1]), level=-1, nodes2coord=g["coords"],
+                elems2nodes=g["conn"], volumes=g["volumes"], dphi=list(g["dphi"]), d=int(g["d"]),
+                nodes_dirichlet=g["nodes_dirichlet"], nodes_minim=g["nodes_minim"],
+                dofs_dirichlet=g["dofs_dirichlet"], dofs_minim=g["dofs_minim"],
+                dofs_minim_local=g["dofs_minim_local"])
+    p = fb.Patches(lengths=g["p_lengths"], elems=g["p_elems"], volumes=None, elems2nodes=None,
+                   dphi=None, logical=None, prefix=g["p_prefix"], slot=g["p_slot"])
+    return m, p
+
+
+def _models(g, dim):
+    if "C1" in g:
+        return (fb.NeoHookean(fb.LameParams(float(g["C1"]), float(g["D1"])), dim),
+                O.Model("nh", O.LameParams(float(g["C1"]), float(g["D1"])), dim))
+    return (fb.PLaplacian(fb.PLaplaceParams(float(g["p"])), 2),
+            O.Model("plap", O.PParams(float(g["p"])), 2))
+
+
+def _omesh(g):
+    return O.OMesh(int(g["coords"].shape[1]), -1, g["coords"], g["conn"], g["volumes"],
+                   list(g["dphi"]), int(g["d"]), g["nodes_dirichlet"], g["nodes_minim"],
+                   g["dofs_dirichlet"], g["dofs_minim"], g["dofs_minim_local"])
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def _grel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def _check_fd(g_gpu, v, om, op, omodel, b, eps, g_ref_fd, g_exact):
+    gd, scale = O.numeric_gradient_direct(v, om, op, omodel, b, eps)
+    err = np.abs(g_gpu - gd)
+    bound = FD_FACTOR * scale + 1e-300
+    assert (err <= bound).all(), f"FD roundoff bound violated: max ratio {(err / bound).max()}"
+    gmax = np.abs(g_exact).max()
+    # and within the reference FD's own deviation from the exact gradient
+    ref_dev = np.abs(g_ref_fd - g_exact).max() / gmax
+    assert np.abs(g_gpu - g_ref_fd).max() / gmax <= 2 * ref_dev + 1e-12
+
+
+# ---------------------------------------------------------------- preprocessing
+@pytest.mark.parametrize("level", [0, 1, 2, 3])
+def test_lshape_generator_bit_exact(golden, level):
+    g = golden("lshape_meshes")
+    m = fb.generate_lshape_mesh_2d(level)
+    np.testing.assert_array_equal(m.nodes2coord, g[f"lshape{level}_coords"])
+    np.testing.assert_array_equal(m.elems2nodes, g[f"lshape{level}_conn"])
+    np.testing.assert_allclose(m.volumes, g[f"lshape{level}_volumes"], rtol=1e-13)
+    np.testing.assert_allclose(np.stack(m.dphi), g[f"lshape{level}_dphi"], rtol=1e-12,
+                               atol=1e-12 * np.abs(g[f"lshape{level}_dphi"]).max())
+
+
+def test_bar_generators_bit_exact(golden):
+    for level, name in ((1, "bar1_nh"), (2, "bar2_mesh")):
+        g = golden(name)
+        m = fb.generate_bar_mesh_3d(0.4, 0.01, 0.01, level)
+        np.testing.assert_array_equal(m.nodes2coord, g["coords"])
+        np.testing.assert_array_equal(m.elems2nodes, g["conn"])
+        np.testing.assert_allclose(m.volumes, g["volumes"], rtol=1e-12)
+        np.testing.assert_allclose(np.stack(m.dphi), g["dphi"], rtol=1e-11,
+                                   atol=1e-11 * np.abs(g["dphi"]).max())
+        spec = fb.DirichletSpec([fb.DirichletRegion(where=lambda x: x[:, 0] < 1e-9),
+                                 fb.DirichletRegion(where=lambda x: x[:, 0] > 0.4 - 1e-9)])
+        mm = fb.mark_dirichlet(m, spec, d=3)
+        np.testing.assert_array_equal(mm.nodes_minim, g["nodes_minim"])
+        np.testing.assert_array_equal(mm.dofs_minim, g["dofs_minim"])
+        p = fb.build_patches(mm)
+        np.testing.assert_array_equal(p.lengths, g["p_lengths"])
+        np.testing.assert_array_equal(p.elems, g["p_elems"])
+        np.testing.assert_array_equal(p.slot, g["p_slot"])
+        np.testing.assert_array_equal(np.argmax(p.logical, axis=1), g["p_slot"])
+        if level == 1:
+            assert (mm.nn, mm.ne, mm.nodes_dirichlet.size, mm.dofs_minim.size) == \
+                (729, 1920, 18, 2133)
+            assert (p.lengths.size, p.total_rows) == (711, 7584)
+            for k in ("nodes_dirichlet", "dofs_dirichlet", "dofs_minim_local"):
+                np.testing.assert_array_equal(getattr(mm, k), g[k])
+            np.testing.assert_array_equal(p.prefix, g["p_prefix"])
+            np.testing.assert_array_equal(fb.patch_prefix_indices(p, 3), g["p_indx3"])
+
+
+@pytest.mark.parametrize("name,builder", [
+    ("cfg1_lshape4_p3", lambda: problems.lshape(4, 3.0, seed=2109, keep=True)),
+    ("lshape4_p1.8", lambda: problems.lshape(4, 1.8, seed=2110, keep=True)),
+    ("rect32x16_nh", lambda: problems.rect(32, 16, seed=2109, keep=True)),
+    ("beam8x4x4_nh", lambda: problems.beam(8, 4, 4, seed=2109, keep=True)),
+])
+def test_device_problem_bit_exact(golden, name, builder):
+    """Whole GPU preprocessing chain of a benchmark config vs the reference."""
+    g = golden(name)
+    pr = builder()
+    mt = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in pr.meta.items()}
+    np.testing.assert_array_equal(mt["coords"], g["coords"])
+    np.testing.assert_array_equal(mt["conn"], g["conn"])
+    for k in ("nodes_minim", "dofs_minim", "dofs_minim_local", "dofs_dirichlet"):
+        np.testing.assert_array_equal(mt[k], g[k], err_msg=k)
+    np.testing.assert_array_equal(mt["nodes_dirichlet_idx"], g["nodes_dirichlet"])
+    np.testing.assert_array_equal(mt["p_prefix"], g["p_prefix"])
+    np.testing.assert_array_equal(mt["p_elems"], g["p_elems"])
+    np.testing.assert_array_equal(mt["p_slot"], g["p_slot"])
+    np.testing.assert_array_equal(pr.v.cpu().numpy(), g["v"])          # seeded field
+    np.testing.assert_allclose(pr.b.cpu().numpy(), g["b"], rtol=1e-13,
+                               atol=1e-14 * np.abs(g["b"]).max())
+    # evaluation on the GPU-built problem (GPU dphi / b differ from LAPACK / scipy in ulps)
+    J = pr.dm.energy(pr.v, pr.model, pr.b)
+    gg = pr.dm.exact_gradient(pr.v, pr.model, pr.b)
+    pr.dm.check()
+    assert _rel(float(J[0]), float(g["J"])) < J_TOL
+    assert _grel(gg.cpu().numpy(), g["g_exact"]) < G_TOL
+
+
+# ---------------------------------------------------------------- evaluation
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_energy_and_gradients_vs_reference(golden, name):
+    g = golden(name)
+    m, p = _golden_mesh(g)
+    model, omodel = _models(g, m.dim)
+    om = _omesh(g)
+    op = O.OPatches(g["p_lengths"], g["p_elems"], g["p_slot"], g["p_prefix"])
+    load = fb.LinearLoad(b=g["b"]) if np.any(g["b"]) else None
+    bo = g["b"] if load is not None else None
+    for sfx in ([""] if "v_2" not in g else ["", "_2"]):
+        v = g["v" + sfx]
+        J, W = fb.energy(v, m, model, load)
+        assert _rel(J, float(g["J" + sfx])) < J_TOL, (J, g["J" + sfx])
+        np.testing.assert_allclose(W, g["densities" + sfx], rtol=1e-13,
+                                   atol=1e-15 * np.abs(g["densities" + sfx]).max())
+        ge = fb.exact_gradient(v, m, p, model, load)
+        assert ge.shape == g["g_exact" + sfx].shape
+        assert _grel(ge, g["g_exact" + sfx]) < G_TOL
+        eps = float(g["fd_eps" + sfx])
+        gn = fb.numeric_gradient(v, m, p, model, load, eps=eps)
+        _check_fd(gn, v, om, op, omodel, bo, eps, g["g_fd" + sfx], g["g_exact" + sfx])
+        Jf, gf = fb.energy_and_gradient(v, m, p, model, load)
+        assert _rel(Jf, float(g["J" + sfx])) < J_TOL
+        assert _grel(gf, g["g_exact" + sfx]) < G_TOL
+
+
+@pytest.mark.parametrize("p", [1.5, 3.0, 4.0])
+def test_lshape1_reference_fixture(golden, p):
+    g = golden("lshape1_plap")
+    m, pt = _golden_mesh(g)
+    model = fb.PLaplacian(fb.PLaplaceParams(p), 2)
+    load = fb.LinearLoad(b=g[f"b_p{p:g}"])
+    v = g["v"]
+    assert _rel(fb.energy(v, m, model, load)[0], float(g[f"J_p{p:g}"])) < J_TOL
+    assert _grel(fb.exact_gradient(v, m, pt, model, load), g[f"g_exact_p{p:g}"]) < G_TOL
+    # the reference's loop oracle bar (test_gradients.py:133-155): 1e-13
+    ge = fb.exact_gradient(v, m, pt, model)
+    ref = O.exact_gradient_loop(v, _omesh(g), O.Model("plap", O.PParams(p), 2))
+    np.testing.assert_allclose(ge, ref, rtol=1e-13, atol=1e-13)
+
+
+def test_inadmissible_states_match_reference(golden):
+    g = golden("bar1_nh")
+    m, p = _golden_mesh(g)
+    model = fb.NeoHookean(fb.LameParams(float(g["C1"]), float(g["D1"])), 3)
+    zero = np.zeros(3 * m.nn)
+    J, W = fb.energy(zero, m, model)
+    assert np.isinf(J) and np.isinf(W).all()
+    with pytest.raises(fb.InadmissibleStateError, match="nonpositive det F"):
+        fb.exact_gradient(zero, m, p, model)
+    ident = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    with pytest.raises(fb.InadmissibleStateError,
+                       match=f"perturbed state inadmissible at dof {int(g['fd_bad_dof_eps1'])}$"):
+        fb.numeric_gradient(ident, m, p, model, eps=1.0)
+    # the context recovers after an error
+    ge = fb.exact_gradient(g["v"], m, p, model)
+    assert _grel(ge, g["g_exact"]) < G_TOL
+
+
+def test_density_plugin_rows(rng):
+    """models.py batch functions on the GPU vs the oracle restatement."""
+    for dim in (2, 3):
+        mats = np.eye(dim)[None] + 0.2 * rng.normal(size=(500, dim, dim))
+        F = [[mats[:, j, m].copy() for m in range(dim)] for j in range(dim)]
+        det = O.det_batch(F)
+        for j in range(dim):
+            F[j][j][det <= 0.05] += 1.0
+        prm = fb.ElasticParams(E=2e8, nu=0.3)
+        np.testing.assert_array_equal(fb.models.batch_determinant(F), O.det_batch(F))
+        cof = fb.models.batch_cofactor(F)
+        ocof = O.cof_batch(F)
+        for j in range(dim):
+            for m in range(dim):
+                np.testing.assert_array_equal(cof[j][m], ocof[j][m])
+        np.testing.assert_allclose(fb.models.neo_hookean_density(F, prm), O.nh_W(F, prm),
+                                   rtol=1e-13)
+        dW, odW = fb.models.neo_hookean_ddensity(F, prm), O.nh_dW(F, prm)
+        for j in range(dim):
+            for m in range(dim):
+                np.testing.assert_array_equal(dW[j][m], odW[j][m])
+    G = [[np.array([3.0]), np.array([4.0])]]
+    assert fb.models.p_laplacian_density(G, fb.PLaplaceParams(3.0))[0] == pytest.approx(125 / 3)
+    Z = fb.models.p_laplacian_ddensity([[np.zeros(2), np.zeros(2)]], fb.PLaplaceParams(1.5))
+    assert (Z[0][0] == 0).all() and (Z[0][1] == 0).all()
+    with pytest.raises(fb.InadmissibleStateError):
+        fb.models.neo_hookean_ddensity([[np.array([-1.0]), np.array([0.0])],
+                                        [np.array([0.0]), np.array([1.0])]], prm)
+
+
+# ---------------------------------------------------------------- larger meshes vs oracle
+@pytest.mark.parametrize("kind,size", [("lshape", 6), ("rect", (256, 128)), ("beam", (24, 12, 12))])
+def test_mid_size_vs_oracle(kind, size):
+    if kind == "lshape":
+        pr = problems.lshape(size, 3.0, seed=7, keep=True)
+        om, omodel, b, v = O.problem_lshape(size, 3.0, seed=7)
+        eps = 1e-6
+    elif kind == "rect":
+        pr = problems.rect(*size, seed=7, keep=True)
+        om, omodel, b, v = O.problem_rect(*size, seed=7)
+        eps = 1e-8
+    else:
+        pr = problems.beam(*size, seed=7, keep=True)
+        om, omodel, b, v = O.problem_beam(*size, seed=7)
+        eps = 1e-8
+    np.testing.assert_array_equal(pr.v.cpu().numpy(), v)
+    op = O.OPatches(np.diff(pr.meta["p_prefix"].cpu().numpy(), prepend=0),
+                    pr.meta["p_elems"].cpu().numpy(), pr.meta["p_slot"].cpu().numpy(),
+                    pr.meta["p_prefix"].cpu().numpy())
+    ref_p = O.build_patches(om)
+    np.testing.assert_array_equal(op.elems, ref_p.elems)
+    np.testing.assert_array_equal(op.slot, ref_p.slot)
+    # feed the oracle's b so that J / g compare the evaluation only
+    bd = torch.from_numpy(b).cuda()
+    J = float(pr.dm.energy(pr.v, pr.model, bd)[0])
+    Jo = O.energy(v, om, omodel, b)[0]
+    assert _rel(J, Jo) < J_TOL
+    gg = pr.dm.exact_gradient(pr.v, pr.model, bd).cpu().numpy()
+    go = O.exact_gradient(v, om, ref_p, omodel, b)
+    assert _grel(gg, go) < G_TOL
+    J2 = torch.empty(3, dtype=torch.float64, device="cuda")
+    gg2 = pr.dm.exact_gradient(pr.v, pr.model, bd, J=J2).cpu().numpy()
+    assert _rel(float(J2[0]), Jo) < J_TOL and _grel(gg2, go) < G_TOL
+    gn = pr.dm.numeric_gradient(pr.v, pr.model, bd, eps).cpu().numpy()
+    pr.dm.check()
+    gd, scale = O.numeric_gradient_direct(v, om, ref_p, omodel, b, eps)
+    assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
+
+
+def test_determinism_bitwise():
+    pr = problems.beam(16, 8, 8, seed=3)
+    a = pr.dm.exact_gradient(pr.v, pr.model, pr.b).clone()
+    Ja = pr.dm.energy(pr.v, pr.model, pr.b).clone()
+    for _ in range(3):
+        assert torch.equal(pr.dm.exact_gradient(pr.v, pr.model, pr.b), a)
+        assert torch.equal(pr.dm.energy(pr.v, pr.model, pr.b), Ja)
