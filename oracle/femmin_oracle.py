@@ -176,9 +176,13 @@ KUHN_PERMS = list(itertools.permutations(range(3)))
 KUHN_FLIP = [False, True, True, False, False, True]
 
 
-def beam_mesh(nx, ny, nz, x0, x1, y0, y1, z0, z1, level=-1) -> OMesh:
-    """mesh.py:125-174 with free (nx, ny, nz) and box bounds."""
-    xs = np.linspace(x0, x1, nx + 1)
+def beam_mesh(nx, ny, nz, x0, x1, y0, y1, z0, z1, level=-1, ix0=0, ix1=None) -> OMesh:
+    """mesh.py:125-174 with free (nx, ny, nz) and box bounds; optionally only
+    the x1-slab of cubes [ix0, ix1) of that grid (slab-local numbering, global
+    linspace coordinates)."""
+    ix1 = nx if ix1 is None else ix1
+    xs = np.linspace(x0, x1, nx + 1)[ix0:ix1 + 1]
+    nx = ix1 - ix0
     ys = np.linspace(y0, y1, ny + 1)
     zs = np.linspace(z0, z1, nz + 1)
     N = (nx + 1) * (ny + 1) * (nz + 1)
@@ -481,7 +485,7 @@ def exact_gradient(v, mesh: OMesh, P: OPatches, model, b=None):
     return g
 
 
-def _perturbed_row_densities(v, mesh, P, model, eps):
+def _perturbed_row_densities(v, mesh, P, model, eps, with_libm=False):
     """Core of gradients.py:84-121: the d*||T|| densities for each sign
     (-eps first), with G recomputed from perturbed nodal values."""
     d, dim = model.d, mesh.dim
@@ -498,7 +502,18 @@ def _perturbed_row_densities(v, mesh, P, model, eps):
         G = grad_field(dphi_rows, veps)
         GG = [[np.concatenate([G[j][m] if blk == j else Fp[j][m] for blk in range(d)])
                for m in range(dim)] for j in range(d)]             # gradients.py:35-51
-        out.append(model.density(GG))
+        W = model.density(GG)
+        if with_libm:
+            # magnitude of the libm-evaluated term of W (its ulp differs between
+            # numpy and CUDA): 2 C1 |log det| for Neo-Hookean, |W| for p-Laplace
+            if model.kind == "nh":
+                det = det_batch(GG)
+                L = 2.0 * model.params.C1 * np.abs(np.log(np.where(det > 0, det, 1.0)))
+            else:
+                L = np.abs(W)
+            out.append((W, L))
+        else:
+            out.append(W)
     return out
 
 
@@ -526,19 +541,21 @@ def numeric_gradient(v, mesh: OMesh, P: OPatches, model, b=None, eps=1e-8):
 def numeric_gradient_direct(v, mesh: OMesh, P: OPatches, model, b=None, eps=1e-8):
     """Same central differences with per-patch sequential sums instead of the
     global cumsum; also returns a per-dof roundoff scale
-    u * sum_patch vol*(|W+|+|W-|) / (2 eps) used as the FD parity bound."""
+    u * sum_patch vol*(|W+| + |W-| + L+ + L-) / (2 eps) used as the FD parity
+    bound, L the magnitude of the libm-evaluated term (log / pow)."""
     d = model.d
-    Wm, Wp = _perturbed_row_densities(v, mesh, P, model, eps)
+    (Wm, Lm), (Wp, Lp) = _perturbed_row_densities(v, mesh, P, model, eps, with_libm=True)
     T = P.total_rows
     vol = mesh.volumes[P.elems]
     starts = np.concatenate([[0], P.prefix[:-1]])
     Sp, Sm, Sa = [], [], []
     for j in range(d):
-        wp = vol * Wp[j * T:(j + 1) * T]
-        wm = vol * Wm[j * T:(j + 1) * T]
+        sl = slice(j * T, (j + 1) * T)
+        wp = vol * Wp[sl]
+        wm = vol * Wm[sl]
         Sp.append(np.add.reduceat(wp, starts))
         Sm.append(np.add.reduceat(wm, starts))
-        Sa.append(np.add.reduceat(np.abs(wp) + np.abs(wm), starts))
+        Sa.append(np.add.reduceat(np.abs(wp) + np.abs(wm) + vol * (Lp[sl] + Lm[sl]), starts))
     g = _rows_to_dofs((np.concatenate(Sp) - np.concatenate(Sm)) / (2.0 * eps), mesh, d)
     scale = _rows_to_dofs(np.concatenate(Sa) * np.finfo(float).eps / (2.0 * eps), mesh, d)
     if b is not None:
@@ -621,10 +638,22 @@ def problem_rect(nx: int, ny: int, seed: int = 2109):
     return m, model, b, field_nh(m, seed, 1e-2 * (2.0 / nx))
 
 
-def problem_beam(nx: int, ny: int, nz: int, seed: int = 2109, lx=2.0, ly=1.0, lz=1.0):
-    """Configs 4/5: [0,lx]x[0,ly]x[0,lz] Kuhn beam, NH 3D, f = (0,0,-2.5e7)."""
-    m = beam_mesh(nx, ny, nz, 0.0, lx, 0.0, ly, 0.0, lz)
+def problem_beam(nx: int, ny: int, nz: int, seed: int = 2109, lx=2.0, ly=1.0, lz=1.0,
+                 ix0: int = 0, ix1: int | None = None):
+    """Configs 4/5: [0,lx]x[0,ly]x[0,lz] Kuhn beam, NH 3D, f = (0,0,-2.5e7).
+    With (ix0, ix1): the slab of one rank of the x1 partition; its
+    load vector sums only the slab's elements and the field draws the global
+    dof hash."""
+    ix1 = nx if ix1 is None else ix1
+    m = beam_mesh(nx, ny, nz, 0.0, lx, 0.0, ly, 0.0, lz, ix0=ix0, ix1=ix1)
     m = mark_dirichlet(m, fixed_mask(m, [(left_face, None)], 3), 3)
     b = load_vector(m, (0.0, 0.0, -2.5e7), 3)
     model = Model("nh", LameParams.from_E_nu_lambda(E_MOD, NU), 3)
-    return m, model, b, field_nh(m, seed, 1e-2 * (lx / nx))
+    nxl = ix1 - ix0
+    local = np.arange(m.nn, dtype=np.int64)
+    gid = (local % (nxl + 1) + ix0) + (nx + 1) * (local // (nxl + 1))
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    dof = m.dofs_minim
+    gdof = 3 * gid[dof // 3] + dof % 3
+    v[dof] = v[dof] + 1e-2 * (lx / nx) * (2.0 * uniform01(seed, gdof) - 1.0)
+    return m, model, b, v
