@@ -2,16 +2,18 @@
 // (mesh.py:31-53, patches.py:22-71) and exposes the evaluation entry points of
 // include/femmin_b200.h.
 //
-// Context build (all on the GPU, CUB radix sorts, deterministic):
-//   1. free-node ranks, output offsets of the restricted gradient
+// Context build (GPU, CUB radix sorts, deterministic; host only sees counts):
+//   1. free-node ranks and output offsets of the restricted gradient
 //      (gradients.py:68-74 _blocks_to_dofs order);
-//   2. node tiles: free nodes bucketed into spatial boxes (box edge = k * mesh
-//      width, width from the mean element measure), boxes split to <= tile_nodes;
-//   3. element owner tile = tile of its first free node (orphans: no free node);
-//      storage order sorted by (owner tile, element) -> 128-byte records;
-//   4. tile element lists = union of the tile nodes' patches (patches.py:37-71
-//      rows), slot masks OR-reduced by key, J flag where the tile owns the element;
-//   5. node entries (te_local << 2 | slot) in patch order (ascending element).
+//   2. node tiles: free nodes bucketed into spatial boxes (edge = k * mesh width,
+//      width from the mean element measure), boxes in Morton order, split to
+//      <= 256 nodes and <= entry-cap node entries;
+//   3. element owner tile = tile of its first free node (orphans: none);
+//      storage order sorted by (owner tile, element) -> element records;
+//   4. tile element lists = own elements (contiguous storage) + halo elements
+//      (union of the tile nodes' patches, patches.py:37-71 rows, minus own),
+//      slot masks OR-reduced by key;
+//   5. node descriptors and entries (te_local << 2 | slot) sorted by te_local.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -27,6 +29,8 @@ namespace fm {
 
 static thread_local std::string g_err;
 void set_error(const std::string &m) { g_err = m; }
+
+constexpr int ENTRY_CAP_DEFAULT = 8192;  // node entries per tile (16 KB of shared memory)
 
 // ---------------------------------------------------------------- kernels
 __global__ void k_ranks(int64_t nfree, int d, const int64_t *nodes_minim, const uint8_t *fixed,
@@ -51,7 +55,7 @@ __device__ __forceinline__ unsigned long long ord_bits(double x) {
   unsigned long long u = __double_as_longlong(x);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
-__host__ __device__ inline double from_ord(unsigned long long u) {
+static inline double from_ord(unsigned long long u) {
   unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
   double x;
   memcpy(&x, &b, 8);
@@ -76,17 +80,36 @@ __global__ void k_bbox(int64_t n, int dim, const int64_t *nodes, const double *X
   }
 }
 
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {  // 21 bits -> every 3rd bit
+  x &= 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
 __global__ void k_box_keys(int64_t nfree, int dim, const int64_t *nodes, const double *X,
                            double x0, double y0, double z0, double ex, double ey, double ez,
-                           double hh, int64_t nbx, int64_t nby, uint64_t *keys, int32_t *vals) {
+                           double hh, uint64_t *keys, int32_t *vals) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nfree;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t node = nodes[r];
-    int64_t ix = (int64_t)floor((X[node * dim] - x0 + hh) / ex);
-    int64_t iy = (int64_t)floor((X[node * dim + 1] - y0 + hh) / ey);
-    int64_t iz = dim == 3 ? (int64_t)floor((X[node * dim + 2] - z0 + hh) / ez) : 0;
-    keys[r] = (uint64_t)(ix + nbx * (iy + nby * iz));
+    uint64_t ix = (uint64_t)floor((X[node * dim] - x0 + hh) / ex);
+    uint64_t iy = (uint64_t)floor((X[node * dim + 1] - y0 + hh) / ey);
+    uint64_t iz = dim == 3 ? (uint64_t)floor((X[node * dim + 2] - z0 + hh) / ez) : 0;
+    keys[r] = spread3(ix) | (spread3(iy) << 1) | (spread3(iz) << 2);  // Morton order
     vals[r] = (int32_t)r;
+  }
+}
+
+__global__ void k_sorted_lengths(int64_t n, const int32_t *ranks, const int64_t *prefix,
+                                 int32_t *lens) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int r = ranks[k];
+    lens[k] = (int32_t)(prefix[r] - (r ? prefix[r - 1] : 0));
   }
 }
 
@@ -105,8 +128,7 @@ __global__ void k_tile_of_pos(int64_t ntn, int n_tiles, const int32_t *tile_node
 
 __global__ void k_owner(int64_t ne, int nv, const int64_t *conn, const int32_t *rank_of,
                         const int32_t *tile_of_rank, int n_tiles, uint32_t *okey,
-                        int32_t *oval, int32_t *owner_of, unsigned long long *n_orph) {
-  unsigned long long cnt = 0;
+                        int32_t *oval, int32_t *owner_of) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
        e += (int64_t)gridDim.x * blockDim.x) {
     int own = n_tiles;
@@ -117,18 +139,28 @@ __global__ void k_owner(int64_t ne, int nv, const int64_t *conn, const int32_t *
         break;
       }
     }
-    cnt += own == n_tiles;
     okey[e] = (uint32_t)own;
     oval[e] = (int32_t)e;
     owner_of[e] = own;
   }
-  if (cnt) atomicAdd(n_orph, cnt);
 }
 
 __global__ void k_inverse(int64_t n, const int32_t *perm, int32_t *inv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     inv[perm[i]] = (int32_t)i;
+}
+
+// first index in the sorted array with value >= key, for keys t = 0..n
+__global__ void k_lower_bounds_u32(int n, int64_t len, const uint32_t *sorted, int32_t *out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n; t += gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sorted[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
+    }
+    out[t] = (int32_t)lo;
+  }
 }
 
 template <int DIM>
@@ -158,15 +190,18 @@ __global__ void k_build_aos(int64_t ne, const int32_t *s2o, const int64_t *conn,
   }
 }
 
+// (tile, halo?, element) keys of every patch row: te order = own first, then halo
 __global__ void k_pair_keys(int64_t nfree, const int64_t *prefix, const int64_t *elems,
-                            const int64_t *slot, const int32_t *tile_of_rank, uint64_t *keys,
-                            uint8_t *vals) {
+                            const int64_t *slot, const int32_t *tile_of_rank,
+                            const int32_t *owner_of, uint64_t *keys, uint8_t *vals) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nfree;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = r ? prefix[r - 1] : 0, z = prefix[r];
-    uint64_t t = (uint64_t)tile_of_rank[r] << 32;
+    const int t = tile_of_rank[r];
     for (int64_t q = a; q < z; ++q) {
-      keys[q] = t | (uint64_t)elems[q];
+      const int64_t e = elems[q];
+      const uint64_t halo = owner_of[e] != t;
+      keys[q] = ((uint64_t)t << 33) | (halo << 32) | (uint64_t)e;
       vals[q] = (uint8_t)(1u << slot[q]);
     }
   }
@@ -176,72 +211,70 @@ struct OrOp {
   __device__ __forceinline__ uint8_t operator()(uint8_t a, uint8_t b) const { return a | b; }
 };
 
-__global__ void k_tile_elems(int64_t M, const uint64_t *ukeys, const uint8_t *umask,
-                             const int32_t *o2s, const int32_t *owner_of, int32_t *tile_elems,
-                             uint8_t *flags) {
+// per tile: [ptr[t], split[t]) own pairs, [split[t], ptr[t+1]) halo pairs
+__global__ void k_tile_bounds(int n_tiles, int64_t M, const uint64_t *ukeys, int32_t *ptr,
+                              int32_t *split) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n_tiles; t += gridDim.x * blockDim.x) {
+    for (int w = 0; w < 2; ++w) {
+      const uint64_t key = ((uint64_t)t << 33) | ((uint64_t)w << 32);
+      int64_t lo = 0, hi = M;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ukeys[mid] < key) lo = mid + 1; else hi = mid;
+      }
+      (w ? split : ptr)[t] = (int32_t)lo;
+    }
+  }
+}
+
+__global__ void k_halo_ids(int64_t M, const uint64_t *ukeys, const int32_t *split,
+                           const int32_t *halo_begin, const int32_t *o2s, int32_t *halo_ids) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = ukeys[i];
-    int t = (int)(k >> 32);
-    int64_t e = (int64_t)(k & 0xffffffffull);
-    tile_elems[i] = o2s[e];
-    flags[i] = umask[i] | (owner_of[e] == t ? FLAG_J : 0);
+    const uint64_t k = ukeys[i];
+    if (!((k >> 32) & 1)) continue;
+    const int t = (int)(k >> 33);
+    const int64_t e = (int64_t)(k & 0xffffffffull);
+    halo_ids[halo_begin[t] + (i - split[t])] = o2s[e];
   }
 }
 
-__global__ void k_tile_elem_ptr(int n_tiles, int64_t M, const uint64_t *ukeys, int32_t *ptr) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n_tiles; t += gridDim.x * blockDim.x) {
-    uint64_t key = (uint64_t)t << 32;
-    int64_t lo = 0, hi = M;  // first index with ukeys >= key
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (ukeys[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    ptr[t] = (int32_t)lo;
-  }
-}
-
-__global__ void k_orphans(int64_t n_orph, int64_t first_storage, int64_t M, int32_t *tile_elems,
-                          uint8_t *flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_orph;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    tile_elems[M + i] = (int32_t)(first_storage + i);
-    flags[M + i] = FLAG_J;
-  }
-}
-
-__global__ void k_entry_lens(int64_t ntn, const int32_t *tile_node_rank, const int64_t *prefix,
-                             int32_t *lens) {
+__global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const int32_t *tile_of_rank,
+                            const int64_t *prefix, const int64_t *elems, const int64_t *slot,
+                            const int32_t *owner_of, const uint64_t *ukeys, const int32_t *ptr,
+                            const int32_t *entry_abs, const int32_t *entry_off,
+                            const int32_t *free_node, const int32_t *free_out,
+                            const uint8_t *free_mask, uint16_t *entries, int4 *desc,
+                            unsigned long long *overflow) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
        k += (int64_t)gridDim.x * blockDim.x) {
-    int r = tile_node_rank[k];
-    lens[k] = (int32_t)(prefix[r] - (r ? prefix[r - 1] : 0));
-  }
-}
-
-__global__ void k_entries(int64_t ntn, const int32_t *tile_node_rank, const int32_t *tile_of_rank,
-                          const int64_t *prefix, const int64_t *elems, const int64_t *slot,
-                          const uint64_t *ukeys, const int32_t *tile_elem_ptr,
-                          const int32_t *entry_ptr, uint16_t *entries,
-                          unsigned long long *overflow) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    int r = tile_node_rank[k];
-    int t = tile_of_rank[r];
-    int64_t a = r ? prefix[r - 1] : 0, z = prefix[r];
-    int64_t lo0 = tile_elem_ptr[t], hi0 = tile_elem_ptr[t + 1];
-    int32_t o = entry_ptr[k];
+    const int r = tile_node_rank[k];
+    const int t = tile_of_rank[r];
+    const int64_t a = r ? prefix[r - 1] : 0, z = prefix[r];
+    const int64_t lo0 = ptr[t], hi0 = ptr[t + 1];
+    uint16_t *out = entries + entry_abs[k];
+    int n = 0;
     for (int64_t q = a; q < z; ++q) {
-      uint64_t key = ((uint64_t)t << 32) | (uint64_t)elems[q];
+      const int64_t e = elems[q];
+      const uint64_t key = ((uint64_t)t << 33) | ((uint64_t)(owner_of[e] != t) << 32) | (uint64_t)e;
       int64_t lo = lo0, hi = hi0;
       while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
         if (ukeys[mid] < key) lo = mid + 1; else hi = mid;
       }
-      int64_t te = lo - lo0;
+      const int64_t te = lo - lo0;
       if (te >= MAX_TILE_ELEMS || lo >= hi0 || ukeys[lo] != key) atomicAdd(overflow, 1ull);
-      entries[o++] = (uint16_t)((te << 2) | slot[q]);
+      uint16_t v = (uint16_t)((te << 2) | slot[q]);
+      int p = n++;  // insertion sort by te (entries of one node are few)
+      while (p > 0 && out[p - 1] > v) {
+        out[p] = out[p - 1];
+        --p;
+      }
+      out[p] = v;
     }
+    const int fo = free_out[r];
+    if (fo >= (1 << OUT_MASK_SHIFT)) atomicAdd(overflow, 1ull);
+    desc[k] = make_int4(entry_off[k], n, free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
   }
 }
 
@@ -277,6 +310,16 @@ static int check_model(const fm_ctx *c, const fm_model *m) {
   return FM_OK;
 }
 
+template <class F> static cudaError_t cub_call(F f, cudaStream_t s) {
+  size_t bytes = 0;
+  cudaError_t e = f(nullptr, bytes);
+  if (e != cudaSuccess) return e;
+  Scratch tmp;
+  e = tmp.alloc(bytes, s);
+  if (e != cudaSuccess) return e;
+  return f(tmp.p, bytes);
+}
+
 struct TimedLaunch {
   fm_ctx *c;
   cudaStream_t s;
@@ -298,15 +341,15 @@ using namespace fm;
 
 extern "C" {
 
+const char *fm_last_error(void) { return g_err.c_str(); }
+int fm_version(void) { return 1; }
+
 int fm_ctx_time_next(fm_ctx *c, void *ev_start, void *ev_stop) {
   FM_ARG(c, "null context");
   c->ev_start = reinterpret_cast<cudaEvent_t>(ev_start);
   c->ev_stop = reinterpret_cast<cudaEvent_t>(ev_stop);
   return FM_OK;
 }
-
-const char *fm_last_error(void) { return g_err.c_str(); }
-int fm_version(void) { return 1; }
 
 int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, fm_ctx **out) {
   FM_ARG(m && out, "null argument");
@@ -330,23 +373,29 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->ne = m->ne;
   c->nfree = m->nfree;
   c->p_total = m->p_total;
-  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : (dim == 3 ? 256 : 512);
-  NT = std::max(32, std::min(512, NT / 32 * 32));
-  int box[3] = {dim == 3 ? 8 : 32, dim == 3 ? 8 : 16, dim == 3 ? 4 : 1};
+  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : CONSUMERS;
+  NT = std::max(32, std::min(CONSUMERS, NT));
+  int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? 8 : 16, dim == 3 ? 4 : 1};
   if (tiling)
     for (int a = 0; a < 3; ++a)
       if (tiling->box[a] > 0) box[a] = tiling->box[a];
   c->tile_nodes = NT;
   const int64_t nfree = m->nfree, ne = m->ne, T = m->p_total;
   size_t &B = c->bytes;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (c->n_sm <= 0) c->n_sm = 148;
+  }
 
-#define CK(x)                                                   \
-  do {                                                          \
-    cudaError_t _e = (x);                                       \
-    if (_e != cudaSuccess) {                                    \
+#define CK(x)                                                     \
+  do {                                                            \
+    cudaError_t _e = (x);                                         \
+    if (_e != cudaSuccess) {                                      \
       set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); \
-      return fail(FM_CUDA_ERROR);                               \
-    }                                                           \
+      return fail(FM_CUDA_ERROR);                                 \
+    }                                                             \
   } while (0)
 
   // 1. ranks and output offsets ---------------------------------------------
@@ -359,34 +408,36 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     Scratch cnt;
     CK(cnt.alloc((nfree + 1) * 4, s));
     CK(cudaMemsetAsync(cnt.p, 0, (nfree + 1) * 4, s));
-    k_ranks<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, d, m->nodes_minim, m->fixed, c->rank_of,
-                                                 c->free_node, c->free_mask, cnt.as<int32_t>());
+    if (nfree)
+      k_ranks<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, d, m->nodes_minim, m->fixed,
+                                                   c->rank_of, c->free_node, c->free_mask,
+                                                   cnt.as<int32_t>());
     CK(cudaGetLastError());
-    size_t bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.as<int32_t>(), c->free_out, nfree + 1,
-                                     s));
-    Scratch tmp;
-    CK(tmp.alloc(bytes, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.as<int32_t>(), c->free_out, nfree + 1, s));
+    int32_t *cp = cnt.as<int32_t>();
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, cp, c->free_out, nfree + 1, s);
+    }, s));
     int32_t nfd = 0;
     CK(cudaMemcpyAsync(&nfd, c->free_out + nfree, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->nfree_dofs = nfd;
   }
 
-  // 2. node tiles -----------------------------------------------------------
-  std::vector<int32_t> h_tnp;  // tile node ptr (host)
-  Scratch s_tnr;               // sorted ranks = tile_node_rank
+  // 2. node tiles (Morton-ordered boxes) -------------------------------------
+  std::vector<int32_t> h_tnp{0};      // tile node ptr
+  std::vector<int32_t> h_lens;        // patch length per sorted node
+  Scratch s_tnr;                      // sorted ranks = tile node order
+  CK(s_tnr.alloc(std::max<int64_t>(nfree, 1) * 4, s));
   if (nfree > 0) {
     double volsum = 0.0;
     {
-      Scratch out, tmp;
-      CK(out.alloc(8, s));
-      size_t bytes = 0;
-      CK(cub::DeviceReduce::Sum(nullptr, bytes, m->volumes, out.as<double>(), ne, s));
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceReduce::Sum(tmp.p, bytes, m->volumes, out.as<double>(), ne, s));
-      CK(cudaMemcpyAsync(&volsum, out.p, 8, cudaMemcpyDeviceToHost, s));
+      Scratch o;
+      CK(o.alloc(8, s));
+      const double *vp = m->volumes;
+      double *op = o.as<double>();
+      CK(cub_call([&](void *t, size_t &b) { return cub::DeviceReduce::Sum(t, b, vp, op, ne, s); },
+                  s));
+      CK(cudaMemcpyAsync(&volsum, o.p, 8, cudaMemcpyDeviceToHost, s));
     }
     unsigned long long hmn[3], hmx[3];
     {
@@ -404,69 +455,63 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
     const double fact = dim == 3 ? 6.0 : 2.0;
     const double h = std::pow(fact * volsum / (double)ne, 1.0 / dim);
-    double x0[3] = {0, 0, 0}, ext[3] = {0, 0, 0}, edge[3] = {1, 1, 1};
-    int64_t nb[3] = {1, 1, 1};
+    double x0[3] = {0, 0, 0}, edge[3] = {1, 1, 1};
     for (int a = 0; a < dim; ++a) {
       x0[a] = from_ord(hmn[a]);
-      ext[a] = from_ord(hmx[a]) - x0[a];
       edge[a] = box[a] * h;
-      nb[a] = (int64_t)std::floor((ext[a] + 0.5 * h) / edge[a]) + 1;
+      double nb = std::floor((from_ord(hmx[a]) - x0[a] + 0.5 * h) / edge[a]) + 1;
+      if (!(nb < 2e6)) {
+        set_error("tiling box grid too large (> 2^21 boxes per axis)");
+        return fail(FM_INVALID_ARG);
+      }
     }
-    if ((double)nb[0] * nb[1] * nb[2] > 4e18) {
-      set_error("tiling box grid too large");
-      return fail(FM_INVALID_ARG);
-    }
-    Scratch keys, keys2, vals2, runs, counts, nruns;
+    Scratch keys, keys2, vals2, lens;
     CK(keys.alloc(nfree * 8, s));
     CK(keys2.alloc(nfree * 8, s));
-    CK(s_tnr.alloc(nfree * 4, s));
     CK(vals2.alloc(nfree * 4, s));
-    k_box_keys<<<grid_for(nfree, 256), 256, 0, s>>>(
-        nfree, dim, m->nodes_minim, m->coords, x0[0], x0[1], x0[2], edge[0], edge[1], edge[2],
-        0.5 * h, nb[0], nb[1], keys.as<uint64_t>(), s_tnr.as<int32_t>());
+    CK(lens.alloc(nfree * 4, s));
+    k_box_keys<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, dim, m->nodes_minim, m->coords, x0[0],
+                                                    x0[1], x0[2], edge[0], edge[1], edge[2],
+                                                    0.5 * h, keys.as<uint64_t>(),
+                                                    s_tnr.as<int32_t>());
     CK(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(keys.as<uint64_t>(), keys2.as<uint64_t>());
     cub::DoubleBuffer<int32_t> dv(s_tnr.as<int32_t>(), vals2.as<int32_t>());
-    int end_bit = std::max(1, bits_for((uint64_t)(nb[0] * nb[1] * nb[2])));
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, nfree, 0, end_bit, s));
-    {
-      Scratch tmp;
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, dk, dv, nfree, 0, end_bit, s));
-    }
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, nfree, 0, 63, s);
+    }, s));
     if (dv.Current() != s_tnr.as<int32_t>())
       CK(cudaMemcpyAsync(s_tnr.p, dv.Current(), nfree * 4, cudaMemcpyDeviceToDevice, s));
-    CK(runs.alloc(nfree * 8, s));
-    CK(counts.alloc(nfree * 4, s));
-    CK(nruns.alloc(8, s));
-    bytes = 0;
-    CK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, dk.Current(), runs.as<uint64_t>(),
-                                          counts.as<int32_t>(), nruns.as<int32_t>(), nfree, s));
-    {
-      Scratch tmp;
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, dk.Current(), runs.as<uint64_t>(),
-                                            counts.as<int32_t>(), nruns.as<int32_t>(), nfree,
-                                            s));
-    }
-    int32_t nr = 0;
-    CK(cudaMemcpyAsync(&nr, nruns.p, 4, cudaMemcpyDeviceToHost, s));
+    k_sorted_lengths<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, s_tnr.as<int32_t>(),
+                                                          m->p_prefix, lens.as<int32_t>());
+    CK(cudaGetLastError());
+    std::vector<uint64_t> hkeys(nfree);
+    h_lens.resize(nfree);
+    CK(cudaMemcpyAsync(hkeys.data(), dk.Current(), nfree * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_lens.data(), lens.p, nfree * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    std::vector<int32_t> cnts(nr);
-    CK(cudaMemcpy(cnts.data(), counts.p, (size_t)nr * 4, cudaMemcpyDeviceToHost));
-    h_tnp.push_back(0);
-    int64_t pos = 0;
-    for (int32_t cb : cnts) {
-      int k = (cb + NT - 1) / NT;
-      for (int q = 0; q < k; ++q) {
-        int64_t sz = (int64_t)cb * (q + 1) / k - (int64_t)cb * q / k;
-        pos += sz;
-        h_tnp.push_back((int32_t)pos);
+    // split boxes into tiles of <= NT nodes and <= ENTRY_CAP entries
+    int64_t i = 0;
+    while (i < nfree) {
+      int64_t j = i;
+      while (j < nfree && hkeys[j] == hkeys[i]) ++j;
+      const int64_t cnt = j - i;
+      int64_t ent = 0;
+      for (int64_t k = i; k < j; ++k) ent += h_lens[k];
+      int64_t pieces = std::max<int64_t>((cnt + NT - 1) / NT,
+                                         (ent + ENTRY_CAP_DEFAULT - 1) / ENTRY_CAP_DEFAULT);
+      for (;; ++pieces) {
+        bool ok = true;
+        for (int64_t q = 0; q < pieces && ok; ++q) {
+          int64_t a = i + cnt * q / pieces, z = i + cnt * (q + 1) / pieces, e2 = 0;
+          for (int64_t k = a; k < z; ++k) e2 += h_lens[k];
+          ok = (z - a) <= NT && e2 <= ENTRY_CAP_DEFAULT;
+        }
+        if (ok) break;
       }
+      for (int64_t q = 1; q <= pieces; ++q) h_tnp.push_back((int32_t)(i + cnt * q / pieces));
+      i = j;
     }
-  } else {
-    h_tnp.push_back(0);
   }
   const int n_tiles = (int)h_tnp.size() - 1;
   c->n_tiles = n_tiles;
@@ -474,54 +519,46 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   for (int t = 0; t < n_tiles; ++t)
     c->max_tile_nodes = std::max(c->max_tile_nodes, h_tnp[t + 1] - h_tnp[t]);
 
-  Scratch s_tor;  // tile_of_rank
+  Scratch s_tor, d_tnp;  // tile_of_rank, tile node ptr
   CK(s_tor.alloc(std::max<int64_t>(nfree, 1) * 4, s));
-  CK(dmalloc(&c->tile_node_rank, nfree, &B));
-  if (nfree) CK(cudaMemcpyAsync(c->tile_node_rank, s_tnr.p, nfree * 4, cudaMemcpyDeviceToDevice, s));
+  CK(d_tnp.alloc(h_tnp.size() * 4, s));
+  CK(cudaMemcpyAsync(d_tnp.p, h_tnp.data(), h_tnp.size() * 4, cudaMemcpyHostToDevice, s));
+  if (nfree)
+    k_tile_of_pos<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, n_tiles, d_tnp.as<int32_t>(),
+                                                       s_tnr.as<int32_t>(), s_tor.as<int32_t>());
+  CK(cudaGetLastError());
 
   // 3. element owners and storage order ---------------------------------------
-  Scratch okey, okey2, oval2, owner_of, o2s, cnt_orph;
+  Scratch okey, okey2, oval2, owner_of, o2s, own_ptr;
   CK(okey.alloc(ne * 4, s));
   CK(okey2.alloc(ne * 4, s));
   CK(oval2.alloc(ne * 4, s));
   CK(owner_of.alloc(ne * 4, s));
   CK(o2s.alloc(ne * 4, s));
-  CK(cnt_orph.alloc(8, s));
+  CK(own_ptr.alloc((n_tiles + 2) * 4, s));
   CK(dmalloc(&c->storage_to_orig, ne, &B));
-  CK(cudaMemsetAsync(cnt_orph.p, 0, 8, s));
-  {
-    Scratch d_tnp;
-    CK(d_tnp.alloc(h_tnp.size() * 4, s));
-    CK(cudaMemcpyAsync(d_tnp.p, h_tnp.data(), h_tnp.size() * 4, cudaMemcpyHostToDevice, s));
-    if (nfree)
-      k_tile_of_pos<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, n_tiles, d_tnp.as<int32_t>(),
-                                                         c->tile_node_rank, s_tor.as<int32_t>());
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
-  }
   k_owner<<<grid_for(ne, 256), 256, 0, s>>>(ne, nv, m->conn, c->rank_of, s_tor.as<int32_t>(),
-                                            n_tiles, okey.as<uint32_t>(),
-                                            c->storage_to_orig, owner_of.as<int32_t>(),
-                                            cnt_orph.as<unsigned long long>());
+                                            n_tiles, okey.as<uint32_t>(), c->storage_to_orig,
+                                            owner_of.as<int32_t>());
   CK(cudaGetLastError());
   {
     cub::DoubleBuffer<uint32_t> dk(okey.as<uint32_t>(), okey2.as<uint32_t>());
     cub::DoubleBuffer<int32_t> dv(c->storage_to_orig, oval2.as<int32_t>());
-    int end_bit = std::max(1, bits_for((uint64_t)n_tiles));
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, ne, 0, end_bit, s));
-    Scratch tmp;
-    CK(tmp.alloc(bytes, s));
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, dk, dv, ne, 0, end_bit, s));
+    const int end_bit = std::max(1, bits_for((uint64_t)n_tiles));
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, ne, 0, end_bit, s);
+    }, s));
     if (dv.Current() != c->storage_to_orig)
       CK(cudaMemcpyAsync(c->storage_to_orig, dv.Current(), ne * 4, cudaMemcpyDeviceToDevice, s));
+    k_lower_bounds_u32<<<grid_for(n_tiles + 2, 256), 256, 0, s>>>(n_tiles + 1, ne, dk.Current(),
+                                                                  own_ptr.as<int32_t>());
+    CK(cudaGetLastError());
   }
   k_inverse<<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, o2s.as<int32_t>());
   CK(cudaGetLastError());
-  unsigned long long n_orph = 0;
-  CK(cudaMemcpyAsync(&n_orph, cnt_orph.p, 8, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> h_own(n_tiles + 2);
+  CK(cudaMemcpyAsync(h_own.data(), own_ptr.p, (n_tiles + 2) * 4, cudaMemcpyDeviceToHost, s));
 
-  // element records
   const int rb = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
   CK(dmalloc(&c->aos, (size_t)ne * rb, &B));
   if (dim == 3)
@@ -532,9 +569,12 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
                                                      m->dphi, c->aos);
   CK(cudaGetLastError());
 
-  // 4. tile element lists -------------------------------------------------------
+  // 4. tile element lists (own + halo) ----------------------------------------
   int64_t M = 0;
-  Scratch ukeys, umask;
+  Scratch ukeys, umask, tptr, tsplit;
+  CK(tptr.alloc((n_tiles + 1) * 4, s));
+  CK(tsplit.alloc((n_tiles + 1) * 4, s));
+  std::vector<int32_t> h_ptr(n_tiles + 1, 0), h_split(n_tiles + 1, 0);
   if (nfree > 0) {
     Scratch pk, pk2, pv, pv2, nsel;
     CK(pk.alloc(T * 8, s));
@@ -542,126 +582,151 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(pv.alloc(T, s));
     CK(pv2.alloc(T, s));
     k_pair_keys<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, m->p_prefix, m->p_elems, m->p_slot,
-                                                     s_tor.as<int32_t>(), pk.as<uint64_t>(),
-                                                     pv.as<uint8_t>());
+                                                     s_tor.as<int32_t>(), owner_of.as<int32_t>(),
+                                                     pk.as<uint64_t>(), pv.as<uint8_t>());
     CK(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(pk.as<uint64_t>(), pk2.as<uint64_t>());
     cub::DoubleBuffer<uint8_t> dv(pv.as<uint8_t>(), pv2.as<uint8_t>());
-    int end_bit = 32 + bits_for((uint64_t)n_tiles);
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, T, 0, end_bit, s));
-    {
-      Scratch tmp;
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, dk, dv, T, 0, end_bit, s));
-    }
+    const int end_bit = 33 + bits_for((uint64_t)n_tiles);
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, T, 0, end_bit, s);
+    }, s));
     CK(ukeys.alloc(T * 8, s));
     CK(umask.alloc(T, s));
     CK(nsel.alloc(8, s));
-    bytes = 0;
-    CK(cub::DeviceReduce::ReduceByKey(nullptr, bytes, dk.Current(), ukeys.as<uint64_t>(),
-                                      dv.Current(), umask.as<uint8_t>(), nsel.as<int64_t>(),
-                                      OrOp(), T, s));
-    {
-      Scratch tmp;
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, dk.Current(), ukeys.as<uint64_t>(),
-                                        dv.Current(), umask.as<uint8_t>(), nsel.as<int64_t>(),
-                                        OrOp(), T, s));
-    }
+    uint64_t *uk = ukeys.as<uint64_t>();
+    uint8_t *um = umask.as<uint8_t>();
+    int64_t *ns = nsel.as<int64_t>();
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceReduce::ReduceByKey(t, b, dk.Current(), uk, dv.Current(), um, ns, OrOp(),
+                                            T, s);
+    }, s));
     CK(cudaMemcpyAsync(&M, nsel.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    k_tile_bounds<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(n_tiles, M, uk, tptr.as<int32_t>(),
+                                                             tsplit.as<int32_t>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_ptr.data(), tptr.p, (n_tiles + 1) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_split.data(), tsplit.p, (n_tiles + 1) * 4, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaStreamSynchronize(s));
-  const int OT = 4 * NT;  // orphan elements per orphan tile
-  const int n_otiles = (int)((n_orph + OT - 1) / OT);
-  c->n_tiles_all = n_tiles + n_otiles;
-  c->n_tile_elems = M + (int64_t)n_orph;
-  CK(dmalloc(&c->tile_elems, c->n_tile_elems, &B));
-  CK(dmalloc(&c->tile_flags, c->n_tile_elems, &B));
-  CK(dmalloc(&c->tile_elem_ptr, c->n_tiles_all + 1, &B));
-  CK(dmalloc(&c->tile_node_ptr, c->n_tiles_all + 1, &B));
-  if (M)
-    k_tile_elems<<<grid_for(M, 256), 256, 0, s>>>(M, ukeys.as<uint64_t>(), umask.as<uint8_t>(),
-                                                  o2s.as<int32_t>(), owner_of.as<int32_t>(),
-                                                  c->tile_elems, c->tile_flags);
-  if (n_tiles)
-    k_tile_elem_ptr<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(n_tiles, M, ukeys.as<uint64_t>(),
-                                                               c->tile_elem_ptr);
-  if (n_orph)
-    k_orphans<<<grid_for(n_orph, 256), 256, 0, s>>>((int64_t)n_orph, ne - (int64_t)n_orph, M,
-                                                    c->tile_elems, c->tile_flags);
-  CK(cudaGetLastError());
-  {
-    std::vector<int32_t> ext;
-    for (int q = 1; q <= n_otiles; ++q)
-      ext.push_back((int32_t)(M + std::min<int64_t>((int64_t)q * OT, (int64_t)n_orph)));
-    if (n_tiles == 0) ext.insert(ext.begin(), 0);
-    if (!ext.empty())
-      CK(cudaMemcpyAsync(c->tile_elem_ptr + (n_tiles ? n_tiles + 1 : 0), ext.data(),
-                         ext.size() * 4, cudaMemcpyHostToDevice, s));
-    std::vector<int32_t> tnp(h_tnp);
-    for (int q = 0; q < n_otiles; ++q) tnp.push_back(h_tnp.back());
-    CK(cudaMemcpyAsync(c->tile_node_ptr, tnp.data(), tnp.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  std::vector<int32_t> h_tep(c->n_tiles_all + 1);
-  CK(cudaMemcpy(h_tep.data(), c->tile_elem_ptr, h_tep.size() * 4, cudaMemcpyDeviceToHost));
+  const int64_t n_orph = (int64_t)ne - h_own[n_tiles];
+  // host-side tile metadata
+  std::vector<TileMeta> hm;
+  std::vector<int32_t> h_halo_begin(n_tiles + 1, 0);
+  int64_t halo_total = 0, entry_total = 0;
+  std::vector<int32_t> h_entry_off(std::max<int64_t>(nfree, 1)), h_entry_abs(std::max<int64_t>(nfree, 1));
   c->max_tile_elems = 0;
-  for (int t = 0; t < c->n_tiles_all; ++t)
-    c->max_tile_elems = std::max(c->max_tile_elems, h_tep[t + 1] - h_tep[t]);
+  c->max_tile_entries = 0;
+  int max_halo = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    TileMeta tm{};
+    tm.own_begin = h_own[t];
+    tm.own_count = h_own[t + 1] - h_own[t];
+    if (tm.own_count != h_split[t] - h_ptr[t]) {
+      set_error("internal error: owner partition and tile element lists disagree");
+      return fail(FM_CUDA_ERROR);
+    }
+    tm.halo_count = h_ptr[t + 1] - h_split[t];
+    tm.halo_begin = (int)halo_total;
+    h_halo_begin[t] = (int)halo_total;
+    halo_total += (tm.halo_count + 3) / 4 * 4;
+    tm.node_begin = h_tnp[t];
+    tm.node_count = h_tnp[t + 1] - h_tnp[t];
+    tm.entry_begin = (int)entry_total;
+    int off = 0;
+    for (int k = h_tnp[t]; k < h_tnp[t + 1]; ++k) {
+      h_entry_off[k] = off;
+      h_entry_abs[k] = (int)entry_total + off;
+      off += h_lens[k];
+    }
+    tm.entry_count = off;
+    entry_total += (off + 7) / 8 * 8;
+    tm.elem_begin = h_ptr[t];
+    hm.push_back(tm);
+    c->max_tile_elems = std::max(c->max_tile_elems, tm.own_count + tm.halo_count);
+    c->max_tile_entries = std::max(c->max_tile_entries, off);
+    max_halo = std::max(max_halo, tm.halo_count);
+  }
   if (c->max_tile_elems > MAX_TILE_ELEMS) {
     set_error("a node tile touches more than 16384 elements; use smaller tiles");
     return fail(FM_INVALID_ARG);
   }
+  const int OT = 4 * CONSUMERS;  // orphan elements per J-only tile
+  for (int64_t o = 0; o < n_orph; o += OT) {
+    TileMeta tm{};
+    tm.own_begin = (int)(h_own[n_tiles] + o);
+    tm.own_count = (int)std::min<int64_t>(OT, n_orph - o);
+    tm.halo_begin = (int)halo_total;
+    tm.node_begin = h_tnp.back();
+    tm.entry_begin = (int)entry_total;
+    tm.elem_begin = (int)M;
+    hm.push_back(tm);
+  }
+  c->n_tiles_all = (int)hm.size();
+  c->n_tile_elems = M;
+  c->entry_cap = (c->max_tile_entries + 7) / 8 * 8;
+  c->halo_cap = (max_halo + 3) / 4 * 4;
+  CK(dmalloc(&c->meta, hm.size(), &B));
+  CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
+  CK(dmalloc(&c->halo_ids, halo_total + 4, &B));
+  CK(dmalloc(&c->flags, M + 16, &B));
+  CK(dmalloc(&c->node_desc, std::max<int64_t>(nfree, 1), &B));
+  CK(dmalloc(&c->node_entries, entry_total + 8, &B));
+  c->n_node_entries = entry_total;
+  CK(cudaMemsetAsync(c->halo_ids, 0, (halo_total + 4) * 4, s));
+  CK(cudaMemsetAsync(c->node_entries, 0, (entry_total + 8) * 2, s));
+  if (M) {
+    CK(cudaMemcpyAsync(c->flags, umask.p, M, cudaMemcpyDeviceToDevice, s));
+    Scratch hb;
+    CK(hb.alloc((n_tiles + 1) * 4, s));
+    CK(cudaMemcpyAsync(hb.p, h_halo_begin.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
+    k_halo_ids<<<grid_for(M, 256), 256, 0, s>>>(M, ukeys.as<uint64_t>(), tsplit.as<int32_t>(),
+                                                 hb.as<int32_t>(), o2s.as<int32_t>(),
+                                                 c->halo_ids);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+  }
 
-  // 5. node entries -------------------------------------------------------------
-  CK(dmalloc(&c->node_entry_ptr, nfree + 1, &B));
-  CK(dmalloc(&c->node_entries, T, &B));
-  c->n_node_entries = T;
+  // 5. node descriptors and entries ---------------------------------------------
   if (nfree > 0) {
-    Scratch lens, ovf;
-    CK(lens.alloc((nfree + 1) * 4, s));
+    Scratch eoff, eabs, ovf;
+    CK(eoff.alloc(nfree * 4, s));
+    CK(eabs.alloc(nfree * 4, s));
     CK(ovf.alloc(8, s));
-    CK(cudaMemsetAsync(lens.p, 0, (nfree + 1) * 4, s));
     CK(cudaMemsetAsync(ovf.p, 0, 8, s));
-    k_entry_lens<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->tile_node_rank, m->p_prefix,
-                                                      lens.as<int32_t>());
-    size_t bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, lens.as<int32_t>(), c->node_entry_ptr,
-                                     nfree + 1, s));
-    {
-      Scratch tmp;
-      CK(tmp.alloc(bytes, s));
-      CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, lens.as<int32_t>(), c->node_entry_ptr,
-                                       nfree + 1, s));
-    }
-    k_entries<<<grid_for(nfree, 256), 256, 0, s>>>(
-        nfree, c->tile_node_rank, s_tor.as<int32_t>(), m->p_prefix, m->p_elems, m->p_slot,
-        ukeys.as<uint64_t>(), c->tile_elem_ptr, c->node_entry_ptr, c->node_entries,
-        ovf.as<unsigned long long>());
+    CK(cudaMemcpyAsync(eoff.p, h_entry_off.data(), nfree * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(eabs.p, h_entry_abs.data(), nfree * 4, cudaMemcpyHostToDevice, s));
+    k_node_desc<<<grid_for(nfree, 256), 256, 0, s>>>(
+        nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), m->p_prefix, m->p_elems, m->p_slot,
+        owner_of.as<int32_t>(), ukeys.as<uint64_t>(), tptr.as<int32_t>(), eabs.as<int32_t>(),
+        eoff.as<int32_t>(), c->free_node, c->free_out, c->free_mask, c->node_entries,
+        c->node_desc, ovf.as<unsigned long long>());
     CK(cudaGetLastError());
     unsigned long long h_ovf = 0;
     CK(cudaMemcpyAsync(&h_ovf, ovf.p, 8, cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> h_nep(nfree + 1);
-    CK(cudaMemcpyAsync(h_nep.data(), c->node_entry_ptr, (nfree + 1) * 4, cudaMemcpyDeviceToHost,
-                       s));
     CK(cudaStreamSynchronize(s));
     if (h_ovf) {
-      set_error("internal error: patch entry not found in its tile");
+      set_error("internal error: patch entry not found in its tile or output offset overflow");
       return fail(FM_CUDA_ERROR);
     }
-    c->max_tile_entries = 0;
-    for (int t = 0; t < n_tiles; ++t)
-      c->max_tile_entries = std::max(c->max_tile_entries, h_nep[h_tnp[t + 1]] - h_nep[h_tnp[t]]);
-  } else {
-    CK(cudaMemsetAsync(c->node_entry_ptr, 0, 4, s));
+  }
+
+  // pipeline depth that fits the shared memory of one SM
+  c->stages = 4;
+  while (c->stages > 2 &&
+         tile_exact_smem(dim, d, c->stages, c->entry_cap, c->halo_cap) > 227 * 1024)
+    --c->stages;
+  if (tile_exact_smem(dim, d, c->stages, c->entry_cap, c->halo_cap) > 227 * 1024) {
+    set_error("tile tables exceed shared memory; use smaller tiles");
+    return fail(FM_INVALID_ARG);
   }
 
   // scratch ------------------------------------------------------------------
   c->n_energy_blocks = 148 * 8;
   c->n_dot_blocks = 148 * 2;
-  CK(dmalloc(&c->jpart, std::max<int64_t>(c->n_tiles_all, c->n_energy_blocks), &B));
+  c->n_part = std::max(c->n_sm, c->n_energy_blocks);
+  CK(dmalloc(&c->jpart, c->n_part, &B));
   CK(dmalloc(&c->dotpart, c->n_dot_blocks, &B));
   CK(dmalloc(&c->status, 2, &B));
   unsigned long long init[2] = {0ull, ~0ull};
@@ -671,23 +736,22 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
 
   fm_ctx_stats &st = c->stats;
   st.n_tiles = n_tiles;
-  st.n_orphan_tiles = n_otiles;
-  st.tile_elems_total = c->n_tile_elems;
+  st.n_orphan_tiles = c->n_tiles_all - n_tiles;
+  st.tile_elems_total = M + n_orph;
   st.node_entries_total = c->n_node_entries;
   st.max_tile_elems = c->max_tile_elems;
   st.max_tile_entries = c->max_tile_entries;
   st.bytes_device = (int64_t)c->bytes;
-  st.redundancy = (double)c->n_tile_elems / (double)ne;
+  st.redundancy = (double)(M + n_orph) / (double)ne;
   *out = c;
   return FM_OK;
 }
 
 int fm_ctx_destroy(fm_ctx *c) {
   if (!c) return FM_OK;
-  void *ptrs[] = {c->aos,          c->tile_elem_ptr, c->tile_elems,   c->tile_node_ptr,
-                  c->tile_node_rank, c->node_entry_ptr, c->tile_flags, c->node_entries,
-                  c->free_node,    c->free_out,      c->rank_of,      c->storage_to_orig,
-                  c->free_mask,    c->jpart,         c->dotpart,      c->status};
+  void *ptrs[] = {c->aos,       c->meta,      c->halo_ids,  c->flags,   c->node_desc,
+                  c->node_entries, c->free_node, c->free_out, c->rank_of, c->storage_to_orig,
+                  c->free_mask, c->jpart,     c->dotpart,   c->status};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -733,11 +797,12 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
   const bool wj = J_out != nullptr;
-  const int nt = wj ? c->n_tiles_all : c->n_tiles;
-  if (nt > 0) {
+  TileArgs ta = c->tile_args();
+  if (!wj) ta.n_tiles_all = c->n_tiles;  // J-only orphan tiles not needed
+  const int grid = std::min(c->n_sm, std::max(1, ta.n_tiles_all));
+  if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, c->tile_args(), nt, c->tile_nodes,
-                              (size_t)c->max_tile_entries * 2 + 16, wj, true, v, b, g, c->jpart,
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->stages, wj, v, b, g, c->jpart,
                               c->status, ma, s));
     c->launches++;
   }
@@ -748,7 +813,7 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
       nd = c->n_dot_blocks;
       c->launches++;
     }
-    FM_CUDA(launch_finalize(c->jpart, nt, c->dotpart, nd, J_out, s));
+    FM_CUDA(launch_finalize(c->jpart, ta.n_tiles_all > 0 ? grid : 0, c->dotpart, nd, J_out, s));
     c->launches++;
   }
   return FM_OK;
@@ -765,8 +830,7 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   ModelArgs ma = model_args(model);
   TimedLaunch tl(c, s);
   FM_CUDA(launch_tile_fd(c->dim, model->kind, c->tile_args(), c->n_tiles, c->tile_nodes,
-                         (size_t)c->max_tile_entries * 2 + 16, v, b, eps, g, c->status + 1, ma,
-                         s));
+                         (size_t)c->entry_cap * 2 + 16, v, b, eps, g, c->status + 1, ma, s));
   c->launches++;
   return FM_OK;
 }

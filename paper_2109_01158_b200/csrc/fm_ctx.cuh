@@ -5,8 +5,16 @@
 // Element records (AoS, one per element, storage order = grouped by owner tile):
 //   3D: 128 B = int32 conn[4] | f64 vol | f64 dphi[3][4] | int32 orig | pad
 //   2D:  80 B = int32 conn[3] | int32 orig | f64 vol | f64 dphi[2][3] | pad
-// One record is exactly one (3D) 128-byte line: a gather by element id costs
-// one line, and vol + dphi + conn arrive together.
+// A record is one 128-byte line (3D): a gather by element id costs one line and
+// brings vol, dphi and conn together.  In shared memory 3D records are stored
+// with a 144-byte stride (9 x 16 B, odd) so that lane i reading record i is
+// bank-conflict free; 80 B (5 x 16 B) is already odd.
+//
+// Node tiles: each tile owns <= 256 free nodes of a spatial box.  Its element
+// list is [own elements (contiguous storage range, the tile is their J owner)]
+// + [halo elements (storage ids)], and its node entries (te_local << 2 | slot)
+// are sorted by te_local per node so that a streaming pass over the element
+// list can be consumed chunk by chunk.
 #pragma once
 
 #include <math.h>
@@ -16,12 +24,23 @@
 
 namespace fm {
 
-constexpr int FLAG_J = 16;           // tile element contributes to J (its owner tile)
-constexpr int MAX_TILE_ELEMS = 16384; // node entries store te_local in 14 bits
+constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
+constexpr int CONSUMERS = 256;         // consumer threads = chunk size = max tile nodes
+constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
 
 template <int DIM> struct RecBytes;
-template <> struct RecBytes<2> { static constexpr int value = 80; };
-template <> struct RecBytes<3> { static constexpr int value = 128; };
+template <> struct RecBytes<2> { static constexpr int value = 80, smem = 80; };
+template <> struct RecBytes<3> { static constexpr int value = 128, smem = 144; };
+
+struct TileMeta {
+  int own_begin, own_count;      // storage range of the elements the tile owns
+  int halo_begin, halo_count;    // range in halo_ids
+  int node_begin, node_count;    // range in node_desc
+  int entry_begin, entry_count;  // range in node_entries (entry_begin % 8 == 0)
+  int elem_begin;                // range start in flags (own + halo)
+  int pad[3];
+};
+static_assert(sizeof(TileMeta) == 48, "TileMeta layout");
 
 template <int DIM> struct Elem {
   int c[DIM + 1];
@@ -30,7 +49,7 @@ template <int DIM> struct Elem {
   double g[DIM][DIM + 1];  // dphi[m][l]
 };
 
-// Element records are read exactly once per visit: stream them past L1.
+// Element records read once per visit: stream them past L1.
 __device__ __forceinline__ double2 ld_stream(const double2 *p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
@@ -40,14 +59,9 @@ __device__ __forceinline__ double2 ld_stream(const double2 *p) {
 }
 
 template <int DIM>
-__device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64_t s,
-                                          Elem<DIM> &E) {
-  const double2 *p =
-      reinterpret_cast<const double2 *>(aos + s * (int64_t)RecBytes<DIM>::value);
+__device__ __forceinline__ void decode_elem(const double2 (&q)[RecBytes<DIM>::value / 16],
+                                            Elem<DIM> &E) {
   if constexpr (DIM == 3) {
-    double2 q[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) q[k] = ld_stream(p + k);
     E.c[0] = __double2loint(q[0].x);
     E.c[1] = __double2hiint(q[0].x);
     E.c[2] = __double2loint(q[0].y);
@@ -61,9 +75,6 @@ __device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64
       for (int l = 0; l < 4; ++l) E.g[m][l] = f[m * 4 + l];
     E.orig = __double2loint(q[7].y);
   } else {
-    double2 q[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) q[k] = ld_stream(p + k);
     E.c[0] = __double2loint(q[0].x);
     E.c[1] = __double2hiint(q[0].x);
     E.c[2] = __double2loint(q[0].y);
@@ -78,13 +89,34 @@ __device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64
   }
 }
 
+template <int DIM>
+__device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64_t s,
+                                          Elem<DIM> &E) {
+  constexpr int NQ = RecBytes<DIM>::value / 16;
+  const double2 *p = reinterpret_cast<const double2 *>(aos + s * (int64_t)RecBytes<DIM>::value);
+  double2 q[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
+  decode_elem<DIM>(q, E);
+}
+
+template <int DIM>
+__device__ __forceinline__ void load_elem_smem(const uint8_t *rec, Elem<DIM> &E) {
+  constexpr int NQ = RecBytes<DIM>::value / 16;
+  const double2 *p = reinterpret_cast<const double2 *>(rec);
+  double2 q[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) q[k] = p[k];
+  decode_elem<DIM>(q, E);
+}
+
 // Gather the d components of the field at the element's nodes (v interleaved).
 template <int DIM, int D>
-__device__ __forceinline__ void gather_v(const double *__restrict__ v, const Elem<DIM> &E,
+__device__ __forceinline__ void gather_v(const double *__restrict__ v, const int (&c)[DIM + 1],
                                          double (&vv)[D][DIM + 1]) {
 #pragma unroll
   for (int l = 0; l < DIM + 1; ++l) {
-    const double *p = v + (int64_t)E.c[l] * D;
+    const double *p = v + (int64_t)c[l] * D;
 #pragma unroll
     for (int j = 0; j < D; ++j) vv[j][l] = __ldg(p + j);
   }
@@ -110,17 +142,16 @@ __device__ __forceinline__ double np_scalar_pow(double x, double e) {
 // Tile tables (built by fm_ctx_create).
 struct TileArgs {
   const uint8_t *aos;
-  const int32_t *tile_elem_ptr;   // n_tiles_all + 1
-  const int32_t *tile_elems;      // storage index per tile element
-  const uint8_t *tile_flags;      // owned-slot mask | FLAG_J
-  const int32_t *tile_node_ptr;   // n_tiles_all + 1 (orphan tiles: empty)
-  const int32_t *tile_node_rank;  // free rank per tile node
-  const int32_t *node_entry_ptr;  // per tile node + 1
-  const uint16_t *node_entries;   // te_local << 2 | slot, ascending element
-  const int32_t *free_node;       // nodes_minim (int32)
-  const int32_t *free_out;        // output offset of the node's first free dof
-  const uint8_t *free_mask;       // free components
-  const int32_t *rank_of;         // node -> free rank or -1
+  const TileMeta *meta;      // n_tiles_all
+  const int32_t *halo_ids;   // storage index of halo elements
+  const uint8_t *flags;      // owned-slot mask per tile element (own then halo)
+  const int4 *node_desc;     // {entry_off, entry_count, node id, out | mask << 28}
+  const uint16_t *entries;   // te_local << 2 | slot, sorted by te_local per node
+  const int32_t *rank_of;    // node -> free rank or -1
+  int n_tiles;               // node tiles
+  int n_tiles_all;           // + orphan tiles (J only)
+  int entry_cap;             // max entries of one tile, rounded up to 8
+  int halo_cap;              // max halo elements of one tile, rounded up to 4
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
@@ -148,19 +179,21 @@ struct fm_ctx {
   int64_t nn = 0, ne = 0, nfree = 0, nfree_dofs = 0, p_total = 0;
   int32_t n_tiles = 0, n_tiles_all = 0;
   int64_t n_tile_elems = 0, n_node_entries = 0;
-  int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0;
+  int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, halo_cap = 0;
+  int n_sm = 148, stages = 4;
   uint8_t *aos = nullptr;
-  int32_t *tile_elem_ptr = nullptr, *tile_elems = nullptr, *tile_node_ptr = nullptr;
-  int32_t *tile_node_rank = nullptr, *node_entry_ptr = nullptr;
-  uint8_t *tile_flags = nullptr;
+  fm::TileMeta *meta = nullptr;
+  int32_t *halo_ids = nullptr;
+  uint8_t *flags = nullptr;
+  int4 *node_desc = nullptr;
   uint16_t *node_entries = nullptr;
   int32_t *free_node = nullptr, *free_out = nullptr, *rank_of = nullptr;
   int32_t *storage_to_orig = nullptr;
   uint8_t *free_mask = nullptr;
   // scratch
-  double *jpart = nullptr;        // per tile (fused) / per block (energy)
+  double *jpart = nullptr;        // per CTA (fused) / per block (energy)
   double *dotpart = nullptr;      // b.v partials
-  int n_dot_blocks = 0, n_energy_blocks = 0;
+  int n_dot_blocks = 0, n_energy_blocks = 0, n_part = 0;
   unsigned long long *status = nullptr;  // [0] exact inadmissible, [1] FD min key
   int64_t launches = 0;
   size_t bytes = 0;
@@ -168,8 +201,7 @@ struct fm_ctx {
   fm_ctx_stats stats{};
 
   fm::TileArgs tile_args() const {
-    return fm::TileArgs{aos,          tile_elem_ptr, tile_elems, tile_flags,
-                        tile_node_ptr, tile_node_rank, node_entry_ptr, node_entries,
-                        free_node,     free_out,       free_mask,      rank_of};
+    return fm::TileArgs{aos,     meta,    halo_ids,    flags,     node_desc, node_entries,
+                        rank_of, n_tiles, n_tiles_all, entry_cap, halo_cap};
   }
 };

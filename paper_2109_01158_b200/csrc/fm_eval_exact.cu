@@ -1,165 +1,342 @@
-// Fused energy + exact gradient over node tiles (gradients.py:124-149 and
-// assembly.py:94-106 in one pass).
+// Fused energy + exact gradient (gradients.py:124-149 with assembly.py:94-106)
+// as one persistent, warp-specialised, mbarrier-pipelined kernel.
 //
-// One CTA owns one tile of free nodes (a spatial box).  It visits every element
-// incident to its nodes (its own elements plus a one-element halo), in chunks of
-// blockDim elements, one element per thread:
-//   phase A  gather record + nodal values, F = grad v, P = vol*dW/dF, and the
-//            contributions vol * sum_m dW[j][m] dphi[m][l] for the slots l whose
-//            node this tile owns -> shared-memory staging; vol*W for elements the
-//            tile owns (each element counted in J exactly once).
-//   phase B  each node thread consumes its staged entries in ascending element
-//            order (the reference patch order, patches.py:51-53) into registers.
-// No floating-point atomics: per-node sums are fixed-order, J is a fixed block
-// tree into per-tile partials reduced by fm_finalize in tile order.
+// One CTA per SM walks its node tiles (t = blockIdx.x, += gridDim.x; tiles are
+// in Morton order of their spatial boxes so concurrently running CTAs share
+// halo elements and nodal values through L2).
+//
+//   producer warp   for every chunk of 256 tile elements issues one 1D bulk
+//                   copy (cp.async.bulk, TMA engine) per 128-byte element
+//                   record into a ring of STAGES shared-memory buffers
+//                   (mbarrier complete_tx), and per tile the node descriptors
+//                   and node entries into a double-buffered tile area.
+//   8 consumer      thread c computes element c of the chunk from shared
+//   warps           memory: F = grad v (nodal values prefetched one chunk
+//                   ahead into registers), P' = vol * dW/dF folded to
+//                   P' = a F + b cof, the contributions P' . grad phi_l of the
+//                   four local nodes -> shared staging; vol * W when the tile
+//                   owns the element.  Then, as node threads, they consume their
+//                   entries of this chunk (sorted by tile element) into
+//                   registers: a fixed summation order, no float atomics.
+//
+// J: per-thread partials over a static tile assignment -> fixed block tree ->
+// one partial per CTA, reduced in CTA order by k_finalize.
 #include "fm_density.cuh"
 #include "fm_kernels.h"
+#include "fm_pipe.cuh"
 
 namespace fm {
 
-template <int DIM, int MODEL, bool WJ, bool WG>
-__global__ void __launch_bounds__(512) k_tile_exact(TileArgs a, const double *__restrict__ v,
-                                                    const double *__restrict__ b,
-                                                    double *__restrict__ g,
-                                                    double *__restrict__ jpart,
-                                                    unsigned long long *status, ModelArgs mdl) {
+template <int DIM>
+struct PipeLayout {
+  static constexpr int RS = RecBytes<DIM>::smem;
+  static constexpr int NQ = RecBytes<DIM>::value / 16;
+  __host__ __device__ static size_t stage_bytes() { return (size_t)CONSUMERS * RS; }
+  // tile buffer: meta (64) | node desc (256 x 16) | entries | halo ids
+  __host__ __device__ static size_t entries_off() { return 64 + (size_t)CONSUMERS * 16; }
+  __host__ __device__ static size_t halo_off(int entry_cap) {
+    return entries_off() + (((size_t)entry_cap * 2 + 15) / 16) * 16;
+  }
+  __host__ __device__ static size_t tile_bytes(int entry_cap, int halo_cap) {
+    return halo_off(entry_cap) + (((size_t)halo_cap * 4 + 15) / 16) * 16;
+  }
+  __host__ __device__ static size_t staging_bytes(int D) {
+    return (size_t)CONSUMERS * (DIM + 1) * D * 8;
+  }
+  __host__ __device__ static size_t total(int stages, int entry_cap, int halo_cap, int D) {
+    return stages * stage_bytes() + 2 * tile_bytes(entry_cap, halo_cap) + staging_bytes(D) +
+           32 * 8 + (2 * stages + 4) * 8;
+  }
+};
+
+// NH: P' = vol * dW/dF = a F + b cof with a = 2 C1 vol, b = vol (2 D1 (det-1) - 2 C1/det)
+// (models.py:103-120 regrouped).  p-Laplace: P' = vol |g|^(p-2) g.
+template <int DIM, int MODEL>
+__device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
+                                          double vol, const ModelArgs &m, bool want_w,
+                                          double (&P)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
+                                          double &W, bool &bad) {
+  if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
+    double C[DIM][DIM];
+    cof_F<DIM>(F, C);
+    double det = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) det = fma(F[0][k], C[0][k], det);
+    bad = !(det > 0.0);
+    const double rdet = 1.0 / det;
+    const double a = 2.0 * m.C1 * vol;
+    const double bc = vol * (2.0 * m.D1 * (det - 1.0) - 2.0 * m.C1 * rdet);
+#pragma unroll
+    for (int j = 0; j < DIM; ++j)
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) P[j][k] = fma(a, F[j][k], bc * C[j][k]);
+    if (want_w) {
+      double I1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) I1 = fma(F[j][k], F[j][k], I1);
+      const double dm1 = det - 1.0;
+      W = bad ? INFINITY : m.C1 * ((I1 - (double)DIM) - 2.0 * log(det)) + m.D1 * (dm1 * dm1);
+    }
+  } else {
+    bad = false;
+    double n2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) n2 = fma(F[0][k], F[0][k], n2);
+    double fac;
+    if (m.p >= 2.0)
+      fac = np_scalar_pow(n2, m.e_dw);
+    else
+      fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
+    fac *= vol;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) P[0][k] = fac * F[0][k];
+    if (want_w) W = np_scalar_pow(n2, m.e_w) / m.p;
+  }
+}
+
+template <int DIM, int MODEL, bool WJ, int STAGES>
+__global__ void __launch_bounds__(CONSUMERS + 32, 1)
+    k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
+                 double *__restrict__ g, double *__restrict__ jpart, unsigned long long *status,
+                 ModelArgs mdl) {
   constexpr int NV = DIM + 1;
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *stage = reinterpret_cast<double *>(smem_raw);              // [blockDim][NV][D]
-  double *red = stage + (WG ? blockDim.x * NV * D : 0);               // [32]
-  uint16_t *ents = reinterpret_cast<uint16_t *>(red + 32);            // tile node entries
+  using L = PipeLayout<DIM>;
+  constexpr int RS = L::RS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char *rec_base = smem;
+  unsigned char *tile_base = rec_base + STAGES * L::stage_bytes();
+  const size_t TB = L::tile_bytes(a.entry_cap, a.halo_cap);
+  const size_t HO = L::halo_off(a.entry_cap);
+  double *staging = reinterpret_cast<double *>(tile_base + 2 * TB);
+  double *red = staging + CONSUMERS * NV * D;
+  uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
 
-  const int t = blockIdx.x;
-  const int e0 = a.tile_elem_ptr[t], e1 = a.tile_elem_ptr[t + 1];
-  const int n0 = a.tile_node_ptr[t], n1 = a.tile_node_ptr[t + 1];
-  const int me = n0 + (int)threadIdx.x;
-  const bool has_node = WG && me < n1;
-  int cur = 0, end = 0;
-  if (WG) {
-    const int q0 = a.node_entry_ptr[n0], q1 = a.node_entry_ptr[n1];
-    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) ents[q - q0] = a.node_entries[q];
-    if (has_node) {
-      cur = a.node_entry_ptr[me] - q0;
-      end = a.node_entry_ptr[me + 1] - q0;
+  const int tid = threadIdx.x;
+  const bool producer = tid >= CONSUMERS;
+  const int lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
     }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull + s, 1);
+      mbar_init(tempty + s, 1);
+    }
+    fence_barrier_init();
   }
-  double acc[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) acc[j] = 0.0;
-  double jsum = 0.0;
-  bool bad_any = false;
-  if (WG) __syncthreads();
+  __syncthreads();
 
-  for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
-    const int i = c0 + threadIdx.x;
-    if (i < e1) {
-      const int s = a.tile_elems[i];
-      const int fl = a.tile_flags[i];
-      Elem<DIM> E;
-      load_elem<DIM>(a.aos, s, E);
-      double vv[D][NV];
-      gather_v<DIM, D>(v, E, vv);
-      double F[D][DIM];
-      grad_F<DIM, D>(vv, E.g, F);
-      if (WJ && (fl & FLAG_J)) jsum += E.vol * density<DIM, MODEL>(F, mdl);
-      if (WG && (fl & 15)) {
-        double P[D][DIM];
-        bool bad;
-        ddensity<DIM, MODEL>(F, mdl, P, bad);
-        bad_any |= bad;
-        double *row = stage + (size_t)threadIdx.x * NV * D;
+  double jsum = 0.0;
+  if (producer) {
+    // ------------------------------------------------------------- producer
+    uint32_t q = 0, j = 0;
+    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x, ++j) {
+      const TileMeta tm = a.meta[t];
+      unsigned char *tb = tile_base + (j & 1) * TB;
+      mbar_wait(tempty + (j & 1), ((j >> 1) & 1) ^ 1);
+      const int32_t *halo_s = reinterpret_cast<const int32_t *>(tb + HO);
+      if (lane == 0) {
+        *reinterpret_cast<TileMeta *>(tb) = tm;
+        const uint32_t nb = (uint32_t)tm.node_count * 16;
+        const uint32_t eb = (uint32_t)((tm.entry_count * 2 + 15) / 16) * 16;
+        const uint32_t hb = (uint32_t)((tm.halo_count * 4 + 15) / 16) * 16;
+        mbar_arrive_expect_tx(tfull + (j & 1), nb + eb + hb);
+        if (nb) bulk_g2s(tb + 64, a.node_desc + tm.node_begin, nb, tfull + (j & 1));
+        if (eb) bulk_g2s(tb + L::entries_off(), a.entries + tm.entry_begin, eb, tfull + (j & 1));
+        if (hb) bulk_g2s(tb + HO, a.halo_ids + tm.halo_begin, hb, tfull + (j & 1));
+      }
+      __syncwarp();
+      bool halo_ready = false;
+      const int ne_t = tm.own_count + tm.halo_count;
+      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
+        const int s = q % STAGES;
+        const int cnt = min(CONSUMERS, ne_t - c0);
+        if (!halo_ready && c0 + cnt > tm.own_count) {  // halo ids arrive with the tile buffer
+          mbar_wait(tfull + (j & 1), (j >> 1) & 1);
+          halo_ready = true;
+        }
+        mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RecBytes<DIM>::value);
+        __syncwarp();
+        unsigned char *dst = rec_base + s * L::stage_bytes();
+        for (int i = lane; i < cnt; i += 32) {
+          const int e = c0 + i;
+          const int src = e < tm.own_count ? tm.own_begin + e : halo_s[e - tm.own_count];
+          bulk_g2s(dst + i * RS, a.aos + (int64_t)src * RecBytes<DIM>::value,
+                   RecBytes<DIM>::value, full + s);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- consumers
+    uint32_t q = 0, j = 0;
+    bool bad_any = false;
+    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x, ++j) {
+      unsigned char *tb = tile_base + (j & 1) * TB;
+      mbar_wait(tfull + (j & 1), (j >> 1) & 1);
+      const TileMeta tm = *reinterpret_cast<const TileMeta *>(tb);
+      const int4 *desc = reinterpret_cast<const int4 *>(tb + 64);
+      const uint16_t *ents = reinterpret_cast<const uint16_t *>(tb + L::entries_off());
+      const bool has_nodes = tm.node_count > 0;
+      const bool my_node = tid < tm.node_count;
+      int cur = 0, end = 0, node = 0, outw = 0;
+      double bj[D], acc[D];
 #pragma unroll
-        for (int l = 0; l < NV; ++l) {
-          if (fl & (1 << l)) {
+      for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
+      if (my_node) {
+        const int4 nd = desc[tid];
+        cur = nd.x;
+        end = nd.x + nd.y;
+        node = nd.z;
+        outw = nd.w;
+        if (b) {
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-              double sdot = P[j][0] * E.g[0][l];
+          for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)node * D + k);
+        }
+      }
+      const int ne_t = tm.own_count + tm.halo_count;
+      const int nch = (ne_t + CONSUMERS - 1) / CONSUMERS;
+      double vv[D][NV], vn[D][NV];
+      // nodal values of chunk 0
+      if (nch > 0) {
+        const int s = q % STAGES;
+        mbar_wait(full + s, (q / STAGES) & 1);
+        if (tid < ne_t) {
+          const int *cc = reinterpret_cast<const int *>(rec_base + s * L::stage_bytes() + tid * RS);
+          int c[NV];
 #pragma unroll
-              for (int k = 1; k < DIM; ++k) sdot = sdot + P[j][k] * E.g[k][l];
-              row[l * D + j] = E.vol * sdot;
-            }
+          for (int l = 0; l < NV; ++l) c[l] = cc[l];
+          gather_v<DIM, D>(v, c, vv);
+        }
+      }
+      for (int ch = 0; ch < nch; ++ch, ++q) {
+        const int s = q % STAGES;
+        const int c0 = ch * CONSUMERS;
+        if (ch + 1 < nch) {  // prefetch the next chunk's nodal values
+          const uint32_t q1 = q + 1;
+          const int s1 = q1 % STAGES;
+          mbar_wait(full + s1, (q1 / STAGES) & 1);
+          if (c0 + CONSUMERS + tid < ne_t) {
+            const int *cc = reinterpret_cast<const int *>(rec_base + s1 * L::stage_bytes() + tid * RS);
+            int c[NV];
+#pragma unroll
+            for (int l = 0; l < NV; ++l) c[l] = cc[l];
+            gather_v<DIM, D>(v, c, vn);
           }
         }
-      }
-    }
-    if (WG) {
-      __syncthreads();
-      if (has_node) {
-        const int base = c0 - e0, lim = base + (int)blockDim.x;
-        while (cur < end) {
-          const int en = ents[cur];
-          const int te = en >> 2;
-          if (te >= lim) break;
-          const double *src = stage + ((size_t)(te - base) * NV + (en & 3)) * D;
+        const int e = c0 + tid;
+        if (e < ne_t) {
+          Elem<DIM> E;
+          load_elem_smem<DIM>(rec_base + s * L::stage_bytes() + tid * RS, E);
+          double F[D][DIM];
+          grad_F<DIM, D>(vv, E.g, F);
+          const bool own = e < tm.own_count;
+          if (has_nodes) {
+            double P[D][DIM], W = 0.0;
+            bool bad;
+            element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
+            bad_any |= bad;
+            if (WJ && own) jsum += E.vol * W;
+            double *row = staging + tid;  // [slot][comp][CONSUMERS]: conflict-free stores
 #pragma unroll
-          for (int j = 0; j < D; ++j) acc[j] += src[j];
-          ++cur;
+            for (int l = 0; l < NV; ++l)
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                double sdot = P[k][0] * E.g[0][l];
+#pragma unroll
+                for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
+                row[(l * D + k) * CONSUMERS] = sdot;
+              }
+          } else if (WJ) {
+            jsum += E.vol * density<DIM, MODEL>(F, mdl);
+          }
         }
+        named_sync(1, CONSUMERS);
+        if (tid == 0) mbar_arrive(empty + s);
+        if (my_node) {
+          const int lim = c0 + CONSUMERS;
+          while (cur < end) {
+            const int en = ents[cur];
+            const int te = en >> 2;
+            if (te >= lim) break;
+            const double *src = staging + (te - c0) + (en & 3) * D * CONSUMERS;
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
+            ++cur;
+          }
+        }
+        named_sync(1, CONSUMERS);
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+#pragma unroll
+          for (int l = 0; l < NV; ++l) vv[k][l] = vn[k][l];
       }
-      __syncthreads();
+      if (my_node) {
+        const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
+        int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+      }
+      if (tid == 0) mbar_arrive(tempty + (j & 1));
     }
-  }
-
-  if (WG) {
     if (bad_any) atomicOr(status, 1ull);
-    if (has_node) {
-      const int r = a.tile_node_rank[me];
-      const int64_t node = a.free_node[r];
-      const int mask = a.free_mask[r];
-      int o = a.free_out[r];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (mask & (1 << j)) {
-          double bj = b ? __ldg(b + node * D + j) : 0.0;
-          g[o++] = acc[j] - bj;
-        }
-      }
-    }
   }
   if (WJ) {
-    double s = block_sum(jsum, red);
-    if (threadIdx.x == 0) jpart[t] = s;
+    double r = block_sum(jsum, red);
+    if (tid == 0) jpart[blockIdx.x] = r;
   }
 }
 
 template <int DIM, int MODEL>
-static cudaError_t launch_exact_t(const TileArgs &a, int n_tiles, int threads, size_t smem_fixed,
-                                  bool wj, bool wg, const double *v, const double *b, double *g,
-                                  double *jpart, unsigned long long *status,
-                                  const ModelArgs &m, cudaStream_t s) {
+static cudaError_t launch_exact_t(const TileArgs &a, int grid, int stages, bool wj,
+                                  const double *v, const double *b, double *g, double *jpart,
+                                  unsigned long long *status, const ModelArgs &m,
+                                  cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  size_t smem = smem_fixed + 32 * sizeof(double) +
-                (wg ? (size_t)threads * (DIM + 1) * D * sizeof(double) : 0);
-  if (wj && wg) {
-    auto k = k_tile_exact<DIM, MODEL, true, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<n_tiles, threads, smem, s>>>(a, v, b, g, jpart, status, m);
-  } else if (wg) {
-    auto k = k_tile_exact<DIM, MODEL, false, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<n_tiles, threads, smem, s>>>(a, v, b, g, jpart, status, m);
+  const size_t smem = PipeLayout<DIM>::total(stages, a.entry_cap, a.halo_cap, D);
+  const int threads = CONSUMERS + 32;
+#define FM_LAUNCH(WJV, ST)                                                            \
+  do {                                                                                \
+    auto k = k_tile_exact<DIM, MODEL, WJV, ST>;                                       \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    k<<<grid, threads, smem, s>>>(a, v, b, g, jpart, status, m);                      \
+  } while (0)
+  if (stages == 3) {
+    if (wj) FM_LAUNCH(true, 3); else FM_LAUNCH(false, 3);
+  } else if (stages == 2) {
+    if (wj) FM_LAUNCH(true, 2); else FM_LAUNCH(false, 2);
   } else {
-    return cudaErrorInvalidValue;  // J alone streams elements once: k_energy
+    if (wj) FM_LAUNCH(true, 4); else FM_LAUNCH(false, 4);
   }
+#undef FM_LAUNCH
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int n_tiles, int threads,
-                              size_t smem_entries, bool wj, bool wg, const double *v,
-                              const double *b, double *g, double *jpart,
-                              unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
+size_t tile_exact_smem(int dim, int d, int stages, int entry_cap, int halo_cap) {
+  return dim == 3 ? PipeLayout<3>::total(stages, entry_cap, halo_cap, d)
+                  : PipeLayout<2>::total(stages, entry_cap, halo_cap, d);
+}
+
+cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int stages,
+                              bool wj, const double *v, const double *b, double *g,
+                              double *jpart, unsigned long long *status, const ModelArgs &m,
+                              cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, n_tiles, threads, smem_entries, wj, wg, v, b,
-                                                g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, n_tiles, threads, smem_entries, wj, wg, v, b,
-                                                g, jpart, status, m, s);
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
   if (dim == 2)
-    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, n_tiles, threads, smem_entries, wj, wg, v,
-                                                  b, g, jpart, status, m, s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, n_tiles, threads, smem_entries, wj, wg, v, b,
-                                                g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, stages, wj, v, b, g, jpart, status, m,
+                                                  s);
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
 }
 
 }  // namespace fm

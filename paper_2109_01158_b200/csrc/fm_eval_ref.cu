@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) k_energy(const uint8_t *__restrict__ aos,
     Elem<DIM> E;
     load_elem<DIM>(aos, s, E);
     double vv[D][NV];
-    gather_v<DIM, D>(v, E, vv);
+    gather_v<DIM, D>(v, E.c, vv);
     double F[D][DIM];
     grad_F<DIM, D>(vv, E.g, F);
     double W = density<DIM, MODEL>(F, mdl);
@@ -84,18 +84,18 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
   double *stage = reinterpret_cast<double *>(smem_raw);  // [blockDim][NV][D][2]
   uint16_t *ents = reinterpret_cast<uint16_t *>(stage + blockDim.x * NV * D * 2);
 
-  const int t = blockIdx.x;
-  const int e0 = a.tile_elem_ptr[t], e1 = a.tile_elem_ptr[t + 1];
-  const int n0 = a.tile_node_ptr[t], n1 = a.tile_node_ptr[t + 1];
-  if (n0 == n1) return;  // orphan tile: no free node, nothing to differentiate
-  const int me = n0 + (int)threadIdx.x;
-  const bool has_node = me < n1;
-  const int q0 = a.node_entry_ptr[n0], q1 = a.node_entry_ptr[n1];
-  for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) ents[q - q0] = a.node_entries[q];
-  int cur = 0, end = 0;
+  const TileMeta tm = a.meta[blockIdx.x];
+  if (tm.node_count == 0) return;  // orphan tile: no free node, nothing to differentiate
+  const bool has_node = (int)threadIdx.x < tm.node_count;
+  for (int q = threadIdx.x; q < tm.entry_count; q += blockDim.x)
+    ents[q] = a.entries[tm.entry_begin + q];
+  int cur = 0, end = 0, node = 0, outw = 0;
   if (has_node) {
-    cur = a.node_entry_ptr[me] - q0;
-    end = a.node_entry_ptr[me + 1] - q0;
+    const int4 nd = a.node_desc[tm.node_begin + threadIdx.x];
+    cur = nd.x;
+    end = nd.x + nd.y;
+    node = nd.z;
+    outw = nd.w;
   }
   double accm[D], accp[D];
 #pragma unroll
@@ -103,15 +103,16 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
   unsigned long long mykey = ~0ull;
   __syncthreads();
 
-  for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
+  const int ne_t = tm.own_count + tm.halo_count;
+  for (int c0 = 0; c0 < ne_t; c0 += blockDim.x) {
     const int i = c0 + threadIdx.x;
-    if (i < e1) {
-      const int s = a.tile_elems[i];
-      const int fl = a.tile_flags[i];
+    if (i < ne_t) {
+      const int s = i < tm.own_count ? tm.own_begin + i : a.halo_ids[tm.halo_begin + i - tm.own_count];
+      const int fl = a.flags[tm.elem_begin + i];
       Elem<DIM> E;
       load_elem<DIM>(a.aos, s, E);
       double vv[D][NV];
-      gather_v<DIM, D>(v, E, vv);
+      gather_v<DIM, D>(v, E.c, vv);
       double F[D][DIM];
       grad_F<DIM, D>(vv, E.g, F);
       double *row = stage + (size_t)threadIdx.x * NV * D * 2;
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
     }
     __syncthreads();
     if (has_node) {
-      const int base = c0 - e0, lim = base + (int)blockDim.x;
+      const int base = c0, lim = base + (int)blockDim.x;
       while (cur < end) {
         const int en = ents[cur];
         const int te = en >> 2;
@@ -166,10 +167,8 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
   }
   if (mykey != ~0ull) atomicMin(badkey, mykey);
   if (has_node) {
-    const int r = a.tile_node_rank[me];
-    const int64_t node = a.free_node[r];
-    const int mask = a.free_mask[r];
-    int o = a.free_out[r];
+    const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
+    int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
     const double inv = 2.0 * eps;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
