@@ -15,6 +15,8 @@
 //      slot masks OR-reduced by key;
 //   5. node descriptors and entries (te_local << 2 | slot) sorted by te_local.
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -320,6 +322,39 @@ template <class F> static cudaError_t cub_call(F f, cudaStream_t s) {
   return f(tmp.p, bytes);
 }
 
+// 3D element records viewed as a 2D tensor [ne rows][16 f64]: six box heights
+// 8..256 with the 128-byte swizzle (chunk ^ row % 8) the consumers read with.
+static int make_record_tmaps(const uint8_t *aos, int64_t ne, TmaMaps *out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) !=
+            cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn) {
+      set_error("cuTensorMapEncodeTiled is not available from the driver");
+      return FM_CUDA_ERROR;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  static_assert(sizeof(CUtensorMap) == sizeof(TmaDesc), "tensor map size");
+  for (int k = 0; k < 6; ++k) {
+    cuuint64_t dims[2] = {16, (cuuint64_t)ne};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {16, (cuuint32_t)(8 << k)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap *>(&out->box[k]),
+                        CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)aos, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
+      return FM_CUDA_ERROR;
+    }
+  }
+  return FM_OK;
+}
+
 struct TimedLaunch {
   fm_ctx *c;
   cudaStream_t s;
@@ -568,6 +603,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     k_build_aos<2><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
                                                      m->dphi, c->aos);
   CK(cudaGetLastError());
+  if (dim == 3) {  // element records as a (ne x 128 B) tensor for the TMA loads
+    int st = make_record_tmaps(c->aos, ne, &c->tma);
+    if (st) return fail(st);
+  }
 
   // 4. tile element lists (own + halo) ----------------------------------------
   int64_t M = 0;
@@ -802,8 +841,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   const int grid = std::min(c->n_sm, std::max(1, ta.n_tiles_all));
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->stages, wj, v, b, g, c->jpart,
-                              c->status, ma, s));
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, c->tma, ta, grid, c->stages, wj, v, b, g,
+                              c->jpart, c->status, ma, s));
     c->launches++;
   }
   if (wj) {

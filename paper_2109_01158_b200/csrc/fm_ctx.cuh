@@ -30,7 +30,15 @@ constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask <
 
 template <int DIM> struct RecBytes;
 template <> struct RecBytes<2> { static constexpr int value = 80, smem = 80; };
-template <> struct RecBytes<3> { static constexpr int value = 128, smem = 144; };
+template <> struct RecBytes<3> { static constexpr int value = 128, smem = 128; };
+
+// 16-B chunk c of shared-memory record r: 3D records use the TMA 128-byte swizzle
+// (chunk index XOR r mod 8, stage buffers 1024-B aligned), 2D records an odd stride.
+template <int DIM>
+__device__ __forceinline__ int rec_chunk_off(int r, int c) {
+  if constexpr (DIM == 3) return r * 128 + ((c ^ (r & 7)) << 4);
+  else return r * 80 + (c << 4);
+}
 
 struct TileMeta {
   int own_begin, own_count;      // storage range of the elements the tile owns
@@ -101,14 +109,22 @@ __device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64
 }
 
 template <int DIM>
-__device__ __forceinline__ void load_elem_smem(const uint8_t *rec, Elem<DIM> &E) {
+__device__ __forceinline__ void load_elem_smem(const uint8_t *stage, int r, Elem<DIM> &E) {
   constexpr int NQ = RecBytes<DIM>::value / 16;
-  const double2 *p = reinterpret_cast<const double2 *>(rec);
   double2 q[NQ];
 #pragma unroll
-  for (int k = 0; k < NQ; ++k) q[k] = p[k];
+  for (int k = 0; k < NQ; ++k)
+    q[k] = *reinterpret_cast<const double2 *>(stage + rec_chunk_off<DIM>(r, k));
   decode_elem<DIM>(q, E);
 }
+
+// CUtensorMap is a 128-byte, 64-byte aligned opaque descriptor; boxes of 8..256 rows.
+struct alignas(64) TmaDesc {
+  unsigned char bytes[128];
+};
+struct TmaMaps {
+  TmaDesc box[6];  // rows 8 << k
+};
 
 // Gather the d components of the field at the element's nodes (v interleaved).
 template <int DIM, int D>
@@ -198,6 +214,7 @@ struct fm_ctx {
   int64_t launches = 0;
   size_t bytes = 0;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // armed by fm_ctx_time_next
+  fm::TmaMaps tma{};  // 3D element records as a 2D tensor (rows x 128 B), SWIZZLE_128B
   fm_ctx_stats stats{};
 
   fm::TileArgs tile_args() const {

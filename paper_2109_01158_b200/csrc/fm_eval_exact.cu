@@ -5,19 +5,21 @@
 // in Morton order of their spatial boxes so concurrently running CTAs share
 // halo elements and nodal values through L2).
 //
-//   producer warp   for every chunk of 256 tile elements issues one 1D bulk
-//                   copy (cp.async.bulk, TMA engine) per 128-byte element
-//                   record into a ring of STAGES shared-memory buffers
-//                   (mbarrier complete_tx), and per tile the node descriptors
-//                   and node entries into a double-buffered tile area.
+//   producer warp   per chunk of 256 tile elements: the tile's own elements are
+//                   a contiguous storage range -> TMA 2D tensor loads (boxes of
+//                   8..256 records, SWIZZLE_128B) in 3D / one 1D bulk copy in
+//                   2D; halo records (and a < 8-record remainder) -> 16-byte
+//                   LDGSTS by the 32 lanes into the same swizzled layout.  Both
+//                   complete on the stage's mbarrier.  Per tile it bulk-copies the
+//                   node descriptors, node entries and halo ids into a
+//                   double-buffered tile area.
 //   8 consumer      thread c computes element c of the chunk from shared
 //   warps           memory: F = grad v (nodal values prefetched one chunk
-//                   ahead into registers), P' = vol * dW/dF folded to
-//                   P' = a F + b cof, the contributions P' . grad phi_l of the
-//                   four local nodes -> shared staging; vol * W when the tile
-//                   owns the element.  Then, as node threads, they consume their
-//                   entries of this chunk (sorted by tile element) into
-//                   registers: a fixed summation order, no float atomics.
+//                   ahead into registers), P' = vol * dW/dF = a F + b cof, the
+//                   contributions P' . grad phi_l of the four local nodes ->
+//                   shared staging; vol * W when the tile owns the element.  Then
+//                   as node threads they consume this chunk's entries (sorted by
+//                   tile element) into registers: fixed order, no float atomics.
 //
 // J: per-thread partials over a static tile assignment -> fixed block tree ->
 // one partial per CTA, reduced in CTA order by k_finalize.
@@ -30,8 +32,9 @@ namespace fm {
 template <int DIM>
 struct PipeLayout {
   static constexpr int RS = RecBytes<DIM>::smem;
-  static constexpr int NQ = RecBytes<DIM>::value / 16;
-  __host__ __device__ static size_t stage_bytes() { return (size_t)CONSUMERS * RS; }
+  __host__ __device__ static size_t stage_bytes() {
+    return ((size_t)CONSUMERS * RS + 1023) / 1024 * 1024;
+  }
   // tile buffer: meta (64) | node desc (256 x 16) | entries | halo ids
   __host__ __device__ static size_t entries_off() { return 64 + (size_t)CONSUMERS * 16; }
   __host__ __device__ static size_t halo_off(int entry_cap) {
@@ -43,9 +46,10 @@ struct PipeLayout {
   __host__ __device__ static size_t staging_bytes(int D) {
     return (size_t)CONSUMERS * (DIM + 1) * D * 8;
   }
+  // + 1024 for aligning the dynamic shared memory base
   __host__ __device__ static size_t total(int stages, int entry_cap, int halo_cap, int D) {
-    return stages * stage_bytes() + 2 * tile_bytes(entry_cap, halo_cap) + staging_bytes(D) +
-           32 * 8 + (2 * stages + 4) * 8;
+    return 1024 + stages * stage_bytes() + 2 * tile_bytes(entry_cap, halo_cap) +
+           staging_bytes(D) + 32 * 8 + (2 * stages + 4) * 8;
   }
 };
 
@@ -98,14 +102,17 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
 
 template <int DIM, int MODEL, bool WJ, int STAGES>
 __global__ void __launch_bounds__(CONSUMERS + 32, 1)
-    k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
-                 double *__restrict__ g, double *__restrict__ jpart, unsigned long long *status,
-                 ModelArgs mdl) {
+    k_tile_exact(const __grid_constant__ TmaMaps tma, TileArgs a, const double *__restrict__ v,
+                 const double *__restrict__ b, double *__restrict__ g,
+                 double *__restrict__ jpart, unsigned long long *status, ModelArgs mdl) {
   constexpr int NV = DIM + 1;
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
+  constexpr int RB = RecBytes<DIM>::value;  // bytes of one record (global)
+  constexpr int NCH = RB / 16;               // 16-B chunks per record
   using L = PipeLayout<DIM>;
-  constexpr int RS = L::RS;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char *rec_base = smem;
   unsigned char *tile_base = rec_base + STAGES * L::stage_bytes();
   const size_t TB = L::tile_bytes(a.entry_cap, a.halo_cap);
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
   const int lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, 1 + 32);  // expect_tx arrival + one LDGSTS arrival per producer lane
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -158,20 +165,41 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
       for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
         const int s = q % STAGES;
         const int cnt = min(CONSUMERS, ne_t - c0);
-        if (!halo_ready && c0 + cnt > tm.own_count) {  // halo ids arrive with the tile buffer
-          mbar_wait(tfull + (j & 1), (j >> 1) & 1);
+        const int n_own = max(0, min(cnt, tm.own_count - c0));
+        // 3D: TMA boxes cover the 8-aligned part of the own range; 2D: one bulk copy
+        const int n_bulk = DIM == 3 ? (n_own & ~7) : n_own;
+        if (!halo_ready && cnt > n_bulk && c0 + cnt > tm.own_count) {
+          mbar_wait(tfull + (j & 1), (j >> 1) & 1);  // halo ids arrive with the tile buffer
           halo_ready = true;
         }
         mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RecBytes<DIM>::value);
-        __syncwarp();
         unsigned char *dst = rec_base + s * L::stage_bytes();
-        for (int i = lane; i < cnt; i += 32) {
-          const int e = c0 + i;
-          const int src = e < tm.own_count ? tm.own_begin + e : halo_s[e - tm.own_count];
-          bulk_g2s(dst + i * RS, a.aos + (int64_t)src * RecBytes<DIM>::value,
-                   RecBytes<DIM>::value, full + s);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(full + s, (uint32_t)n_bulk * RB);
+          if constexpr (DIM == 3) {
+            int off = 0;
+#pragma unroll 1
+            for (int k = 5; k >= 0; --k) {
+              const int rows = 8 << k;
+              if (n_bulk - off >= rows) {
+                tma_load_2d(dst + off * 128, &tma.box[k], 0, tm.own_begin + c0 + off, full + s);
+                off += rows;
+              }
+            }
+          } else {
+            if (n_bulk)
+              bulk_g2s(dst, a.aos + (int64_t)(tm.own_begin + c0) * RB, (uint32_t)n_bulk * RB,
+                       full + s);
+          }
         }
+        // remaining records of the chunk: 16-byte LDGSTS, lane-parallel
+        for (int idx = lane; idx < (cnt - n_bulk) * NCH; idx += 32) {
+          const int r = n_bulk + idx / NCH, c = idx % NCH;
+          const int e = c0 + r;
+          const int src = e < tm.own_count ? tm.own_begin + e : halo_s[e - tm.own_count];
+          cp_async16(dst + rec_chunk_off<DIM>(r, c), a.aos + (int64_t)src * RB + c * 16);
+        }
+        cp_async_arrive_noinc(full + s);
       }
     }
   } else {
@@ -204,37 +232,41 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
       const int ne_t = tm.own_count + tm.halo_count;
       const int nch = (ne_t + CONSUMERS - 1) / CONSUMERS;
       double vv[D][NV], vn[D][NV];
-      // nodal values of chunk 0
-      if (nch > 0) {
+      if (nch > 0) {  // nodal values of chunk 0
         const int s = q % STAGES;
         mbar_wait(full + s, (q / STAGES) & 1);
         if (tid < ne_t) {
-          const int *cc = reinterpret_cast<const int *>(rec_base + s * L::stage_bytes() + tid * RS);
-          int c[NV];
+          const int4 cc = *reinterpret_cast<const int4 *>(rec_base + s * L::stage_bytes() +
+                                                          rec_chunk_off<DIM>(tid, 0));
+          const int c[4] = {cc.x, cc.y, cc.z, cc.w};
+          int cn[NV];
 #pragma unroll
-          for (int l = 0; l < NV; ++l) c[l] = cc[l];
-          gather_v<DIM, D>(v, c, vv);
+          for (int l = 0; l < NV; ++l) cn[l] = c[l];
+          gather_v<DIM, D>(v, cn, vv);
         }
       }
       for (int ch = 0; ch < nch; ++ch, ++q) {
         const int s = q % STAGES;
         const int c0 = ch * CONSUMERS;
+        const unsigned char *stage = rec_base + s * L::stage_bytes();
         if (ch + 1 < nch) {  // prefetch the next chunk's nodal values
           const uint32_t q1 = q + 1;
           const int s1 = q1 % STAGES;
           mbar_wait(full + s1, (q1 / STAGES) & 1);
           if (c0 + CONSUMERS + tid < ne_t) {
-            const int *cc = reinterpret_cast<const int *>(rec_base + s1 * L::stage_bytes() + tid * RS);
-            int c[NV];
+            const int4 cc = *reinterpret_cast<const int4 *>(rec_base + s1 * L::stage_bytes() +
+                                                            rec_chunk_off<DIM>(tid, 0));
+            const int c[4] = {cc.x, cc.y, cc.z, cc.w};
+            int cn[NV];
 #pragma unroll
-            for (int l = 0; l < NV; ++l) c[l] = cc[l];
-            gather_v<DIM, D>(v, c, vn);
+            for (int l = 0; l < NV; ++l) cn[l] = c[l];
+            gather_v<DIM, D>(v, cn, vn);
           }
         }
         const int e = c0 + tid;
         if (e < ne_t) {
           Elem<DIM> E;
-          load_elem_smem<DIM>(rec_base + s * L::stage_bytes() + tid * RS, E);
+          load_elem_smem<DIM>(stage, tid, E);
           double F[D][DIM];
           grad_F<DIM, D>(vv, E.g, F);
           const bool own = e < tm.own_count;
@@ -296,9 +328,9 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
 }
 
 template <int DIM, int MODEL>
-static cudaError_t launch_exact_t(const TileArgs &a, int grid, int stages, bool wj,
-                                  const double *v, const double *b, double *g, double *jpart,
-                                  unsigned long long *status, const ModelArgs &m,
+static cudaError_t launch_exact_t(const TmaMaps &tma, const TileArgs &a, int grid, int stages,
+                                  bool wj, const double *v, const double *b, double *g,
+                                  double *jpart, unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   const size_t smem = PipeLayout<DIM>::total(stages, a.entry_cap, a.halo_cap, D);
@@ -307,7 +339,7 @@ static cudaError_t launch_exact_t(const TileArgs &a, int grid, int stages, bool 
   do {                                                                                \
     auto k = k_tile_exact<DIM, MODEL, WJV, ST>;                                       \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k<<<grid, threads, smem, s>>>(a, v, b, g, jpart, status, m);                      \
+    k<<<grid, threads, smem, s>>>(tma, a, v, b, g, jpart, status, m);                 \
   } while (0)
   if (stages == 3) {
     if (wj) FM_LAUNCH(true, 3); else FM_LAUNCH(false, 3);
@@ -325,18 +357,21 @@ size_t tile_exact_smem(int dim, int d, int stages, int entry_cap, int halo_cap) 
                   : PipeLayout<2>::total(stages, entry_cap, halo_cap, d);
 }
 
-cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int stages,
-                              bool wj, const double *v, const double *b, double *g,
-                              double *jpart, unsigned long long *status, const ModelArgs &m,
-                              cudaStream_t s) {
+cudaError_t launch_tile_exact(int dim, int model, const TmaMaps &tma, const TileArgs &a,
+                              int grid, int stages, bool wj, const double *v, const double *b,
+                              double *g, double *jpart, unsigned long long *status,
+                              const ModelArgs &m, cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(tma, a, grid, stages, wj, v, b, g, jpart, status,
+                                                m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(tma, a, grid, stages, wj, v, b, g, jpart, status,
+                                                m, s);
   if (dim == 2)
-    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, stages, wj, v, b, g, jpart, status, m,
-                                                  s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, stages, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(tma, a, grid, stages, wj, v, b, g, jpart,
+                                                  status, m, s);
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(tma, a, grid, stages, wj, v, b, g, jpart, status,
+                                                m, s);
 }
 
 }  // namespace fm

@@ -9,10 +9,10 @@
 namespace fm {
 
 // persistent pipelined fused J + exact gradient; grid = #SMs, CONSUMERS + 32 threads
-cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int stages,
-                              bool wj, const double *v, const double *b, double *g,
-                              double *jpart, unsigned long long *status, const ModelArgs &m,
-                              cudaStream_t s);
+cudaError_t launch_tile_exact(int dim, int model, const TmaMaps &tma, const TileArgs &a,
+                              int grid, int stages, bool wj, const double *v, const double *b,
+                              double *g, double *jpart, unsigned long long *status,
+                              const ModelArgs &m, cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int stages, int entry_cap, int halo_cap);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
