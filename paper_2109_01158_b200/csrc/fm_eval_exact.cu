@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
   constexpr int NCH = RB / 16;               // 16-B chunks per record
   using L = PipeLayout<DIM>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char *smem = reinterpret_cast<unsigned char *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // align to 1024 B (TMA 128-byte swizzle atom) while staying derived from the
+  // __shared__ symbol, so that all accesses compile to LDS/STS, not generic LD/ST
+  unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char *rec_base = smem;
   unsigned char *tile_base = rec_base + STAGES * L::stage_bytes();
   const size_t TB = L::tile_bytes(a.entry_cap, a.halo_cap);
