@@ -3,23 +3,25 @@
 //
 // One CTA per SM walks its node tiles (t = blockIdx.x, += gridDim.x; tiles are
 // in Morton order of their spatial boxes so concurrently running CTAs share
-// halo elements and nodal values through L2).
+// halo elements and nodal values through L2).  Per chunk of 256 tile elements
+// a ring stage holds the element records and the gathered nodal values:
 //
-//   producer warp   per chunk of 256 tile elements: the tile's own elements are
-//                   a contiguous storage range -> TMA 2D tensor loads (boxes of
-//                   8..256 records, SWIZZLE_128B) in 3D / one 1D bulk copy in
-//                   2D; halo records (and a < 8-record remainder) -> 16-byte
-//                   LDGSTS by the 32 lanes into the same swizzled layout.  Both
-//                   complete on the stage's mbarrier.  Per tile it bulk-copies the
-//                   node descriptors, node entries and halo ids into a
-//                   double-buffered tile area.
-//   8 consumer      thread c computes element c of the chunk from shared
-//   warps           memory: F = grad v (nodal values prefetched one chunk
-//                   ahead into registers), P' = vol * dW/dF = a F + b cof, the
-//                   contributions P' . grad phi_l of the four local nodes ->
-//                   shared staging; vol * W when the tile owns the element.  Then
-//                   as node threads they consume this chunk's entries (sorted by
-//                   tile element) into registers: fixed order, no float atomics.
+//   record producer  the tile's own elements are a contiguous storage range ->
+//   (warp 8)         TMA 2D tensor loads (boxes of 8..256 records, SWIZZLE_128B)
+//                    in 3D / one 1D bulk copy in 2D; halo records and the < 8
+//                    remainder -> 16-byte LDGSTS by the 32 lanes into the same
+//                    layout.  Per tile: node descriptors, node entries and halo
+//                    ids -> double-buffered tile area (bulk copies).
+//   value producer   once a stage's records landed, reads their connectivity
+//   (warp 9)         and gathers the nodal field values v[conn] into the
+//                    stage's value buffer with 8-byte LDGSTS.
+//   8 consumer       thread c: element c of the chunk from shared memory:
+//   warps            F = grad v, P' = vol * dW/dF = a F + b cof, contributions
+//                    P' . grad phi_l of the four local nodes, written over the
+//                    (consumed) value buffer; vol * W when the tile owns the
+//                    element.  Then as node threads they consume this chunk's
+//                    entries (sorted by tile element) into registers: fixed
+//                    summation order, no floating-point atomics.
 //
 // J: per-thread partials over a static tile assignment -> fixed block tree ->
 // one partial per CTA, reduced in CTA order by k_finalize.
@@ -29,12 +31,19 @@
 
 namespace fm {
 
+constexpr int PRODUCER_WARPS = 2;
+
 template <int DIM>
 struct PipeLayout {
   static constexpr int RS = RecBytes<DIM>::smem;
-  __host__ __device__ static size_t stage_bytes() {
+  __host__ __device__ static size_t rec_bytes() {
     return ((size_t)CONSUMERS * RS + 1023) / 1024 * 1024;
   }
+  // nodal values [NV*D][CONSUMERS] f64, reused as the contribution staging
+  __host__ __device__ static size_t val_bytes(int D) {
+    return (((size_t)CONSUMERS * (DIM + 1) * D * 8) + 1023) / 1024 * 1024;
+  }
+  __host__ __device__ static size_t stage_bytes(int D) { return rec_bytes() + val_bytes(D); }
   // tile buffer: meta (64) | node desc (256 x 16) | entries | halo ids
   __host__ __device__ static size_t entries_off() { return 64 + (size_t)CONSUMERS * 16; }
   __host__ __device__ static size_t halo_off(int entry_cap) {
@@ -43,13 +52,10 @@ struct PipeLayout {
   __host__ __device__ static size_t tile_bytes(int entry_cap, int halo_cap) {
     return halo_off(entry_cap) + (((size_t)halo_cap * 4 + 15) / 16) * 16;
   }
-  __host__ __device__ static size_t staging_bytes(int D) {
-    return (size_t)CONSUMERS * (DIM + 1) * D * 8;
-  }
   // + 1024 for aligning the dynamic shared memory base
   __host__ __device__ static size_t total(int stages, int entry_cap, int halo_cap, int D) {
-    return 1024 + stages * stage_bytes() + 2 * tile_bytes(entry_cap, halo_cap) +
-           staging_bytes(D) + 32 * 8 + (2 * stages + 4) * 8;
+    return 1024 + stages * stage_bytes(D) + 2 * tile_bytes(entry_cap, halo_cap) + 32 * 8 +
+           (3 * stages + 4) * 8;
   }
 };
 
@@ -101,7 +107,7 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
 }
 
 template <int DIM, int MODEL, bool WJ, int STAGES>
-__global__ void __launch_bounds__(CONSUMERS + 32, 1)
+__global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
     k_tile_exact(const __grid_constant__ TmaMaps tma, TileArgs a, const double *__restrict__ v,
                  const double *__restrict__ b, double *__restrict__ g,
                  double *__restrict__ jpart, unsigned long long *status, ModelArgs mdl) {
@@ -114,24 +120,26 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
   // align to 1024 B (TMA 128-byte swizzle atom) while staying derived from the
   // __shared__ symbol, so that all accesses compile to LDS/STS, not generic LD/ST
   unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char *rec_base = smem;
-  unsigned char *tile_base = rec_base + STAGES * L::stage_bytes();
+  const size_t SB = L::stage_bytes(D);
+  unsigned char *stage_base = smem;
+  unsigned char *tile_base = stage_base + STAGES * SB;
   const size_t TB = L::tile_bytes(a.entry_cap, a.halo_cap);
   const size_t HO = L::halo_off(a.entry_cap);
-  double *staging = reinterpret_cast<double *>(tile_base + 2 * TB);
-  double *red = staging + CONSUMERS * NV * D;
+  double *red = reinterpret_cast<double *>(tile_base + 2 * TB);
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);
-  uint64_t *empty = full + STAGES;
+  uint64_t *vfull = full + STAGES;
+  uint64_t *empty = vfull + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
+  constexpr int CW = CONSUMERS / 32;  // consumer warps
 
   const int tid = threadIdx.x;
-  const bool producer = tid >= CONSUMERS;
-  const int lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1 + 32);  // expect_tx arrival + one LDGSTS arrival per producer lane
-      mbar_init(empty + s, 1);
+      mbar_init(vfull + s, 32);     // one LDGSTS arrival per value-producer lane
+      mbar_init(empty + s, CW);     // one arrival per consumer warp
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull + s, 1);
@@ -142,8 +150,8 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
   __syncthreads();
 
   double jsum = 0.0;
-  if (producer) {
-    // ------------------------------------------------------------- producer
+  if (warp == CW) {
+    // ------------------------------------------------------- record producer
     uint32_t q = 0, j = 0;
     for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x, ++j) {
       const TileMeta tm = a.meta[t];
@@ -174,7 +182,7 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
           halo_ready = true;
         }
         mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
-        unsigned char *dst = rec_base + s * L::stage_bytes();
+        unsigned char *dst = stage_base + s * SB;
         if (lane == 0) {
           mbar_arrive_expect_tx(full + s, (uint32_t)n_bulk * RB);
           if constexpr (DIM == 3) {
@@ -201,6 +209,32 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
           cp_async16(dst + rec_chunk_off<DIM>(r, c), a.aos + (int64_t)src * RB + c * 16);
         }
         cp_async_arrive_noinc(full + s);
+      }
+    }
+  } else if (warp == CW + 1) {
+    // ------------------------------------------------------- value producer
+    uint32_t q = 0;
+    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x) {
+      const TileMeta tm = a.meta[t];
+      const int ne_t = tm.own_count + tm.halo_count;
+      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
+        const int s = q % STAGES;
+        const int cnt = min(CONSUMERS, ne_t - c0);
+        mbar_wait(full + s, (q / STAGES) & 1);
+        const unsigned char *rec = stage_base + s * SB;
+        double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
+        for (int idx = lane; idx < cnt * NV; idx += 32) {
+          const int r = idx / NV, l = idx % NV;
+          const int node = *reinterpret_cast<const int *>(rec + rec_chunk_off<DIM>(r, 0) + 4 * l);
+          const double *src = v + (int64_t)node * D;
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             smem_u32(vb + (l * D + k) * CONSUMERS + r)),
+                         "l"(src + k)
+                         : "memory");
+        }
+        cp_async_arrive_noinc(vfull + s);
       }
     }
   } else {
@@ -231,85 +265,62 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
         }
       }
       const int ne_t = tm.own_count + tm.halo_count;
-      const int nch = (ne_t + CONSUMERS - 1) / CONSUMERS;
-      double vv[D][NV], vn[D][NV];
-      if (nch > 0) {  // nodal values of chunk 0
+      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
         const int s = q % STAGES;
+        const unsigned char *stage = stage_base + s * SB;
+        double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
         mbar_wait(full + s, (q / STAGES) & 1);
-        if (tid < ne_t) {
-          const int4 cc = *reinterpret_cast<const int4 *>(rec_base + s * L::stage_bytes() +
-                                                          rec_chunk_off<DIM>(tid, 0));
-          const int c[4] = {cc.x, cc.y, cc.z, cc.w};
-          int cn[NV];
-#pragma unroll
-          for (int l = 0; l < NV; ++l) cn[l] = c[l];
-          gather_v<DIM, D>(v, cn, vv);
-        }
-      }
-      for (int ch = 0; ch < nch; ++ch, ++q) {
-        const int s = q % STAGES;
-        const int c0 = ch * CONSUMERS;
-        const unsigned char *stage = rec_base + s * L::stage_bytes();
-        if (ch + 1 < nch) {  // prefetch the next chunk's nodal values
-          const uint32_t q1 = q + 1;
-          const int s1 = q1 % STAGES;
-          mbar_wait(full + s1, (q1 / STAGES) & 1);
-          if (c0 + CONSUMERS + tid < ne_t) {
-            const int4 cc = *reinterpret_cast<const int4 *>(rec_base + s1 * L::stage_bytes() +
-                                                            rec_chunk_off<DIM>(tid, 0));
-            const int c[4] = {cc.x, cc.y, cc.z, cc.w};
-            int cn[NV];
-#pragma unroll
-            for (int l = 0; l < NV; ++l) cn[l] = c[l];
-            gather_v<DIM, D>(v, cn, vn);
-          }
-        }
+        mbar_wait(vfull + s, (q / STAGES) & 1);
         const int e = c0 + tid;
-        if (e < ne_t) {
-          Elem<DIM> E;
+        const bool valid = e < ne_t;
+        const bool own = e < tm.own_count;
+        double P[D][DIM], W = 0.0;
+        Elem<DIM> E;
+        if (valid) {
           load_elem_smem<DIM>(stage, tid, E);
+          double vv[D][NV];
+#pragma unroll
+          for (int l = 0; l < NV; ++l)
+#pragma unroll
+            for (int k = 0; k < D; ++k) vv[k][l] = vb[(l * D + k) * CONSUMERS + tid];
           double F[D][DIM];
           grad_F<DIM, D>(vv, E.g, F);
-          const bool own = e < tm.own_count;
           if (has_nodes) {
-            double P[D][DIM], W = 0.0;
             bool bad;
             element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
             bad_any |= bad;
             if (WJ && own) jsum += E.vol * W;
-            double *row = staging + tid;  // [slot][comp][CONSUMERS]: conflict-free stores
-#pragma unroll
-            for (int l = 0; l < NV; ++l)
-#pragma unroll
-              for (int k = 0; k < D; ++k) {
-                double sdot = P[k][0] * E.g[0][l];
-#pragma unroll
-                for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
-                row[(l * D + k) * CONSUMERS] = sdot;
-              }
           } else if (WJ) {
             jsum += E.vol * density<DIM, MODEL>(F, mdl);
           }
         }
-        named_sync(1, CONSUMERS);
-        if (tid == 0) mbar_arrive(empty + s);
+        named_sync(1, CONSUMERS);  // every thread has read its nodal values
+        if (valid && has_nodes) {
+#pragma unroll
+          for (int l = 0; l < NV; ++l)
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              double sdot = P[k][0] * E.g[0][l];
+#pragma unroll
+              for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
+              vb[(l * D + k) * CONSUMERS + tid] = sdot;  // [slot][comp][CONSUMERS]
+            }
+        }
+        named_sync(1, CONSUMERS);  // contributions staged
         if (my_node) {
           const int lim = c0 + CONSUMERS;
           while (cur < end) {
             const int en = ents[cur];
             const int te = en >> 2;
             if (te >= lim) break;
-            const double *src = staging + (te - c0) + (en & 3) * D * CONSUMERS;
+            const double *src = vb + (te - c0) + (en & 3) * D * CONSUMERS;
 #pragma unroll
             for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
             ++cur;
           }
         }
-        named_sync(1, CONSUMERS);
-#pragma unroll
-        for (int k = 0; k < D; ++k)
-#pragma unroll
-          for (int l = 0; l < NV; ++l) vv[k][l] = vn[k][l];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
       }
       if (my_node) {
         const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(CONSUMERS + 32, 1)
         for (int k = 0; k < D; ++k)
           if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
       }
+      named_sync(1, CONSUMERS);  // all node threads done with the tile buffer
       if (tid == 0) mbar_arrive(tempty + (j & 1));
     }
     if (bad_any) atomicOr(status, 1ull);
@@ -335,7 +347,7 @@ static cudaError_t launch_exact_t(const TmaMaps &tma, const TileArgs &a, int gri
                                   cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   const size_t smem = PipeLayout<DIM>::total(stages, a.entry_cap, a.halo_cap, D);
-  const int threads = CONSUMERS + 32;
+  const int threads = CONSUMERS + 32 * PRODUCER_WARPS;
 #define FM_LAUNCH(WJV, ST)                                                            \
   do {                                                                                \
     auto k = k_tile_exact<DIM, MODEL, WJV, ST>;                                       \
