@@ -12,11 +12,11 @@
 //                    remainder -> 16-byte LDGSTS by the 32 lanes into the same
 //                    layout.  Per tile: node descriptors, node entries and halo
 //                    ids -> double-buffered tile area (bulk copies).
-//   value producer   once a stage's records landed, reads their connectivity
-//   (warp 9)         and gathers the nodal field values v[conn] into the
-//                    stage's value buffer with 8-byte LDGSTS.
-//   8 consumer       thread c: element c of the chunk from shared memory:
-//   warps            F = grad v, P' = vol * dW/dF = a F + b cof, contributions
+//   8 consumer       thread c: gathers the nodal values of its element of the
+//   warps            NEXT chunk into the stage's value buffer (8-byte LDGSTS,
+//                    one commit group per chunk), then computes element c of
+//                    this chunk from shared memory:
+//                    F = grad v, P' = vol * dW/dF = a F + b cof, contributions
 //                    P' . grad phi_l of the four local nodes, written over the
 //                    (consumed) value buffer; vol * W when the tile owns the
 //                    element.  Then as node threads they consume this chunk's
@@ -31,7 +31,7 @@
 
 namespace fm {
 
-constexpr int PRODUCER_WARPS = 2;
+constexpr int PRODUCER_WARPS = 1;
 
 template <int DIM>
 struct PipeLayout {
@@ -127,8 +127,7 @@ __global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
   const size_t HO = L::halo_off(a.entry_cap);
   double *red = reinterpret_cast<double *>(tile_base + 2 * TB);
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);
-  uint64_t *vfull = full + STAGES;
-  uint64_t *empty = vfull + STAGES;
+  uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   constexpr int CW = CONSUMERS / 32;  // consumer warps
@@ -138,7 +137,6 @@ __global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1 + 32);  // expect_tx arrival + one LDGSTS arrival per producer lane
-      mbar_init(vfull + s, 32);     // one LDGSTS arrival per value-producer lane
       mbar_init(empty + s, CW);     // one arrival per consumer warp
     }
     for (int s = 0; s < 2; ++s) {
@@ -211,127 +209,140 @@ __global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
         cp_async_arrive_noinc(full + s);
       }
     }
-  } else if (warp == CW + 1) {
-    // ------------------------------------------------------- value producer
-    uint32_t q = 0;
-    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x) {
-      const TileMeta tm = a.meta[t];
-      const int ne_t = tm.own_count + tm.halo_count;
-      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
-        const int s = q % STAGES;
-        const int cnt = min(CONSUMERS, ne_t - c0);
-        mbar_wait(full + s, (q / STAGES) & 1);
-        const unsigned char *rec = stage_base + s * SB;
+  } else {
+    // ------------------------------------------------------------- consumers
+    // Flat stream over (tile, chunk).  Per chunk q: the nodal values of chunk
+    // q+1 are gathered by each consumer thread for its own element with 8-byte
+    // LDGSTS into the stage's value buffer (one commit group per chunk), so
+    // they land while chunk q is computed; the thread then overwrites its own
+    // value slots with its contributions (no barrier needed for that).
+    bool bad_any = false;
+    int t = blockIdx.x;
+    uint32_t q = 0, j = 0;
+    auto issue_values = [&](uint32_t qq, int c0, int ne) {
+      const int s = qq % STAGES;
+      mbar_wait(full + s, (qq / STAGES) & 1);
+      if (c0 + tid < ne) {
+        const int4 cc = *reinterpret_cast<const int4 *>(stage_base + s * SB +
+                                                        rec_chunk_off<DIM>(tid, 0));
+        const int c[4] = {cc.x, cc.y, cc.z, cc.w};
         double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
-        for (int idx = lane; idx < cnt * NV; idx += 32) {
-          const int r = idx / NV, l = idx % NV;
-          const int node = *reinterpret_cast<const int *>(rec + rec_chunk_off<DIM>(r, 0) + 4 * l);
-          const double *src = v + (int64_t)node * D;
+#pragma unroll
+        for (int l = 0; l < NV; ++l) {
+          const double *src = v + (int64_t)c[l] * D;
 #pragma unroll
           for (int k = 0; k < D; ++k)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             smem_u32(vb + (l * D + k) * CONSUMERS + r)),
+                             smem_u32(vb + (l * D + k) * CONSUMERS + tid)),
                          "l"(src + k)
                          : "memory");
         }
-        cp_async_arrive_noinc(vfull + s);
       }
-    }
-  } else {
-    // ------------------------------------------------------------- consumers
-    uint32_t q = 0, j = 0;
-    bool bad_any = false;
-    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x, ++j) {
-      unsigned char *tb = tile_base + (j & 1) * TB;
-      mbar_wait(tfull + (j & 1), (j >> 1) & 1);
-      const TileMeta tm = *reinterpret_cast<const TileMeta *>(tb);
-      const int4 *desc = reinterpret_cast<const int4 *>(tb + 64);
-      const uint16_t *ents = reinterpret_cast<const uint16_t *>(tb + L::entries_off());
-      const bool has_nodes = tm.node_count > 0;
-      const bool my_node = tid < tm.node_count;
-      int cur = 0, end = 0, node = 0, outw = 0;
-      double bj[D], acc[D];
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (t < a.n_tiles_all) {
+      TileMeta tm = a.meta[t];
+      issue_values(0, 0, tm.own_count + tm.halo_count);
+      while (true) {
+        // ---- tile start
+        unsigned char *tb = tile_base + (j & 1) * TB;
+        mbar_wait(tfull + (j & 1), (j >> 1) & 1);
+        const int4 *desc = reinterpret_cast<const int4 *>(tb + 64);
+        const uint16_t *ents = reinterpret_cast<const uint16_t *>(tb + L::entries_off());
+        const bool has_nodes = tm.node_count > 0;
+        const bool my_node = tid < tm.node_count;
+        int cur = 0, end = 0, outw = 0;
+        double bj[D], acc[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
-      if (my_node) {
-        const int4 nd = desc[tid];
-        cur = nd.x;
-        end = nd.x + nd.y;
-        node = nd.z;
-        outw = nd.w;
-        if (b) {
-#pragma unroll
-          for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)node * D + k);
-        }
-      }
-      const int ne_t = tm.own_count + tm.halo_count;
-      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
-        const int s = q % STAGES;
-        const unsigned char *stage = stage_base + s * SB;
-        double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
-        mbar_wait(full + s, (q / STAGES) & 1);
-        mbar_wait(vfull + s, (q / STAGES) & 1);
-        const int e = c0 + tid;
-        const bool valid = e < ne_t;
-        const bool own = e < tm.own_count;
-        double P[D][DIM], W = 0.0;
-        Elem<DIM> E;
-        if (valid) {
-          load_elem_smem<DIM>(stage, tid, E);
-          double vv[D][NV];
-#pragma unroll
-          for (int l = 0; l < NV; ++l)
-#pragma unroll
-            for (int k = 0; k < D; ++k) vv[k][l] = vb[(l * D + k) * CONSUMERS + tid];
-          double F[D][DIM];
-          grad_F<DIM, D>(vv, E.g, F);
-          if (has_nodes) {
-            bool bad;
-            element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
-            bad_any |= bad;
-            if (WJ && own) jsum += E.vol * W;
-          } else if (WJ) {
-            jsum += E.vol * density<DIM, MODEL>(F, mdl);
-          }
-        }
-        named_sync(1, CONSUMERS);  // every thread has read its nodal values
-        if (valid && has_nodes) {
-#pragma unroll
-          for (int l = 0; l < NV; ++l)
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-              double sdot = P[k][0] * E.g[0][l];
-#pragma unroll
-              for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
-              vb[(l * D + k) * CONSUMERS + tid] = sdot;  // [slot][comp][CONSUMERS]
-            }
-        }
-        named_sync(1, CONSUMERS);  // contributions staged
+        for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
         if (my_node) {
-          const int lim = c0 + CONSUMERS;
-          while (cur < end) {
-            const int en = ents[cur];
-            const int te = en >> 2;
-            if (te >= lim) break;
-            const double *src = vb + (te - c0) + (en & 3) * D * CONSUMERS;
+          const int4 nd = desc[tid];
+          cur = nd.x;
+          end = nd.x + nd.y;
+          outw = nd.w;
+          if (b) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
-            ++cur;
+            for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
-      }
-      if (my_node) {
-        const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
-        int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+        const int ne_t = tm.own_count + tm.halo_count;
+        const int tn = t + gridDim.x;
+        const TileMeta tmn = tn < a.n_tiles_all ? a.meta[tn] : TileMeta{};
+        for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
+          const int s = q % STAGES;
+          const unsigned char *stage = stage_base + s * SB;
+          double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
+          // prefetch the nodal values of the next chunk (this tile or the next one)
+          if (c0 + CONSUMERS < ne_t)
+            issue_values(q + 1, c0 + CONSUMERS, ne_t);
+          else if (tn < a.n_tiles_all)
+            issue_values(q + 1, 0, tmn.own_count + tmn.halo_count);
+          else
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // this chunk's values landed
+          const int e = c0 + tid;
+          if (e < ne_t) {
+            const bool own = e < tm.own_count;
+            Elem<DIM> E;
+            load_elem_smem<DIM>(stage, tid, E);
+            double vv[D][NV];
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-          if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+            for (int l = 0; l < NV; ++l)
+#pragma unroll
+              for (int k = 0; k < D; ++k) vv[k][l] = vb[(l * D + k) * CONSUMERS + tid];
+            double F[D][DIM];
+            grad_F<DIM, D>(vv, E.g, F);
+            if (has_nodes) {
+              double P[D][DIM], W = 0.0;
+              bool bad;
+              element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
+              bad_any |= bad;
+              if (WJ && own) jsum += E.vol * W;
+#pragma unroll
+              for (int l = 0; l < NV; ++l)
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                  double sdot = P[k][0] * E.g[0][l];
+#pragma unroll
+                  for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
+                  vb[(l * D + k) * CONSUMERS + tid] = sdot;  // own slots: [slot][comp][thread]
+                }
+            } else if (WJ) {
+              jsum += E.vol * density<DIM, MODEL>(F, mdl);
+            }
+          }
+          named_sync(1, CONSUMERS);  // contributions staged
+          if (my_node) {
+            const int lim = c0 + CONSUMERS;
+            while (cur < end) {
+              const int en = ents[cur];
+              const int te = en >> 2;
+              if (te >= lim) break;
+              const double *src = vb + (te - c0) + (en & 3) * D * CONSUMERS;
+#pragma unroll
+              for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
+              ++cur;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
+        }
+        if (my_node) {
+          const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
+          int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+        }
+        named_sync(1, CONSUMERS);  // all node threads done with the tile buffer
+        if (tid == 0) mbar_arrive(tempty + (j & 1));
+        ++j;
+        t = tn;
+        if (t >= a.n_tiles_all) break;
+        tm = tmn;
       }
-      named_sync(1, CONSUMERS);  // all node threads done with the tile buffer
-      if (tid == 0) mbar_arrive(tempty + (j & 1));
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (bad_any) atomicOr(status, 1ull);
   }
   if (WJ) {
