@@ -752,7 +752,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   }
 
   // pipeline depth that fits the shared memory of one SM
-  c->stages = 4;
+  c->stages = 3;
   while (c->stages > 2 &&
          tile_exact_smem(dim, d, c->stages, c->entry_cap, c->halo_cap) > 227 * 1024)
     --c->stages;

@@ -1,27 +1,27 @@
 // Fused energy + exact gradient (gradients.py:124-149 with assembly.py:94-106)
-// as one persistent, warp-specialised, mbarrier-pipelined kernel.
+// as one persistent, multistage-pipelined kernel per SM.
 //
-// One CTA per SM walks its node tiles (t = blockIdx.x, += gridDim.x; tiles are
-// in Morton order of their spatial boxes so concurrently running CTAs share
-// halo elements and nodal values through L2).  Per chunk of 256 tile elements
-// a ring stage holds the element records and the gathered nodal values:
+// One CTA (256 threads) per SM walks its node tiles (t = blockIdx.x,
+// += gridDim.x; tiles are in Morton order of their spatial boxes so concurrently
+// running CTAs share halo elements and nodal values through L2).  The tile
+// element list is processed in chunks of 256 (thread c <-> element c of the
+// chunk) through a ring of STAGES shared-memory stages, STAGES-1 chunks ahead:
 //
-//   record producer  the tile's own elements are a contiguous storage range ->
-//   (warp 8)         TMA 2D tensor loads (boxes of 8..256 records, SWIZZLE_128B)
-//                    in 3D / one 1D bulk copy in 2D; halo records and the < 8
-//                    remainder -> 16-byte LDGSTS by the 32 lanes into the same
-//                    layout.  Per tile: node descriptors, node entries and halo
-//                    ids -> double-buffered tile area (bulk copies).
-//   8 consumer       thread c: gathers the nodal values of its element of the
-//   warps            NEXT chunk into the stage's value buffer (8-byte LDGSTS,
-//                    one commit group per chunk), then computes element c of
-//                    this chunk from shared memory:
-//                    F = grad v, P' = vol * dW/dF = a F + b cof, contributions
-//                    P' . grad phi_l of the four local nodes, written over the
-//                    (consumed) value buffer; vol * W when the tile owns the
-//                    element.  Then as node threads they consume this chunk's
-//                    entries (sorted by tile element) into registers: fixed
-//                    summation order, no floating-point atomics.
+//   records   the tile's own elements are a contiguous storage range -> TMA 2D
+//             tensor loads of 8..256 records with SWIZZLE_128B (3D) or one 1D
+//             bulk copy (2D), issued by thread 0 and completing on the stage's
+//             mbarrier; halo records (and a < 8 remainder) -> each thread copies
+//             its own record with 16-byte LDGSTS into the same swizzled layout.
+//   values    one chunk ahead, each thread gathers the nodal values v[conn] of
+//             its element with 8-byte LDGSTS into the stage's value buffer.
+//   compute   F = grad v, P' = vol * dW/dF = a F + b cof, the contributions
+//             P' . grad phi_l of the four local nodes overwrite the thread's own
+//             value slots; vol * W when the tile owns the element.
+//   assemble  after one barrier each node thread consumes this chunk's entries
+//             (sorted by tile element) into registers: a fixed summation order,
+//             no floating-point atomics.
+// Node descriptors and entries of the next tile are bulk-copied into a second
+// tile buffer while the current tile runs.
 //
 // J: per-thread partials over a static tile assignment -> fixed block tree ->
 // one partial per CTA, reduced in CTA order by k_finalize.
@@ -31,31 +31,26 @@
 
 namespace fm {
 
-constexpr int PRODUCER_WARPS = 1;
-
 template <int DIM>
 struct PipeLayout {
   static constexpr int RS = RecBytes<DIM>::smem;
   __host__ __device__ static size_t rec_bytes() {
     return ((size_t)CONSUMERS * RS + 1023) / 1024 * 1024;
   }
-  // nodal values [NV*D][CONSUMERS] f64, reused as the contribution staging
+  // nodal values [NV*D][CONSUMERS] f64, overwritten by the contributions
   __host__ __device__ static size_t val_bytes(int D) {
     return (((size_t)CONSUMERS * (DIM + 1) * D * 8) + 1023) / 1024 * 1024;
   }
   __host__ __device__ static size_t stage_bytes(int D) { return rec_bytes() + val_bytes(D); }
-  // tile buffer: meta (64) | node desc (256 x 16) | entries | halo ids
-  __host__ __device__ static size_t entries_off() { return 64 + (size_t)CONSUMERS * 16; }
-  __host__ __device__ static size_t halo_off(int entry_cap) {
+  // tile buffer: node desc (256 x 16) | entries
+  __host__ __device__ static size_t entries_off() { return (size_t)CONSUMERS * 16; }
+  __host__ __device__ static size_t tile_bytes(int entry_cap) {
     return entries_off() + (((size_t)entry_cap * 2 + 15) / 16) * 16;
   }
-  __host__ __device__ static size_t tile_bytes(int entry_cap, int halo_cap) {
-    return halo_off(entry_cap) + (((size_t)halo_cap * 4 + 15) / 16) * 16;
-  }
   // + 1024 for aligning the dynamic shared memory base
-  __host__ __device__ static size_t total(int stages, int entry_cap, int halo_cap, int D) {
-    return 1024 + stages * stage_bytes(D) + 2 * tile_bytes(entry_cap, halo_cap) + 32 * 8 +
-           (3 * stages + 4) * 8;
+  __host__ __device__ static size_t total(int stages, int entry_cap, int D) {
+    return 1024 + stages * stage_bytes(D) + 2 * tile_bytes(entry_cap) + 32 * 8 +
+           (stages + 2) * 8;
   }
 };
 
@@ -106,8 +101,37 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
   }
 }
 
+// Position in this CTA's chunk stream: tile t (j-th of the CTA), chunk offset c0.
+struct Cursor {
+  int t, j, c0, ne;
+  TileMeta tm;
+  __device__ void load(const TileArgs &a) {
+    if (t < a.n_tiles_all) {
+      tm = a.meta[t];
+      ne = tm.own_count + tm.halo_count;
+    } else {
+      ne = 0;
+    }
+  }
+  __device__ bool valid(const TileArgs &a) const { return t < a.n_tiles_all; }
+  __device__ void advance(const TileArgs &a) {
+    c0 += CONSUMERS;
+    if (c0 >= ne) {
+      c0 = 0;
+      t += gridDim.x;
+      ++j;
+      load(a);
+    }
+  }
+};
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int DIM, int MODEL, bool WJ, int STAGES>
-__global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
+__global__ void __launch_bounds__(CONSUMERS, 1)
     k_tile_exact(const __grid_constant__ TmaMaps tma, TileArgs a, const double *__restrict__ v,
                  const double *__restrict__ b, double *__restrict__ g,
                  double *__restrict__ jpart, unsigned long long *status, ModelArgs mdl) {
@@ -123,106 +147,77 @@ __global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
   const size_t SB = L::stage_bytes(D);
   unsigned char *stage_base = smem;
   unsigned char *tile_base = stage_base + STAGES * SB;
-  const size_t TB = L::tile_bytes(a.entry_cap, a.halo_cap);
-  const size_t HO = L::halo_off(a.entry_cap);
+  const size_t TB = L::tile_bytes(a.entry_cap);
   double *red = reinterpret_cast<double *>(tile_base + 2 * TB);
-  uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);
-  uint64_t *empty = full + STAGES;
-  uint64_t *tfull = empty + STAGES;
-  uint64_t *tempty = tfull + 2;
-  constexpr int CW = CONSUMERS / 32;  // consumer warps
-
+  uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // TMA / bulk part of a stage
+  uint64_t *tfull = full + STAGES;                          // tile buffers
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1 + 32);  // expect_tx arrival + one LDGSTS arrival per producer lane
-      mbar_init(empty + s, CW);     // one arrival per consumer warp
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(tfull + s, 1);
-      mbar_init(tempty + s, 1);
-    }
+    for (int s = 0; s < STAGES; ++s) mbar_init(full + s, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tfull + 1, 1);
     fence_barrier_init();
   }
   __syncthreads();
 
-  double jsum = 0.0;
-  if (warp == CW) {
-    // ------------------------------------------------------- record producer
-    uint32_t q = 0, j = 0;
-    for (int t = blockIdx.x; t < a.n_tiles_all; t += gridDim.x, ++j) {
+  // tile buffer j&1 <- node descriptors + entries of tile t (thread 0)
+  auto issue_tile = [&](int t, int j) {
+    if (tid == 0 && t < a.n_tiles_all) {
       const TileMeta tm = a.meta[t];
       unsigned char *tb = tile_base + (j & 1) * TB;
-      mbar_wait(tempty + (j & 1), ((j >> 1) & 1) ^ 1);
-      const int32_t *halo_s = reinterpret_cast<const int32_t *>(tb + HO);
-      if (lane == 0) {
-        *reinterpret_cast<TileMeta *>(tb) = tm;
-        const uint32_t nb = (uint32_t)tm.node_count * 16;
-        const uint32_t eb = (uint32_t)((tm.entry_count * 2 + 15) / 16) * 16;
-        const uint32_t hb = (uint32_t)((tm.halo_count * 4 + 15) / 16) * 16;
-        mbar_arrive_expect_tx(tfull + (j & 1), nb + eb + hb);
-        if (nb) bulk_g2s(tb + 64, a.node_desc + tm.node_begin, nb, tfull + (j & 1));
-        if (eb) bulk_g2s(tb + L::entries_off(), a.entries + tm.entry_begin, eb, tfull + (j & 1));
-        if (hb) bulk_g2s(tb + HO, a.halo_ids + tm.halo_begin, hb, tfull + (j & 1));
-      }
-      __syncwarp();
-      bool halo_ready = false;
-      const int ne_t = tm.own_count + tm.halo_count;
-      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
-        const int s = q % STAGES;
-        const int cnt = min(CONSUMERS, ne_t - c0);
-        const int n_own = max(0, min(cnt, tm.own_count - c0));
-        // 3D: TMA boxes cover the 8-aligned part of the own range; 2D: one bulk copy
-        const int n_bulk = DIM == 3 ? (n_own & ~7) : n_own;
-        if (!halo_ready && cnt > n_bulk && c0 + cnt > tm.own_count) {
-          mbar_wait(tfull + (j & 1), (j >> 1) & 1);  // halo ids arrive with the tile buffer
-          halo_ready = true;
-        }
-        mbar_wait(empty + s, ((q / STAGES) & 1) ^ 1);
-        unsigned char *dst = stage_base + s * SB;
-        if (lane == 0) {
-          mbar_arrive_expect_tx(full + s, (uint32_t)n_bulk * RB);
-          if constexpr (DIM == 3) {
-            int off = 0;
+      const uint32_t nb = (uint32_t)tm.node_count * 16;
+      const uint32_t eb = (uint32_t)((tm.entry_count * 2 + 15) / 16) * 16;
+      mbar_arrive_expect_tx(tfull + (j & 1), nb + eb);
+      if (nb) bulk_g2s(tb, a.node_desc + tm.node_begin, nb, tfull + (j & 1));
+      if (eb) bulk_g2s(tb + L::entries_off(), a.entries + tm.entry_begin, eb, tfull + (j & 1));
+    }
+  };
+  // records of the chunk at cursor x into stage s; src = this thread's record id
+  auto issue_records = [&](const Cursor &x, int s, int src) {
+    if (x.valid(a)) {
+      unsigned char *dst = stage_base + s * SB;
+      const int cnt = min(CONSUMERS, x.ne - x.c0);
+      const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
+      const int n_bulk = DIM == 3 ? (n_own & ~7) : n_own;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(full + s, (uint32_t)n_bulk * RB);
+        if constexpr (DIM == 3) {
+          int off = 0;
 #pragma unroll 1
-            for (int k = 5; k >= 0; --k) {
-              const int rows = 8 << k;
-              if (n_bulk - off >= rows) {
-                tma_load_2d(dst + off * 128, &tma.box[k], 0, tm.own_begin + c0 + off, full + s);
-                off += rows;
-              }
+          for (int k = 5; k >= 0; --k) {
+            const int rows = 8 << k;
+            if (n_bulk - off >= rows) {
+              tma_load_2d(dst + off * 128, &tma.box[k], 0, x.tm.own_begin + x.c0 + off, full + s);
+              off += rows;
             }
-          } else {
-            if (n_bulk)
-              bulk_g2s(dst, a.aos + (int64_t)(tm.own_begin + c0) * RB, (uint32_t)n_bulk * RB,
-                       full + s);
           }
+        } else {
+          if (n_bulk)
+            bulk_g2s(dst, a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)n_bulk * RB,
+                     full + s);
         }
-        // remaining records of the chunk: 16-byte LDGSTS, lane-parallel
-        for (int idx = lane; idx < (cnt - n_bulk) * NCH; idx += 32) {
-          const int r = n_bulk + idx / NCH, c = idx % NCH;
-          const int e = c0 + r;
-          const int src = e < tm.own_count ? tm.own_begin + e : halo_s[e - tm.own_count];
-          cp_async16(dst + rec_chunk_off<DIM>(r, c), a.aos + (int64_t)src * RB + c * 16);
-        }
-        cp_async_arrive_noinc(full + s);
+      }
+      if (tid >= n_bulk && tid < cnt) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+          cp_async16(dst + rec_chunk_off<DIM>(tid, c), a.aos + (int64_t)src * RB + c * 16);
       }
     }
-  } else {
-    // ------------------------------------------------------------- consumers
-    // Flat stream over (tile, chunk).  Per chunk q: the nodal values of chunk
-    // q+1 are gathered by each consumer thread for its own element with 8-byte
-    // LDGSTS into the stage's value buffer (one commit group per chunk), so
-    // they land while chunk q is computed; the thread then overwrites its own
-    // value slots with its contributions (no barrier needed for that).
-    bool bad_any = false;
-    int t = blockIdx.x;
-    uint32_t q = 0, j = 0;
-    auto issue_values = [&](uint32_t qq, int c0, int ne) {
-      const int s = qq % STAGES;
+    cp_commit();
+  };
+  // record id of this thread's row at cursor x (halo ids are read from global)
+  auto src_of = [&](const Cursor &x) -> int {
+    if (!x.valid(a)) return 0;
+    const int e = x.c0 + tid;
+    if (e >= x.ne) return 0;
+    return e < x.tm.own_count ? x.tm.own_begin + e
+                              : __ldg(a.halo_ids + x.tm.halo_begin + e - x.tm.own_count);
+  };
+  // nodal values of this thread's element at cursor x (stage s) -> value buffer
+  auto issue_values = [&](const Cursor &x, int s, uint32_t qq) {
+    if (x.valid(a)) {
       mbar_wait(full + s, (qq / STAGES) & 1);
-      if (c0 + tid < ne) {
+      if (x.c0 + tid < x.ne) {
         const int4 cc = *reinterpret_cast<const int4 *>(stage_base + s * SB +
                                                         rec_chunk_off<DIM>(tid, 0));
         const int c[4] = {cc.x, cc.y, cc.z, cc.w};
@@ -238,113 +233,128 @@ __global__ void __launch_bounds__(CONSUMERS + 32 * PRODUCER_WARPS, 1)
                          : "memory");
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    if (t < a.n_tiles_all) {
-      TileMeta tm = a.meta[t];
-      issue_values(0, 0, tm.own_count + tm.halo_count);
-      while (true) {
-        // ---- tile start
-        unsigned char *tb = tile_base + (j & 1) * TB;
-        mbar_wait(tfull + (j & 1), (j >> 1) & 1);
-        const int4 *desc = reinterpret_cast<const int4 *>(tb + 64);
-        const uint16_t *ents = reinterpret_cast<const uint16_t *>(tb + L::entries_off());
-        const bool has_nodes = tm.node_count > 0;
-        const bool my_node = tid < tm.node_count;
-        int cur = 0, end = 0, outw = 0;
-        double bj[D], acc[D];
+    }
+    cp_commit();
+  };
+
+  double jsum = 0.0;
+  bool bad_any = false;
+  // ---- prologue: records of chunks 0..STAGES-2, values of chunk 0, tile 0/1 buffers
+  Cursor comp{(int)blockIdx.x, 0, 0, 0, TileMeta{}};
+  comp.load(a);
+  Cursor iss = comp;
+  issue_tile(comp.t, 0);
+  issue_tile(comp.t + gridDim.x, 1);
+  int src_next = src_of(iss);
+  for (int k = 0; k < STAGES - 1; ++k) {
+    issue_records(iss, k, src_next);
+    iss.advance(a);
+    src_next = src_of(iss);
+  }
+  cp_wait<STAGES - 2>();  // records of chunk 0 (own LDGSTS group)
+  issue_values(comp, 0, 0);
+
+  uint32_t q = 0;
+  while (comp.valid(a)) {
+    // ---- tile start
+    const int j = comp.j;
+    const TileMeta tm = comp.tm;
+    const unsigned char *tb = tile_base + (j & 1) * TB;
+    mbar_wait(tfull + (j & 1), (j >> 1) & 1);
+    const int4 *desc = reinterpret_cast<const int4 *>(tb);
+    const uint16_t *ents = reinterpret_cast<const uint16_t *>(tb + L::entries_off());
+    const bool has_nodes = tm.node_count > 0;
+    const bool my_node = tid < tm.node_count;
+    int cur = 0, end = 0, outw = 0;
+    double bj[D], acc[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
-        if (my_node) {
-          const int4 nd = desc[tid];
-          cur = nd.x;
-          end = nd.x + nd.y;
-          outw = nd.w;
-          if (b) {
+    for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
+    if (my_node) {
+      const int4 nd = desc[tid];
+      cur = nd.x;
+      end = nd.x + nd.y;
+      outw = nd.w;
+      if (b) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
-          }
-        }
-        const int ne_t = tm.own_count + tm.halo_count;
-        const int tn = t + gridDim.x;
-        const TileMeta tmn = tn < a.n_tiles_all ? a.meta[tn] : TileMeta{};
-        for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
-          const int s = q % STAGES;
-          const unsigned char *stage = stage_base + s * SB;
-          double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
-          // prefetch the nodal values of the next chunk (this tile or the next one)
-          if (c0 + CONSUMERS < ne_t)
-            issue_values(q + 1, c0 + CONSUMERS, ne_t);
-          else if (tn < a.n_tiles_all)
-            issue_values(q + 1, 0, tmn.own_count + tmn.halo_count);
-          else
-            asm volatile("cp.async.commit_group;" ::: "memory");
-          asm volatile("cp.async.wait_group 1;" ::: "memory");  // this chunk's values landed
-          const int e = c0 + tid;
-          if (e < ne_t) {
-            const bool own = e < tm.own_count;
-            Elem<DIM> E;
-            load_elem_smem<DIM>(stage, tid, E);
-            double vv[D][NV];
-#pragma unroll
-            for (int l = 0; l < NV; ++l)
-#pragma unroll
-              for (int k = 0; k < D; ++k) vv[k][l] = vb[(l * D + k) * CONSUMERS + tid];
-            double F[D][DIM];
-            grad_F<DIM, D>(vv, E.g, F);
-            if (has_nodes) {
-              double P[D][DIM], W = 0.0;
-              bool bad;
-              element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
-              bad_any |= bad;
-              if (WJ && own) jsum += E.vol * W;
-#pragma unroll
-              for (int l = 0; l < NV; ++l)
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                  double sdot = P[k][0] * E.g[0][l];
-#pragma unroll
-                  for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
-                  vb[(l * D + k) * CONSUMERS + tid] = sdot;  // own slots: [slot][comp][thread]
-                }
-            } else if (WJ) {
-              jsum += E.vol * density<DIM, MODEL>(F, mdl);
-            }
-          }
-          named_sync(1, CONSUMERS);  // contributions staged
-          if (my_node) {
-            const int lim = c0 + CONSUMERS;
-            while (cur < end) {
-              const int en = ents[cur];
-              const int te = en >> 2;
-              if (te >= lim) break;
-              const double *src = vb + (te - c0) + (en & 3) * D * CONSUMERS;
-#pragma unroll
-              for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
-              ++cur;
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty + s);  // this warp is done with the stage
-        }
-        if (my_node) {
-          const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
-          int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
-#pragma unroll
-          for (int k = 0; k < D; ++k)
-            if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
-        }
-        named_sync(1, CONSUMERS);  // all node threads done with the tile buffer
-        if (tid == 0) mbar_arrive(tempty + (j & 1));
-        ++j;
-        t = tn;
-        if (t >= a.n_tiles_all) break;
-        tm = tmn;
+        for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (bad_any) atomicOr(status, 1ull);
+    const int ne_t = comp.ne;
+    for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
+      const int s = q % STAGES;
+      // 1. records of chunk q+STAGES-1 into the stage freed by chunk q-1
+      issue_records(iss, (q + STAGES - 1) % STAGES, src_next);
+      iss.advance(a);
+      src_next = src_of(iss);
+      // 2. values of chunk q+1 (its records: TMA mbarrier + own LDGSTS group)
+      Cursor nx = comp;
+      nx.advance(a);
+      cp_wait<2 * STAGES - 4>();
+      issue_values(nx, (q + 1) % STAGES, q + 1);
+      // 3. compute chunk q (its values: the group committed one iteration ago)
+      cp_wait<2>();
+      const unsigned char *stage = stage_base + s * SB;
+      double *vb = reinterpret_cast<double *>(stage_base + s * SB + L::rec_bytes());
+      const int e = c0 + tid;
+      if (e < ne_t) {
+        const bool own = e < tm.own_count;
+        Elem<DIM> E;
+        load_elem_smem<DIM>(stage, tid, E);
+        double vv[D][NV];
+#pragma unroll
+        for (int l = 0; l < NV; ++l)
+#pragma unroll
+          for (int k = 0; k < D; ++k) vv[k][l] = vb[(l * D + k) * CONSUMERS + tid];
+        double F[D][DIM];
+        grad_F<DIM, D>(vv, E.g, F);
+        if (has_nodes) {
+          double P[D][DIM], W = 0.0;
+          bool bad;
+          element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
+          bad_any |= bad;
+          if (WJ && own) jsum += E.vol * W;
+#pragma unroll
+          for (int l = 0; l < NV; ++l)
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              double sdot = P[k][0] * E.g[0][l];
+#pragma unroll
+              for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
+              vb[(l * D + k) * CONSUMERS + tid] = sdot;  // own slots: [slot][comp][thread]
+            }
+        } else if (WJ) {
+          jsum += E.vol * density<DIM, MODEL>(F, mdl);
+        }
+      }
+      __syncthreads();  // contributions staged
+      // 4. assemble: node threads consume this chunk's entries
+      if (my_node) {
+        const int lim = c0 + CONSUMERS;
+        while (cur < end) {
+          const int en = ents[cur];
+          const int te = en >> 2;
+          if (te >= lim) break;
+          const double *src = vb + (te - c0) + (en & 3) * D * CONSUMERS;
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
+          ++cur;
+        }
+      }
+      __syncthreads();  // stage s free for chunk q+STAGES
+      comp.advance(a);
+    }
+    if (my_node) {
+      const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
+      int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+    }
+    // tile buffer j&1 is free (last barrier above): prefetch tile j+2 into it
+    issue_tile(comp.t + gridDim.x, j + 2);
   }
+  cp_wait<0>();
+  if (bad_any) atomicOr(status, 1ull);
   if (WJ) {
     double r = block_sum(jsum, red);
     if (tid == 0) jpart[blockIdx.x] = r;
@@ -357,28 +367,28 @@ static cudaError_t launch_exact_t(const TmaMaps &tma, const TileArgs &a, int gri
                                   double *jpart, unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  const size_t smem = PipeLayout<DIM>::total(stages, a.entry_cap, a.halo_cap, D);
-  const int threads = CONSUMERS + 32 * PRODUCER_WARPS;
+  const size_t smem = PipeLayout<DIM>::total(stages, a.entry_cap, D);
 #define FM_LAUNCH(WJV, ST)                                                            \
   do {                                                                                \
     auto k = k_tile_exact<DIM, MODEL, WJV, ST>;                                       \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k<<<grid, threads, smem, s>>>(tma, a, v, b, g, jpart, status, m);                 \
+    k<<<grid, CONSUMERS, smem, s>>>(tma, a, v, b, g, jpart, status, m);               \
   } while (0)
+  // the cp.async group accounting of the kernel (wait_group 2*STAGES-4) holds
+  // for STAGES = 2 and 3
   if (stages == 3) {
     if (wj) FM_LAUNCH(true, 3); else FM_LAUNCH(false, 3);
-  } else if (stages == 2) {
-    if (wj) FM_LAUNCH(true, 2); else FM_LAUNCH(false, 2);
   } else {
-    if (wj) FM_LAUNCH(true, 4); else FM_LAUNCH(false, 4);
+    if (wj) FM_LAUNCH(true, 2); else FM_LAUNCH(false, 2);
   }
 #undef FM_LAUNCH
   return cudaGetLastError();
 }
 
 size_t tile_exact_smem(int dim, int d, int stages, int entry_cap, int halo_cap) {
-  return dim == 3 ? PipeLayout<3>::total(stages, entry_cap, halo_cap, d)
-                  : PipeLayout<2>::total(stages, entry_cap, halo_cap, d);
+  (void)halo_cap;
+  return dim == 3 ? PipeLayout<3>::total(stages, entry_cap, d)
+                  : PipeLayout<2>::total(stages, entry_cap, d);
 }
 
 cudaError_t launch_tile_exact(int dim, int model, const TmaMaps &tma, const TileArgs &a,
