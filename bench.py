@@ -158,6 +158,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extras", action="store_true",
+                    help="also time the energy-only and FD kernels")
     ap.add_argument("--tile-nodes", type=int, default=0)
     ap.add_argument("--box", type=str, default="")
     args = ap.parse_args()
@@ -245,6 +247,25 @@ def main():
         ms, kms = float(tt[0]), float(tt[1])
     dm.check()
 
+    extras = {}
+    if args.extras and world == 1:
+        # secondary kernels on the same problem: energy-only pass and FD gradient
+        def timed(fn, n):
+            fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(n):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / n
+        e_ms = timed(lambda: dm.energy(v, model, b, out=J), 20)
+        fd_ms = timed(lambda: dm.numeric_gradient(v, model, b, 1e-8, g=torch.empty_like(g)), 3)
+        extras = {"energy_only_ms": e_ms, "energy_only_Melem_s": ne_total / e_ms / 1e3,
+                  "fd_grad_ms": fd_ms, "fd_grad_Melem_s": ne_total / fd_ms / 1e3}
+        dm.check()
+
     # ---- end to end through the public device API, host buffers ----------
     v_host = v.cpu().pin_memory()
     g_host = torch.empty(g.shape, dtype=torch.float64).pin_memory()
@@ -314,6 +335,8 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if extras:
+            line["extra"] = extras
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -165,29 +165,115 @@ __global__ void k_lower_bounds_u32(int n, int64_t len, const uint32_t *sorted, i
   }
 }
 
+// records (vol | dphi | closure indices, filled by k_fill_loc) + conn4 in storage order
 template <int DIM>
 __global__ void k_build_aos(int64_t ne, const int32_t *s2o, const int64_t *conn, const double *vol,
-                            const double *dphi, uint8_t *aos) {
+                            const double *dphi, uint8_t *aos, int4 *conn4) {
   constexpr int NV = DIM + 1;
+  constexpr int NF = RecBytes<DIM>::value / 8;  // f64 words per record
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < ne;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = s2o[s];
-    uint8_t *rec = aos + s * RecBytes<DIM>::value;
-    int32_t *ci = reinterpret_cast<int32_t *>(rec);
-    double *dd = reinterpret_cast<double *>(rec);
-    for (int l = 0; l < NV; ++l) ci[l] = (int32_t)conn[e * NV + l];
-    if (DIM == 3) {
-      dd[2] = vol[e];
-      for (int m = 0; m < 3; ++m)
-        for (int l = 0; l < 4; ++l) dd[3 + m * 4 + l] = dphi[((int64_t)m * ne + e) * 4 + l];
-      ci[30] = (int32_t)e;
-      ci[31] = 0;
+    double *dd = reinterpret_cast<double *>(aos + s * RecBytes<DIM>::value);
+    dd[0] = vol[e];
+    for (int m = 0; m < DIM; ++m)
+      for (int l = 0; l < NV; ++l) dd[1 + m * NV + l] = dphi[((int64_t)m * ne + e) * NV + l];
+    for (int k = 1 + DIM * NV; k < NF; ++k) dd[k] = 0.0;
+    int4 c;
+    c.x = (int)conn[e * NV];
+    c.y = (int)conn[e * NV + 1];
+    c.z = (int)conn[e * NV + 2];
+    c.w = DIM == 3 ? (int)conn[e * NV + 3] : (int)e;
+    conn4[s] = c;
+  }
+}
+
+// (tile, node) keys of every element a tile visits: node tiles from the unique
+// (tile, halo?, element) list, orphan tiles from their own storage range
+__global__ void k_closure_keys(int64_t M, const uint64_t *ukeys, int64_t n_orph, int64_t orph0,
+                               int n_tiles, int ot, const int32_t *s2o, const int64_t *conn,
+                               int nv, uint64_t *keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + n_orph;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t t;
+    int64_t e;
+    if (i < M) {
+      t = ukeys[i] >> 33;
+      e = (int64_t)(ukeys[i] & 0xffffffffull);
     } else {
-      ci[3] = (int32_t)e;
-      dd[2] = vol[e];
-      for (int m = 0; m < 2; ++m)
-        for (int l = 0; l < 3; ++l) dd[3 + m * 3 + l] = dphi[((int64_t)m * ne + e) * 3 + l];
-      dd[9] = 0.0;
+      const int64_t o = i - M;
+      t = (uint64_t)(n_tiles + o / ot);
+      e = s2o[orph0 + o];
+    }
+    for (int l = 0; l < nv; ++l) keys[i * nv + l] = (t << 32) | (uint64_t)conn[e * nv + l];
+  }
+}
+
+__global__ void k_lower_bounds_u64(int n, int64_t len, const uint64_t *sorted, int shift,
+                                   int32_t *out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n; t += gridDim.x * blockDim.x) {
+    const uint64_t key = (uint64_t)t << shift;
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sorted[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    out[t] = (int32_t)lo;
+  }
+}
+
+__global__ void k_closure_ids(int64_t C, const uint64_t *ckeys, const int32_t *cstart,
+                              const int32_t *cbegin, int32_t *closure) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(ckeys[i] >> 32);
+    closure[cbegin[t] + (i - cstart[t])] = (int32_t)(ckeys[i] & 0xffffffffull);
+  }
+}
+
+// closure indices of every (tile, element): own -> record, halo -> halo_loc
+template <int DIM>
+__global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int64_t orph0,
+                           int n_tiles, int ot, const int32_t *s2o, const int32_t *o2s,
+                           const int64_t *conn, const uint64_t *ckeys, const int32_t *cstart,
+                           const int32_t *split, const int32_t *halo_begin, uint8_t *aos,
+                           uint2 *halo_loc, unsigned long long *overflow) {
+  constexpr int NV = DIM + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + n_orph;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int t;
+    int64_t e, s;
+    bool halo = false;
+    if (i < M) {
+      t = (int)(ukeys[i] >> 33);
+      halo = (ukeys[i] >> 32) & 1;
+      e = (int64_t)(ukeys[i] & 0xffffffffull);
+      s = o2s[e];
+    } else {
+      const int64_t o = i - M;
+      t = n_tiles + (int)(o / ot);
+      s = orph0 + o;
+      e = s2o[s];
+    }
+    const int64_t lo0 = cstart[t], hi0 = cstart[t + 1];
+    uint64_t packed = 0;
+    for (int l = 0; l < NV; ++l) {
+      const uint64_t key = ((uint64_t)t << 32) | (uint64_t)conn[e * NV + l];
+      int64_t lo = lo0, hi = hi0;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ckeys[mid] < key) lo = mid + 1; else hi = mid;
+      }
+      const int64_t idx = lo - lo0;
+      if (idx > 0xffff || lo >= hi0 || ckeys[lo] != key) atomicAdd(overflow, 1ull);
+      packed |= (uint64_t)(idx & 0xffff) << (16 * l);
+    }
+    if (halo) {
+      halo_loc[halo_begin[t] + (i - split[t])] =
+          make_uint2((unsigned)(packed & 0xffffffffull), (unsigned)(packed >> 32));
+    } else {
+      uint64_t *w = reinterpret_cast<uint64_t *>(aos + s * RecBytes<DIM>::value);
+      w[1 + DIM * NV] = packed;  // the 8 bytes after vol | dphi
     }
   }
 }
@@ -320,39 +406,6 @@ template <class F> static cudaError_t cub_call(F f, cudaStream_t s) {
   e = tmp.alloc(bytes, s);
   if (e != cudaSuccess) return e;
   return f(tmp.p, bytes);
-}
-
-// 3D element records viewed as a 2D tensor [ne rows][16 f64]: six box heights
-// 8..256 with the 128-byte swizzle (chunk ^ row % 8) the consumers read with.
-static int make_record_tmaps(const uint8_t *aos, int64_t ne, TmaMaps *out) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) !=
-            cudaSuccess ||
-        qr != cudaDriverEntryPointSuccess || !fn) {
-      set_error("cuTensorMapEncodeTiled is not available from the driver");
-      return FM_CUDA_ERROR;
-    }
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  static_assert(sizeof(CUtensorMap) == sizeof(TmaDesc), "tensor map size");
-  for (int k = 0; k < 6; ++k) {
-    cuuint64_t dims[2] = {16, (cuuint64_t)ne};
-    cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {16, (cuuint32_t)(8 << k)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(reinterpret_cast<CUtensorMap *>(&out->box[k]),
-                        CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)aos, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
-      return FM_CUDA_ERROR;
-    }
-  }
-  return FM_OK;
 }
 
 struct TimedLaunch {
@@ -596,17 +649,14 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
 
   const int rb = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
   CK(dmalloc(&c->aos, (size_t)ne * rb, &B));
+  CK(dmalloc(&c->conn4, ne, &B));
   if (dim == 3)
     k_build_aos<3><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
-                                                     m->dphi, c->aos);
+                                                     m->dphi, c->aos, c->conn4);
   else
     k_build_aos<2><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
-                                                     m->dphi, c->aos);
+                                                     m->dphi, c->aos, c->conn4);
   CK(cudaGetLastError());
-  if (dim == 3) {  // element records as a (ne x 128 B) tensor for the TMA loads
-    int st = make_record_tmaps(c->aos, ne, &c->tma);
-    if (st) return fail(st);
-  }
 
   // 4. tile element lists (own + halo) ----------------------------------------
   int64_t M = 0;
@@ -705,10 +755,92 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->n_tiles_all = (int)hm.size();
   c->n_tile_elems = M;
   c->entry_cap = (c->max_tile_entries + 7) / 8 * 8;
-  c->halo_cap = (max_halo + 3) / 4 * 4;
+  (void)max_halo;
+  CK(dmalloc(&c->halo_ids, halo_total + 4, &B));
+  CK(dmalloc(&c->halo_loc, halo_total + 4, &B));
+  CK(cudaMemsetAsync(c->halo_loc, 0, (halo_total + 4) * 8, s));
+
+  // 4b. node closures of every tile and the 16-bit closure indices ---------------
+  {
+    const int NTA = c->n_tiles_all;
+    const int64_t NK = (M + n_orph) * nv;
+    Scratch ck, ck2, cu, nsel, cstart;
+    CK(ck.alloc(NK * 8, s));
+    CK(ck2.alloc(NK * 8, s));
+    CK(cu.alloc(NK * 8, s));
+    CK(nsel.alloc(8, s));
+    CK(cstart.alloc((NTA + 1) * 4, s));
+    k_closure_keys<<<grid_for(M + n_orph, 256), 256, 0, s>>>(
+        M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig, m->conn,
+        nv, ck.as<uint64_t>());
+    CK(cudaGetLastError());
+    cub::DoubleBuffer<uint64_t> dk(ck.as<uint64_t>(), ck2.as<uint64_t>());
+    const int end_bit = 32 + bits_for((uint64_t)NTA);
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, dk, NK, 0, end_bit, s);
+    }, s));
+    uint64_t *cuk = cu.as<uint64_t>();
+    int64_t *ns = nsel.as<int64_t>();
+    CK(cub_call([&](void *t, size_t &b) {
+      return cub::DeviceSelect::Unique(t, b, dk.Current(), cuk, ns, NK, s);
+    }, s));
+    int64_t C = 0;
+    CK(cudaMemcpyAsync(&C, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    k_lower_bounds_u64<<<grid_for(NTA + 1, 256), 256, 0, s>>>(NTA, C, cuk, 32,
+                                                              cstart.as<int32_t>());
+    CK(cudaGetLastError());
+    std::vector<int32_t> h_cs(NTA + 1), h_cb(NTA + 1);
+    CK(cudaMemcpyAsync(h_cs.data(), cstart.p, (NTA + 1) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int64_t ctot = 0;
+    c->clo_cap = 0;
+    for (int t = 0; t < NTA; ++t) {
+      const int cnt = h_cs[t + 1] - h_cs[t];
+      hm[t].clo_begin = (int)ctot;
+      hm[t].clo_count = cnt;
+      h_cb[t] = (int)ctot;
+      ctot += (cnt + 3) / 4 * 4;
+      c->clo_cap = std::max(c->clo_cap, cnt);
+    }
+    h_cb[NTA] = (int)ctot;
+    c->clo_cap = (c->clo_cap + 3) / 4 * 4;
+    if (c->clo_cap > 65536) {
+      set_error("a tile's node closure exceeds 65536 nodes; use smaller tiles");
+      return fail(FM_INVALID_ARG);
+    }
+    CK(dmalloc(&c->closure, ctot + 4, &B));
+    CK(cudaMemsetAsync(c->closure, 0, (ctot + 4) * 4, s));
+    Scratch cb, hb, ovf;
+    CK(cb.alloc((NTA + 1) * 4, s));
+    CK(hb.alloc((n_tiles + 1) * 4, s));
+    CK(ovf.alloc(8, s));
+    CK(cudaMemsetAsync(ovf.p, 0, 8, s));
+    CK(cudaMemcpyAsync(cb.p, h_cb.data(), (NTA + 1) * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(hb.p, h_halo_begin.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
+    k_closure_ids<<<grid_for(C, 256), 256, 0, s>>>(C, cuk, cstart.as<int32_t>(), cb.as<int32_t>(),
+                                                   c->closure);
+    if (dim == 3)
+      k_fill_loc<3><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
+          M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
+          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tsplit.as<int32_t>(),
+          hb.as<int32_t>(), c->aos, c->halo_loc, ovf.as<unsigned long long>());
+    else
+      k_fill_loc<2><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
+          M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
+          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tsplit.as<int32_t>(),
+          hb.as<int32_t>(), c->aos, c->halo_loc, ovf.as<unsigned long long>());
+    CK(cudaGetLastError());
+    unsigned long long h_ovf = 0;
+    CK(cudaMemcpyAsync(&h_ovf, ovf.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h_ovf) {
+      set_error("internal error: element node missing from its tile closure");
+      return fail(FM_CUDA_ERROR);
+    }
+  }
   CK(dmalloc(&c->meta, hm.size(), &B));
   CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
-  CK(dmalloc(&c->halo_ids, halo_total + 4, &B));
   CK(dmalloc(&c->flags, M + 16, &B));
   CK(dmalloc(&c->node_desc, std::max<int64_t>(nfree, 1), &B));
   CK(dmalloc(&c->node_entries, entry_total + 8, &B));
@@ -751,14 +883,17 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
   }
 
-  // pipeline depth that fits the shared memory of one SM
-  c->stages = 3;
-  while (c->stages > 2 &&
-         tile_exact_smem(dim, d, c->stages, c->entry_cap, c->halo_cap) > 227 * 1024)
-    --c->stages;
-  if (tile_exact_smem(dim, d, c->stages, c->entry_cap, c->halo_cap) > 227 * 1024) {
-    set_error("tile tables exceed shared memory; use smaller tiles");
-    return fail(FM_INVALID_ARG);
+  // CTAs per SM that fit the shared memory (228 KB per SM, 1 KB reserved per CTA)
+  {
+    const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap);
+    if (sm <= 113 * 1024)
+      c->ctas_per_sm = 2;
+    else if (sm <= 227 * 1024)
+      c->ctas_per_sm = 1;
+    else {
+      set_error("tile tables exceed shared memory; use smaller tiles");
+      return fail(FM_INVALID_ARG);
+    }
   }
 
   // scratch ------------------------------------------------------------------
@@ -788,9 +923,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
 
 int fm_ctx_destroy(fm_ctx *c) {
   if (!c) return FM_OK;
-  void *ptrs[] = {c->aos,       c->meta,      c->halo_ids,  c->flags,   c->node_desc,
-                  c->node_entries, c->free_node, c->free_out, c->rank_of, c->storage_to_orig,
-                  c->free_mask, c->jpart,     c->dotpart,   c->status};
+  void *ptrs[] = {c->aos,       c->conn4,     c->meta,      c->halo_ids,  c->halo_loc,
+                  c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
+                  c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
+                  c->dotpart,   c->status};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -814,8 +950,8 @@ int fm_energy(fm_ctx *c, const fm_model *model, const double *v, const double *b
   ModelArgs ma = model_args(model);
   {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_energy(c->dim, model->kind, c->aos, c->ne, c->n_energy_blocks, v, c->jpart,
-                          densities, ma, s));
+    FM_CUDA(launch_energy(c->dim, model->kind, c->tile_args(), c->ne, c->n_energy_blocks, v,
+                          c->jpart, densities, ma, s));
   }
   int nd = 0;
   if (b) {
@@ -838,11 +974,11 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   const bool wj = J_out != nullptr;
   TileArgs ta = c->tile_args();
   if (!wj) ta.n_tiles_all = c->n_tiles;  // J-only orphan tiles not needed
-  const int grid = std::min(c->n_sm, std::max(1, ta.n_tiles_all));
+  const int grid = std::min(c->n_sm * c->ctas_per_sm, std::max(1, ta.n_tiles_all));
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, c->tma, ta, grid, c->stages, wj, v, b, g,
-                              c->jpart, c->status, ma, s));
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, wj, v, b, g, c->jpart, c->status,
+                              ma, s));
     c->launches++;
   }
   if (wj) {

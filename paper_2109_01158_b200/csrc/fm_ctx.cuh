@@ -2,19 +2,20 @@
 // mesh.py:31-53 / patches.py:22-34, re-laid out for sm_100a) and the device
 // functions shared by the evaluation kernels.
 //
-// Element records (AoS, one per element, storage order = grouped by owner tile):
-//   3D: 128 B = int32 conn[4] | f64 vol | f64 dphi[3][4] | int32 orig | pad
-//   2D:  80 B = int32 conn[3] | int32 orig | f64 vol | f64 dphi[2][3] | pad
-// A record is one 128-byte line (3D): a gather by element id costs one line and
-// brings vol, dphi and conn together.  In shared memory 3D records are stored
-// with a 144-byte stride (9 x 16 B, odd) so that lane i reading record i is
-// bank-conflict free; 80 B (5 x 16 B) is already odd.
+// Element records (AoS, storage order = grouped by owner tile, 16-B multiples
+// with an ODD number of 16-B chunks so that lane i reading record i from shared
+// memory is bank-conflict free):
+//   3D: 112 B = f64 vol | f64 dphi[3][4] | u16 loc[4]
+//   2D:  80 B = f64 vol | f64 dphi[2][3] | u16 loc[3] | pad
+// loc are the element's nodes as indices into its OWNER tile's node closure
+// (sorted distinct nodes of all elements the tile visits); global node ids live
+// in conn4 (int4 per element, storage order) for the streaming kernels.
 //
 // Node tiles: each tile owns <= 256 free nodes of a spatial box.  Its element
 // list is [own elements (contiguous storage range, the tile is their J owner)]
-// + [halo elements (storage ids)], and its node entries (te_local << 2 | slot)
-// are sorted by te_local per node so that a streaming pass over the element
-// list can be consumed chunk by chunk.
+// + [halo elements (storage ids + loc w.r.t. this tile)], and its node entries
+// (te_local << 2 | slot) are sorted by te_local per node so that a streaming
+// pass over the element list can be consumed chunk by chunk.
 #pragma once
 
 #include <math.h>
@@ -25,34 +26,27 @@
 namespace fm {
 
 constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
-constexpr int CONSUMERS = 256;         // consumer threads = chunk size = max tile nodes
+constexpr int CONSUMERS = 256;         // threads per tile CTA = chunk size = max tile nodes
 constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
 
 template <int DIM> struct RecBytes;
-template <> struct RecBytes<2> { static constexpr int value = 80, smem = 80; };
-template <> struct RecBytes<3> { static constexpr int value = 128, smem = 128; };
-
-// 16-B chunk c of shared-memory record r: 3D records use the TMA 128-byte swizzle
-// (chunk index XOR r mod 8, stage buffers 1024-B aligned), 2D records an odd stride.
-template <int DIM>
-__device__ __forceinline__ int rec_chunk_off(int r, int c) {
-  if constexpr (DIM == 3) return r * 128 + ((c ^ (r & 7)) << 4);
-  else return r * 80 + (c << 4);
-}
+template <> struct RecBytes<2> { static constexpr int value = 80; };
+template <> struct RecBytes<3> { static constexpr int value = 112; };
 
 struct TileMeta {
   int own_begin, own_count;      // storage range of the elements the tile owns
-  int halo_begin, halo_count;    // range in halo_ids
+  int halo_begin, halo_count;    // range in halo_ids / halo_loc
   int node_begin, node_count;    // range in node_desc
   int entry_begin, entry_count;  // range in node_entries (entry_begin % 8 == 0)
   int elem_begin;                // range start in flags (own + halo)
-  int pad[3];
+  int clo_begin, clo_count;      // node closure (clo_begin % 4 == 0)
+  int pad;
 };
 static_assert(sizeof(TileMeta) == 48, "TileMeta layout");
 
 template <int DIM> struct Elem {
-  int c[DIM + 1];
-  int orig;
+  int c[DIM + 1];    // global node ids (streaming kernels)
+  int loc[DIM + 1];  // owner-tile closure indices (tile kernel)
   double vol;
   double g[DIM][DIM + 1];  // dphi[m][l]
 };
@@ -66,39 +60,43 @@ __device__ __forceinline__ double2 ld_stream(const double2 *p) {
   return r;
 }
 
+__device__ __forceinline__ int4 ld_stream_i4(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 template <int DIM>
 __device__ __forceinline__ void decode_elem(const double2 (&q)[RecBytes<DIM>::value / 16],
                                             Elem<DIM> &E) {
+  E.vol = q[0].x;
+  long long lb;
   if constexpr (DIM == 3) {
-    E.c[0] = __double2loint(q[0].x);
-    E.c[1] = __double2hiint(q[0].x);
-    E.c[2] = __double2loint(q[0].y);
-    E.c[3] = __double2hiint(q[0].y);
-    E.vol = q[1].x;
-    const double f[12] = {q[1].y, q[2].x, q[2].y, q[3].x, q[3].y, q[4].x,
-                          q[4].y, q[5].x, q[5].y, q[6].x, q[6].y, q[7].x};
+    const double f[12] = {q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x,
+                          q[3].y, q[4].x, q[4].y, q[5].x, q[5].y, q[6].x};
 #pragma unroll
     for (int m = 0; m < 3; ++m)
 #pragma unroll
       for (int l = 0; l < 4; ++l) E.g[m][l] = f[m * 4 + l];
-    E.orig = __double2loint(q[7].y);
+    lb = __double_as_longlong(q[6].y);
   } else {
-    E.c[0] = __double2loint(q[0].x);
-    E.c[1] = __double2hiint(q[0].x);
-    E.c[2] = __double2loint(q[0].y);
-    E.orig = __double2hiint(q[0].y);
-    E.vol = q[1].x;
-    E.g[0][0] = q[1].y;
-    E.g[0][1] = q[2].x;
-    E.g[0][2] = q[2].y;
-    E.g[1][0] = q[3].x;
-    E.g[1][1] = q[3].y;
-    E.g[1][2] = q[4].x;
+    const double f[6] = {q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x};
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) E.g[m][l] = f[m * 3 + l];
+    lb = __double_as_longlong(q[3].y);
   }
+#pragma unroll
+  for (int l = 0; l < DIM + 1; ++l) E.loc[l] = (int)((lb >> (16 * l)) & 0xffff);
 }
 
+// record + global connectivity from global memory (streaming kernels)
 template <int DIM>
-__device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64_t s,
+__device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos,
+                                          const int4 *__restrict__ conn4, int64_t s,
                                           Elem<DIM> &E) {
   constexpr int NQ = RecBytes<DIM>::value / 16;
   const double2 *p = reinterpret_cast<const double2 *>(aos + s * (int64_t)RecBytes<DIM>::value);
@@ -106,25 +104,23 @@ __device__ __forceinline__ void load_elem(const uint8_t *__restrict__ aos, int64
 #pragma unroll
   for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
   decode_elem<DIM>(q, E);
+  const int4 c = ld_stream_i4(conn4 + s);
+  E.c[0] = c.x;
+  E.c[1] = c.y;
+  E.c[2] = c.z;
+  if constexpr (DIM == 3) E.c[3] = c.w;
 }
 
+// record from a shared-memory stage (row r)
 template <int DIM>
 __device__ __forceinline__ void load_elem_smem(const uint8_t *stage, int r, Elem<DIM> &E) {
   constexpr int NQ = RecBytes<DIM>::value / 16;
+  const double2 *p = reinterpret_cast<const double2 *>(stage + r * RecBytes<DIM>::value);
   double2 q[NQ];
 #pragma unroll
-  for (int k = 0; k < NQ; ++k)
-    q[k] = *reinterpret_cast<const double2 *>(stage + rec_chunk_off<DIM>(r, k));
+  for (int k = 0; k < NQ; ++k) q[k] = p[k];
   decode_elem<DIM>(q, E);
 }
-
-// CUtensorMap is a 128-byte, 64-byte aligned opaque descriptor; boxes of 8..256 rows.
-struct alignas(64) TmaDesc {
-  unsigned char bytes[128];
-};
-struct TmaMaps {
-  TmaDesc box[6];  // rows 8 << k
-};
 
 // Gather the d components of the field at the element's nodes (v interleaved).
 template <int DIM, int D>
@@ -158,16 +154,20 @@ __device__ __forceinline__ double np_scalar_pow(double x, double e) {
 // Tile tables (built by fm_ctx_create).
 struct TileArgs {
   const uint8_t *aos;
-  const TileMeta *meta;      // n_tiles_all
-  const int32_t *halo_ids;   // storage index of halo elements
-  const uint8_t *flags;      // owned-slot mask per tile element (own then halo)
-  const int4 *node_desc;     // {entry_off, entry_count, node id, out | mask << 28}
-  const uint16_t *entries;   // te_local << 2 | slot, sorted by te_local per node
-  const int32_t *rank_of;    // node -> free rank or -1
-  int n_tiles;               // node tiles
-  int n_tiles_all;           // + orphan tiles (J only)
-  int entry_cap;             // max entries of one tile, rounded up to 8
-  int halo_cap;              // max halo elements of one tile, rounded up to 4
+  const int4 *conn4;           // global node ids per element (storage order)
+  const int32_t *s2o;          // storage -> reference element id
+  const TileMeta *meta;        // n_tiles_all
+  const int32_t *halo_ids;     // storage index of halo elements
+  const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements
+  const int32_t *closure;      // node ids of the tile closures
+  const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
+  const int4 *node_desc;       // {entry_off, entry_count, node id, out | mask << 28}
+  const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
+  const int32_t *rank_of;      // node -> free rank or -1
+  int n_tiles;                 // node tiles
+  int n_tiles_all;             // + orphan tiles (J only)
+  int entry_cap;               // max entries of one tile, rounded up to 8
+  int clo_cap;                 // max closure size, rounded up to 4
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
@@ -195,11 +195,13 @@ struct fm_ctx {
   int64_t nn = 0, ne = 0, nfree = 0, nfree_dofs = 0, p_total = 0;
   int32_t n_tiles = 0, n_tiles_all = 0;
   int64_t n_tile_elems = 0, n_node_entries = 0;
-  int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, halo_cap = 0;
-  int n_sm = 148, stages = 4;
+  int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, clo_cap = 0;
+  int n_sm = 148, ctas_per_sm = 2;
   uint8_t *aos = nullptr;
+  int4 *conn4 = nullptr;
   fm::TileMeta *meta = nullptr;
-  int32_t *halo_ids = nullptr;
+  int32_t *halo_ids = nullptr, *closure = nullptr;
+  uint2 *halo_loc = nullptr;
   uint8_t *flags = nullptr;
   int4 *node_desc = nullptr;
   uint16_t *node_entries = nullptr;
@@ -214,11 +216,11 @@ struct fm_ctx {
   int64_t launches = 0;
   size_t bytes = 0;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // armed by fm_ctx_time_next
-  fm::TmaMaps tma{};  // 3D element records as a 2D tensor (rows x 128 B), SWIZZLE_128B
   fm_ctx_stats stats{};
 
   fm::TileArgs tile_args() const {
-    return fm::TileArgs{aos,     meta,    halo_ids,    flags,     node_desc, node_entries,
-                        rank_of, n_tiles, n_tiles_all, entry_cap, halo_cap};
+    return fm::TileArgs{aos,     conn4,     storage_to_orig, meta,        halo_ids,
+                        halo_loc, closure,  flags,           node_desc,   node_entries,
+                        rank_of, n_tiles,   n_tiles_all,     entry_cap,   clo_cap};
   }
 };

@@ -11,8 +11,8 @@ namespace fm {
 // assembly.py:94-106: every element once in storage order; block b sums the
 // fixed range [b*per, (b+1)*per) with a fixed tree -> partial[b].
 template <int DIM, int MODEL>
-__global__ void __launch_bounds__(256) k_energy(const uint8_t *__restrict__ aos, int64_t ne,
-                                                int64_t per, const double *__restrict__ v,
+__global__ void __launch_bounds__(256) k_energy(TileArgs a, int64_t ne, int64_t per,
+                                                const double *__restrict__ v,
                                                 double *__restrict__ part,
                                                 double *__restrict__ dens, ModelArgs mdl) {
   constexpr int NV = DIM + 1;
@@ -22,13 +22,13 @@ __global__ void __launch_bounds__(256) k_energy(const uint8_t *__restrict__ aos,
   double acc = 0.0;
   for (int64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
     Elem<DIM> E;
-    load_elem<DIM>(aos, s, E);
+    load_elem<DIM>(a.aos, a.conn4, s, E);
     double vv[D][NV];
     gather_v<DIM, D>(v, E.c, vv);
     double F[D][DIM];
     grad_F<DIM, D>(vv, E.g, F);
     double W = density<DIM, MODEL>(F, mdl);
-    if (dens) dens[E.orig] = W;
+    if (dens) dens[a.s2o[s]] = W;
     acc += E.vol * W;
   }
   double r = block_sum(acc, red);
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
       const int s = i < tm.own_count ? tm.own_begin + i : a.halo_ids[tm.halo_begin + i - tm.own_count];
       const int fl = a.flags[tm.elem_begin + i];
       Elem<DIM> E;
-      load_elem<DIM>(a.aos, s, E);
+      load_elem<DIM>(a.aos, a.conn4, s, E);
       double vv[D][NV];
       gather_v<DIM, D>(v, E.c, vv);
       double F[D][DIM];
@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
               const int r = a.rank_of[E.c[l]];
               unsigned long long key = ((unsigned long long)sg << 63) |
                                        ((unsigned long long)j << 61) |
-                                       ((unsigned long long)r << 31) | (unsigned long long)E.orig;
+                                       ((unsigned long long)r << 31) |
+                                       (unsigned long long)a.s2o[s];
               mykey = key < mykey ? key : mykey;
             }
             row[(l * D + j) * 2 + sg] = E.vol * W;
@@ -198,14 +199,14 @@ __global__ void k_descent(int64_t nfree, int d, const int32_t *free_node, const 
 
 // ----------------------------------------------------------------- launchers
 template <int DIM, int MODEL>
-static cudaError_t energy_t(const uint8_t *aos, int64_t ne, int nblocks, const double *v,
+static cudaError_t energy_t(const TileArgs &aos, int64_t ne, int nblocks, const double *v,
                             double *part, double *dens, const ModelArgs &m, cudaStream_t s) {
   int64_t per = (ne + nblocks - 1) / nblocks;
   k_energy<DIM, MODEL><<<nblocks, 256, 0, s>>>(aos, ne, per, v, part, dens, m);
   return cudaGetLastError();
 }
 
-cudaError_t launch_energy(int dim, int model, const uint8_t *aos, int64_t ne, int nblocks,
+cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, int nblocks,
                           const double *v, double *part, double *dens, const ModelArgs &m,
                           cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)

@@ -8,19 +8,18 @@
 
 namespace fm {
 
-// persistent pipelined fused J + exact gradient; grid = #SMs, CONSUMERS + 32 threads
-cudaError_t launch_tile_exact(int dim, int model, const TmaMaps &tma, const TileArgs &a,
-                              int grid, int stages, bool wj, const double *v, const double *b,
-                              double *g, double *jpart, unsigned long long *status,
-                              const ModelArgs &m, cudaStream_t s);
-size_t tile_exact_smem(int dim, int d, int stages, int entry_cap, int halo_cap);
+// persistent pipelined fused J + exact gradient; grid = ctas_per_sm * #SMs, CONSUMERS threads
+cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, bool wj,
+                              const double *v, const double *b, double *g, double *jpart,
+                              unsigned long long *status, const ModelArgs &m, cudaStream_t s);
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
                            size_t smem_entries, const double *v, const double *b, double eps,
                            double *g, unsigned long long *badkey, const ModelArgs &m,
                            cudaStream_t s);
 
-cudaError_t launch_energy(int dim, int model, const uint8_t *aos, int64_t ne, int nblocks,
+cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, int nblocks,
                           const double *v, double *part, double *dens, const ModelArgs &m,
                           cudaStream_t s);
 
