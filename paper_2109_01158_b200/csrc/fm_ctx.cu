@@ -461,9 +461,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->ne = m->ne;
   c->nfree = m->nfree;
   c->p_total = m->p_total;
-  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : CONSUMERS;
-  NT = std::max(32, std::min(CONSUMERS, NT));
-  int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? 8 : 16, dim == 3 ? 4 : 1};
+  // tile = CTA width: 128 nodes (3D, 8x4x4 boxes, 4 CTAs/SM) or 256 (2D, 16x16)
+  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : (dim == 3 ? 128 : 256);
+  NT = NT <= 128 ? 128 : 256;
+  int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? (NT == 128 ? 4 : 8) : 16, dim == 3 ? 4 : 1};
   if (tiling)
     for (int a = 0; a < 3; ++a)
       if (tiling->box[a] > 0) box[a] = tiling->box[a];
@@ -883,14 +884,19 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
   }
 
-  // CTAs per SM that fit the shared memory (228 KB per SM, 1 KB reserved per CTA)
+  // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads; shared memory
+  // (228 KB per SM, 1 KB reserved per CTA) decides, preferring two node-value
+  // buffers (one tile of lead) when that does not cost a CTA
   {
-    const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap);
-    if (sm <= 113 * 1024)
-      c->ctas_per_sm = 2;
-    else if (sm <= 227 * 1024)
-      c->ctas_per_sm = 1;
-    else {
+    const int regs_cap = c->tile_nodes == 128 ? 4 : 2;
+    auto fit = [&](int nb) {
+      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb);
+      return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));
+    };
+    const int f2 = fit(2), f1 = fit(1);
+    c->node_bufs = (f2 >= f1 && f2 > 0) ? 2 : 1;
+    c->ctas_per_sm = std::max(f2, f1);
+    if (c->ctas_per_sm == 0) {
       set_error("tile tables exceed shared memory; use smaller tiles");
       return fail(FM_INVALID_ARG);
     }
@@ -977,8 +983,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   const int grid = std::min(c->n_sm * c->ctas_per_sm, std::max(1, ta.n_tiles_all));
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, wj, v, b, g, c->jpart, c->status,
-                              ma, s));
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs, wj, v,
+                              b, g, c->jpart, c->status, ma, s));
     c->launches++;
   }
   if (wj) {

@@ -1,24 +1,24 @@
 // Fused energy + exact gradient (gradients.py:124-149 with assembly.py:94-106)
-// as one persistent, pipelined kernel; two 256-thread CTAs per SM.
+// as one persistent, pipelined kernel; several CT-thread CTAs per SM.
 //
 // Each CTA walks its node tiles (t = blockIdx.x, += gridDim.x; tiles are in
 // Morton order of their spatial boxes so concurrently running CTAs share halo
-// elements through L2).  Per tile:
+// elements through L2).  Per tile (<= CT free nodes, one node per thread):
 //   node values   the tile's node closure (sorted distinct nodes of all its
-//                 elements, <= ~650 for 8x8x4 boxes) is gathered ONCE into
-//                 shared memory (8-byte LDGSTS, one tile ahead, double
-//                 buffered); elements address it with 16-bit closure indices,
-//                 so no per-element global gathers of v remain.
-//   records       chunks of 256 elements, double-buffered: the own elements are
+//                 elements) is gathered ONCE into shared memory (8-byte
+//                 LDGSTS; with NB = 2 buffers one tile ahead); elements address
+//                 it with 16-bit closure indices, so no per-element global
+//                 gathers of v remain.
+//   records       chunks of CT elements, double-buffered: the own elements are
 //                 a contiguous storage range -> one 1D bulk copy (TMA engine,
 //                 mbarrier complete_tx); halo records -> 16-byte LDGSTS by the
 //                 thread that owns the row.  Records are 112 B (3D) / 80 B (2D):
 //                 an odd number of 16-B chunks, so row-per-lane reads are
 //                 bank-conflict free without swizzling.
 //   compute       thread c: F = grad v, P' = vol * dW/dF = a F + b cof, the
-//                 contributions P' . grad phi_l of its four local nodes, vol * W
-//                 when the tile owns the element; contributions are staged over
-//                 the (consumed) record buffer.
+//                 contributions P' . grad phi_l of its local nodes, vol * W when
+//                 the tile owns the element; contributions are staged over the
+//                 (consumed) record buffer.
 //   assemble      node threads consume this chunk's entries (sorted by tile
 //                 element) into registers: fixed summation order, no
 //                 floating-point atomics.
@@ -32,16 +32,16 @@ namespace fm {
 
 __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; }
 
-template <int DIM>
+template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
-  __host__ __device__ static size_t stage() { return r16((size_t)CONSUMERS * RB); }
+  __host__ __device__ static size_t stage() { return r16((size_t)CT * RB); }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
-  __host__ __device__ static size_t desc() { return (size_t)CONSUMERS * 16; }
+  __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
   __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
-  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap) {
-    return 2 * stage() + 2 * nodev(D, clo_cap) + cids(clo_cap) + desc() + ents(entry_cap) +
+  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb) {
+    return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() + ents(entry_cap) +
            32 * 8 + 8 * 8;
   }
 };
@@ -93,7 +93,23 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
   }
 }
 
-// Position in this CTA's chunk stream: tile t (j-th of the CTA), chunk offset c0.
+// F = grad v as chained FMAs (one DMUL + NV-1 DFMA per entry)
+template <int DIM, int D>
+__device__ __forceinline__ void grad_F_fma(const double (&vv)[D][DIM + 1],
+                                           const double (&g)[DIM][DIM + 1], double (&F)[D][DIM]) {
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      double s = vv[j][0] * g[m][0];
+#pragma unroll
+      for (int l = 1; l < DIM + 1; ++l) s = fma(vv[j][l], g[m][l], s);
+      F[j][m] = s;
+    }
+}
+
+// Position in this CTA's chunk stream: tile t, chunk offset c0.
+template <int CT>
 struct Cursor {
   int t, c0, ne;
   TileMeta tm;
@@ -107,7 +123,7 @@ struct Cursor {
   }
   __device__ bool valid(const TileArgs &a) const { return t < a.n_tiles_all; }
   __device__ void advance(const TileArgs &a) {
-    c0 += CONSUMERS;
+    c0 += CT;
     if (c0 >= ne) {
       c0 = 0;
       t += gridDim.x;
@@ -123,8 +139,8 @@ struct RowSrc {
   uint2 loc;
 };
 
-template <int DIM, int MODEL, bool WJ>
-__global__ void __launch_bounds__(CONSUMERS, 2)
+template <int DIM, int MODEL, bool WJ, int CT, int NB, int MINB>
+__global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, unsigned long long *status,
                  ModelArgs mdl) {
@@ -132,8 +148,8 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int RB = RecBytes<DIM>::value;
   constexpr int NCH = RB / 16;
-  using L = PipeLayout<DIM>;
-  static_assert((size_t)CONSUMERS * NV * D * 8 <= (size_t)CONSUMERS * RB, "staging fits a stage");
+  using L = PipeLayout<DIM, CT>;
+  static_assert((size_t)CT * NV * D * 8 <= (size_t)CT * RB, "staging fits a stage");
   extern __shared__ __align__(16) unsigned char smem[];
   const int CAP = a.clo_cap;
   // stage s at smem + s * stage(); node-value buffer k at nodev0 + k * nodev()
@@ -141,7 +157,7 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
   auto nodev = [&](int k) {
     return reinterpret_cast<double *>(smem + 2 * L::stage() + k * L::nodev(D, CAP));
   };
-  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * L::stage() + 2 * L::nodev(D, CAP));
+  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * L::stage() + NB * L::nodev(D, CAP));
   int4 *desc = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(cids) + L::cids(CAP));
   uint16_t *ents = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(desc) + L::desc());
   double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(ents) +
@@ -152,10 +168,10 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
   uint64_t *tfull = cfull + 1;                              // descriptors + entries
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(full, CONSUMERS + 1);
-    mbar_init(full + 1, CONSUMERS + 1);
-    mbar_init(nfull, CONSUMERS);
-    mbar_init(nfull + 1, CONSUMERS);
+    mbar_init(full, CT + 1);
+    mbar_init(full + 1, CT + 1);
+    mbar_init(nfull, CT);
+    mbar_init(nfull + 1, CT);
     mbar_init(cfull, 1);
     mbar_init(tfull, 1);
     fence_barrier_init();
@@ -170,19 +186,20 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
       bulk_g2s(cids, a.closure + tm.clo_begin, bytes, cfull);
     }
   };
-  auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev[k]
-    for (int i = tid; i < clo_count; i += CONSUMERS) {
+  auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
+    double *dst = nodev(k);
+    for (int i = tid; i < clo_count; i += CT) {
       const double *src = v + (int64_t)cids[i] * D;
 #pragma unroll
       for (int kk = 0; kk < D; ++kk)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                         smem_u32(nodev(k) + kk * CAP + i)),
+                         smem_u32(dst + kk * CAP + i)),
                      "l"(src + kk)
                      : "memory");
     }
     cp_async_arrive_noinc(nfull + k);
   };
-  auto row_src = [&](const Cursor &x) -> RowSrc {
+  auto row_src = [&](const Cursor<CT> &x) -> RowSrc {
     RowSrc r{0, 0, make_uint2(0, 0)};
     const int e = x.c0 + tid;
     if (x.valid(a) && e < x.ne) {
@@ -197,9 +214,9 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
     }
     return r;
   };
-  auto issue_records = [&](const Cursor &x, int s, const RowSrc &rs) {
+  auto issue_records = [&](const Cursor<CT> &x, int s, const RowSrc &rs) {
     if (!x.valid(a)) return;
-    const int cnt = min(CONSUMERS, x.ne - x.c0);
+    const int cnt = min(CT, x.ne - x.c0);
     const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
     if (tid == 0) {
       mbar_arrive_expect_tx(full + s, (uint32_t)n_own * RB);
@@ -217,18 +234,20 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
 
   double jsum = 0.0;
   bool bad_any = false;
-  Cursor comp{(int)blockIdx.x, 0, 0, TileMeta{}};
+  Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}};
   comp.load(a);
   if (comp.valid(a)) {
-    // ---- prologue: closure + node values of tile 0, closure ids of tile 1, chunk 0
+    // ---- prologue: closure ids (+ node values with NB = 2) and chunk 0 records
     issue_clo(comp.t);
-    mbar_wait(cfull, 0);
-    gather_nodev(comp.tm.clo_count, 0);
-    __syncthreads();
-    issue_clo(comp.t + gridDim.x);
+    if (NB == 2) {
+      mbar_wait(cfull, 0);
+      gather_nodev(comp.tm.clo_count, 0);
+      __syncthreads();
+      issue_clo(comp.t + gridDim.x);
+    }
     RowSrc cur_row = row_src(comp);
     issue_records(comp, 0, cur_row);
-    Cursor iss = comp;
+    Cursor<CT> iss = comp;
     iss.advance(a);
     RowSrc next_row = row_src(iss);
     uint32_t q = 0, j = 0;
@@ -243,17 +262,28 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
         if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
         if (eb) bulk_g2s(ents, a.entries + tm.entry_begin, eb, tfull);
       }
-      // node values of the NEXT tile (one tile of lead), then its successor's ids
-      const int tn = comp.t + gridDim.x;
-      if (tn < a.n_tiles_all) {
-        mbar_wait(cfull, (j + 1) & 1);
-        gather_nodev(a.meta[tn].clo_count, (j + 1) & 1);
-        __syncthreads();  // cids consumed
-        issue_clo(tn + gridDim.x);
+      const double *nv;
+      if (NB == 2) {
+        // node values of the NEXT tile (one tile of lead), then its successor's ids
+        const int tn = comp.t + gridDim.x;
+        if (tn < a.n_tiles_all) {
+          mbar_wait(cfull, (j + 1) & 1);
+          gather_nodev(a.meta[tn].clo_count, (j + 1) & 1);
+          __syncthreads();  // cids consumed
+          issue_clo(tn + gridDim.x);
+        }
+        mbar_wait(nfull + (j & 1), (j >> 1) & 1);
+        nv = nodev(j & 1);
+      } else {
+        // single buffer: gather this tile's node values now (previous tile done)
+        mbar_wait(cfull, j & 1);
+        gather_nodev(tm.clo_count, 0);
+        mbar_wait(nfull, j & 1);
+        __syncthreads();  // cids consumed, every thread's copies visible
+        issue_clo(comp.t + gridDim.x);
+        nv = nodev(0);
       }
-      mbar_wait(nfull + (j & 1), (j >> 1) & 1);
       mbar_wait(tfull, j & 1);
-      const double *nv = nodev(j & 1);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
       int cur = 0, end = 0, outw = 0;
@@ -271,7 +301,7 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
         }
       }
       const int ne_t = comp.ne;
-      for (int c0 = 0; c0 < ne_t; c0 += CONSUMERS, ++q) {
+      for (int c0 = 0; c0 < ne_t; c0 += CT, ++q) {
         const int s = q & 1;
         // records of the next chunk into the other stage (freed by the last barrier)
         issue_records(iss, s ^ 1, next_row);
@@ -298,7 +328,7 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
 #pragma unroll
             for (int k = 0; k < D; ++k) vv[k][l] = nv[k * CAP + E.loc[l]];
           double F[D][DIM];
-          grad_F<DIM, D>(vv, E.g, F);
+          grad_F_fma<DIM, D>(vv, E.g, F);
           const bool own = e < tm.own_count;
           if (has_nodes) {
             double W = 0.0;
@@ -320,19 +350,19 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
               double sdot = P[k][0] * E.g[0][l];
 #pragma unroll
               for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
-              stage_d[(l * D + k) * CONSUMERS + tid] = sdot;  // [slot][comp][row]
+              stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
             }
         }
         __syncthreads();  // contributions staged
         if (my_node) {
-          const int lim = c0 + CONSUMERS;
+          const int lim = c0 + CT;
           while (cur < end) {
             const int en = ents[cur];
             const int te = en >> 2;
             if (te >= lim) break;
-            const double *src = stage_d + (te - c0) + (en & 3) * D * CONSUMERS;
+            const double *src = stage_d + (te - c0) + (en & 3) * D * CT;
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] += src[k * CONSUMERS];
+            for (int k = 0; k < D; ++k) acc[k] += src[k * CT];
             ++cur;
           }
         }
@@ -356,39 +386,52 @@ __global__ void __launch_bounds__(CONSUMERS, 2)
   }
 }
 
-template <int DIM, int MODEL>
-static cudaError_t launch_exact_t(const TileArgs &a, int grid, bool wj, const double *v,
-                                  const double *b, double *g, double *jpart,
-                                  unsigned long long *status, const ModelArgs &m,
-                                  cudaStream_t s) {
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb) {
+  if (ct == 128)
+    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb)
+                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb);
+  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb)
+                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb);
+}
+
+template <int DIM, int MODEL, int CT, int NB, int MINB>
+static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double *v,
+                              const double *b, double *g, double *jpart,
+                              unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  const size_t smem = PipeLayout<DIM>::total(D, a.entry_cap, a.clo_cap);
-#define FM_LAUNCH(WJV)                                                                \
-  do {                                                                                \
-    auto k = k_tile_exact<DIM, MODEL, WJV>;                                           \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k<<<grid, CONSUMERS, smem, s>>>(a, v, b, g, jpart, status, m);                    \
-  } while (0)
-  if (wj) FM_LAUNCH(true); else FM_LAUNCH(false);
-#undef FM_LAUNCH
+  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB);
+  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, MINB>
+              : k_tile_exact<DIM, MODEL, false, CT, NB, MINB>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, status, m);
   return cudaGetLastError();
 }
 
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap) {
-  return dim == 3 ? PipeLayout<3>::total(d, entry_cap, clo_cap)
-                  : PipeLayout<2>::total(d, entry_cap, clo_cap);
+template <int DIM, int MODEL>
+static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, bool wj,
+                                  const double *v, const double *b, double *g, double *jpart,
+                                  unsigned long long *status, const ModelArgs &m,
+                                  cudaStream_t s) {
+  if (ct == 128) {
+    if (nb == 2) return launch_cfg<DIM, MODEL, 128, 2, 4>(a, grid, wj, v, b, g, jpart, status, m, s);
+    return launch_cfg<DIM, MODEL, 128, 1, 4>(a, grid, wj, v, b, g, jpart, status, m, s);
+  }
+  if (nb == 2) return launch_cfg<DIM, MODEL, 256, 2, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
+  return launch_cfg<DIM, MODEL, 256, 1, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
 }
 
-cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, bool wj,
-                              const double *v, const double *b, double *g, double *jpart,
-                              unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
+cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
+                              bool wj, const double *v, const double *b, double *g,
+                              double *jpart, unsigned long long *status, const ModelArgs &m,
+                              cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
   if (dim == 2)
-    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, wj, v, b, g, jpart, status, m, s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, wj, v, b, g, jpart, status, m,
+                                                  s);
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
 }
 
 }  // namespace fm
