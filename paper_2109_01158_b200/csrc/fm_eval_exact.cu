@@ -353,33 +353,18 @@ __global__ void __launch_bounds__(CT, MINB)
               stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
             }
         }
-        // this chunk's entries: [cur, stop) (entries are sorted by tile element)
-        int stop = cur;
-        const int lim = (c0 + CT) << 2;
-        if (my_node)
-          while (stop < end && ents[stop] < lim) ++stop;
         __syncthreads();  // contributions staged
-        // two entries per step: loads of the second overlap the first's adds;
-        // the summation order (ascending tile element) is unchanged
-        for (; cur + 1 < stop; cur += 2) {
-          const int e0 = ents[cur], e1 = ents[cur + 1];
-          const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
-          const double *s1 = stage_d + ((e1 >> 2) - c0) + (e1 & 3) * D * CT;
-          double x0[D], x1[D];
+        if (my_node) {
+          const int lim = c0 + CT;
+          while (cur < end) {
+            const int en = ents[cur];
+            const int te = en >> 2;
+            if (te >= lim) break;
+            const double *src = stage_d + (te - c0) + (en & 3) * D * CT;
 #pragma unroll
-          for (int k = 0; k < D; ++k) {
-            x0[k] = s0[k * CT];
-            x1[k] = s1[k * CT];
+            for (int k = 0; k < D; ++k) acc[k] += src[k * CT];
+            ++cur;
           }
-#pragma unroll
-          for (int k = 0; k < D; ++k) acc[k] = (acc[k] + x0[k]) + x1[k];
-        }
-        if (cur < stop) {
-          const int e0 = ents[cur];
-          const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
-#pragma unroll
-          for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
-          ++cur;
         }
         __syncthreads();  // stage s, descriptors and entries free
         comp.advance(a);
