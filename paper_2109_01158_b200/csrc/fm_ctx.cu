@@ -385,6 +385,11 @@ static ModelArgs model_args(const fm_model *m) {
   a.D1 = m->D1;
   a.e_w = m->p / 2.0;
   a.e_dw = (m->p - 2.0) / 2.0;
+  static const int ablate = [] {
+    const char *e = getenv("FM_TILE_ABLATE");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = ablate;
   return a;
 }
 

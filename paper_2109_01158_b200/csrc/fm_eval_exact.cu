@@ -330,7 +330,12 @@ __global__ void __launch_bounds__(CT, MINB)
           double F[D][DIM];
           grad_F_fma<DIM, D>(vv, E.g, F);
           const bool own = e < tm.own_count;
-          if (has_nodes) {
+          if (mdl.dbg & 1) {  // ablation: no constitutive work
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+#pragma unroll
+              for (int m = 0; m < DIM; ++m) P[k][m] = F[k][m];
+          } else if (has_nodes) {
             double W = 0.0;
             bool bad;
             element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(CT, MINB)
             }
         }
         __syncthreads();  // contributions staged
-        if (my_node) {
+        if (my_node && !(mdl.dbg & 2)) {
           const int lim = c0 + CT;
           while (cur < end) {
             const int en = ents[cur];
