@@ -225,6 +225,9 @@ __global__ void __launch_bounds__(CT, MINB)
                  full + s);
     }
     if (tid >= n_own && tid < cnt) {
+      if ((mdl.dbg & 4) && (rs.src < 0 || !rs.halo))
+        printf("FMCHK src t=%d c0=%d tid=%d src=%d halo=%d own=%d ne=%d\n", x.t, x.c0, tid, rs.src,
+               rs.halo, x.tm.own_count, x.ne);
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
         cp_async16(stg(s) + tid * RB + c * 16, a.aos + (int64_t)rs.src * RB + c * 16);
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(CT, MINB)
     if (NB == 2) {
       mbar_wait(cfull, 0);
       gather_nodev(comp.tm.clo_count, 0);
+      fence_proxy_async();  // cids reads before the bulk refill
       __syncthreads();
       issue_clo(comp.t + gridDim.x);
     }
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(CT, MINB)
         if (tn < a.n_tiles_all) {
           mbar_wait(cfull, (j + 1) & 1);
           gather_nodev(a.meta[tn].clo_count, (j + 1) & 1);
+          fence_proxy_async();
           __syncthreads();  // cids consumed
           issue_clo(tn + gridDim.x);
         }
@@ -279,6 +284,7 @@ __global__ void __launch_bounds__(CT, MINB)
         mbar_wait(cfull, j & 1);
         gather_nodev(tm.clo_count, 0);
         mbar_wait(nfull, j & 1);
+        fence_proxy_async();
         __syncthreads();  // cids consumed, every thread's copies visible
         issue_clo(comp.t + gridDim.x);
         nv = nodev(0);
@@ -295,6 +301,9 @@ __global__ void __launch_bounds__(CT, MINB)
         cur = nd.x;
         end = nd.x + nd.y;
         outw = nd.w;
+        if ((mdl.dbg & 4) && (nd.x < 0 || nd.x + nd.y > tm.entry_count || nd.z < 0))
+          printf("FMCHK desc t=%d tid=%d x=%d y=%d z=%d w=%d ecount=%d\n", comp.t, tid, nd.x,
+                 nd.y, nd.z, nd.w, tm.entry_count);
         if (b) {
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
@@ -321,6 +330,14 @@ __global__ void __launch_bounds__(CT, MINB)
             E.loc[1] = this_row.loc.x >> 16;
             E.loc[2] = this_row.loc.y & 0xffff;
             if constexpr (DIM == 3) E.loc[3] = this_row.loc.y >> 16;
+          }
+          if (mdl.dbg & 4) {  // bounds checks (debug)
+            for (int l = 0; l < NV; ++l)
+              if (E.loc[l] >= tm.clo_count) {
+                printf("FMCHK loc t=%d e=%d l=%d loc=%d clo=%d halo=%d own=%d\n", comp.t, e, l,
+                       E.loc[l], tm.clo_count, this_row.halo, tm.own_count);
+                E.loc[l] = 0;
+              }
           }
           double vv[D][NV];
 #pragma unroll
@@ -371,6 +388,9 @@ __global__ void __launch_bounds__(CT, MINB)
             ++cur;
           }
         }
+        // the staging stores / record, descriptor and entry reads of this chunk
+        // must be ordered before the bulk copies that refill these buffers
+        fence_proxy_async();
         __syncthreads();  // stage s, descriptors and entries free
         comp.advance(a);
       }

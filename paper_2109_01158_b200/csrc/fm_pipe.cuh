@@ -73,6 +73,13 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
                : "memory");
 }
 
+// Order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (bulk copy / TMA) accesses to the same buffers: required before a
+// buffer that was written or read with ST/LD is refilled by cp.async.bulk.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // named barrier over the consumer warps only
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
