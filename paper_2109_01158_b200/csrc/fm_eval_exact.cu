@@ -219,8 +219,7 @@ __global__ void __launch_bounds__(CT, MINB)
   auto issue_records = [&](const Cursor<CT> &x, int s, const RowSrc &rs) {
     if (!x.valid(a)) return;
     const int cnt = min(CT, x.ne - x.c0);
-    // own rows: one bulk copy (TMA engine), or per-thread LDGSTS with mdl.dbg & 8
-    const int n_own = (mdl.dbg & 8) ? 0 : max(0, min(cnt, x.tm.own_count - x.c0));
+    const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
     if (tid == 0) {
       mbar_arrive_expect_tx(full + s, (uint32_t)n_own * RB);
       if (n_own)
@@ -259,19 +258,12 @@ __global__ void __launch_bounds__(CT, MINB)
     RowSrc next_row = row_src(iss);
     // own records of chunks q+2 .. q+1+PF_DIST are prefetched into L2 (bulk)
     Cursor<CT> pf = iss;
-    // L2 prefetch mode (mdl.dbg >> 4 & 3): 0 none, 1 bulk (TMA), 2 per-thread prefetch
-    const int pf_mode = (mdl.dbg >> 4) & 3;
     auto prefetch = [&](const Cursor<CT> &x) {
-      if (!x.valid(a) || pf_mode == 0) return;
-      const int cnt = min(CT, x.ne - x.c0);
-      const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
-      if (pf_mode == 1) {
-        if (tid == 0 && n_own)
+      if (tid == 0 && x.valid(a)) {
+        const int cnt = min(CT, x.ne - x.c0);
+        const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
+        if (n_own)
           bulk_prefetch_l2(a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)n_own * RB);
-      } else if (tid < n_own) {
-        const unsigned char *p = a.aos + (int64_t)(x.tm.own_begin + x.c0 + tid) * RB;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + RB - 1));
       }
     };
     for (int k = 0; k < PF_DIST; ++k) {
