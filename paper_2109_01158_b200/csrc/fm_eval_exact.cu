@@ -32,8 +32,6 @@ namespace fm {
 
 __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; }
 
-constexpr int PF_DIST = 4;  // chunks of L2 prefetch beyond the shared-memory stages
-
 template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
@@ -256,20 +254,6 @@ __global__ void __launch_bounds__(CT, MINB)
     Cursor<CT> iss = comp;
     iss.advance(a);
     RowSrc next_row = row_src(iss);
-    // own records of chunks q+2 .. q+1+PF_DIST are prefetched into L2 (bulk)
-    Cursor<CT> pf = iss;
-    auto prefetch = [&](const Cursor<CT> &x) {
-      if (tid == 0 && x.valid(a)) {
-        const int cnt = min(CT, x.ne - x.c0);
-        const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
-        if (n_own)
-          bulk_prefetch_l2(a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)n_own * RB);
-      }
-    };
-    for (int k = 0; k < PF_DIST; ++k) {
-      pf.advance(a);
-      prefetch(pf);
-    }
     uint32_t q = 0, j = 0;
 
     while (comp.valid(a)) {
@@ -334,8 +318,6 @@ __global__ void __launch_bounds__(CT, MINB)
         cur_row = next_row;
         iss.advance(a);
         next_row = row_src(iss);
-        pf.advance(a);
-        prefetch(pf);
         mbar_wait(full + s, (q >> 1) & 1);
         const int e = c0 + tid;
         const bool valid = e < ne_t;
