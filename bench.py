@@ -319,8 +319,10 @@ def main():
                        "evals_per_s": 1e3 / ms,
                        "parallelism": f"x1-slabs x{world}" if world > 1 else "single GPU",
                        "l2": "inputs (3.3 GB per eval) larger than the 126 MB L2; no flush",
-                       "tiles": {k: dm.stats[k] for k in ("n_tiles", "redundancy",
-                                                          "max_tile_elems")}},
+                       "tiles": {k: dm.stats[k] for k in (
+                           "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
+                           "ctas_per_sm", "node_bufs", "stage_bufs", "entry_cap",
+                           "closure_cap")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_tile_exact<3,NH,J,G>", "kernel_ms": kms,

@@ -155,6 +155,8 @@ typedef struct {
   int64_t n_tiles, n_orphan_tiles, tile_elems_total, node_entries_total;
   int64_t max_tile_elems, max_tile_entries, bytes_device;
   double redundancy;           /* tile element visits / ne                      */
+  int32_t tile_threads, ctas_per_sm, node_bufs, stage_bufs;  /* tile-kernel launch shape */
+  int32_t entry_cap, closure_cap;                            /* per-tile table capacities */
 } fm_ctx_stats;
 
 int fm_ctx_create(const fm_mesh_desc *desc, const fm_tiling *tiling, void *stream,

@@ -38,7 +38,9 @@ class FmTiling(C.Structure):
 class FmCtxStats(C.Structure):
     _fields_ = [("n_tiles", i64), ("n_orphan_tiles", i64), ("tile_elems_total", i64),
                 ("node_entries_total", i64), ("max_tile_elems", i64),
-                ("max_tile_entries", i64), ("bytes_device", i64), ("redundancy", dbl)]
+                ("max_tile_entries", i64), ("bytes_device", i64), ("redundancy", dbl),
+                ("tile_threads", i32), ("ctas_per_sm", i32), ("node_bufs", i32),
+                ("stage_bufs", i32), ("entry_cap", i32), ("closure_cap", i32)]
 
 
 # name: (restype, argtypes) — every symbol declared in include/femmin_b200.h

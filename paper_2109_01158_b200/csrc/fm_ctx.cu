@@ -894,14 +894,33 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   // buffers (one tile of lead) when that does not cost a CTA
   {
     const int regs_cap = c->tile_nodes == 128 ? 4 : 2;
-    auto fit = [&](int nb) {
-      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb);
+    auto fit = [&](int nb, int ns) {
+      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb, ns);
       return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));
     };
-    const int f2 = fit(2), f1 = fit(1);
-    c->node_bufs = (f2 >= f1 && f2 > 0) ? 2 : 1;
-    c->ctas_per_sm = std::max(f2, f1);
-    if (c->ctas_per_sm == 0) {
+    // most CTAs per SM first, then one barrier per chunk (ns = 2), then a tile
+    // of node-value lead (nb = 2); FM_TILE_CFG="nb,ns" forces a variant
+    int best = -1;
+    for (int nb = 2; nb >= 1; --nb)
+      for (int ns = 2; ns >= 1; --ns) {
+        const int f = fit(nb, ns);
+        const int score = f * 4 + (ns == 2) * 2 + (nb == 2);
+        if (f > 0 && score > best) {
+          best = score;
+          c->node_bufs = nb;
+          c->stage_bufs = ns;
+          c->ctas_per_sm = f;
+        }
+      }
+    if (const char *e = getenv("FM_TILE_CFG")) {
+      int nb = 0, ns = 0;
+      if (sscanf(e, "%d,%d", &nb, &ns) == 2 && fit(nb, ns) > 0) {
+        c->node_bufs = nb;
+        c->stage_bufs = ns;
+        c->ctas_per_sm = fit(nb, ns);
+      }
+    }
+    if (best < 0) {
       set_error("tile tables exceed shared memory; use smaller tiles");
       return fail(FM_INVALID_ARG);
     }
@@ -928,6 +947,12 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   st.max_tile_entries = c->max_tile_entries;
   st.bytes_device = (int64_t)c->bytes;
   st.redundancy = (double)(M + n_orph) / (double)ne;
+  st.tile_threads = c->tile_nodes;
+  st.ctas_per_sm = c->ctas_per_sm;
+  st.node_bufs = c->node_bufs;
+  st.stage_bufs = c->stage_bufs;
+  st.entry_cap = c->entry_cap;
+  st.closure_cap = c->clo_cap;
   *out = c;
   return FM_OK;
 }
@@ -988,8 +1013,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   const int grid = std::min(c->n_sm * c->ctas_per_sm, std::max(1, ta.n_tiles_all));
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs, wj, v,
-                              b, g, c->jpart, c->status, ma, s));
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
+                              c->stage_bufs, wj, v, b, g, c->jpart, c->status, ma, s));
     c->launches++;
   }
   if (wj) {

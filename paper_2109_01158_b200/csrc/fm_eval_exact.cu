@@ -40,9 +40,10 @@ struct PipeLayout {
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
   __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
   __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
-  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb) {
+  __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
+  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int ns) {
     return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() + ents(entry_cap) +
-           32 * 8 + 8 * 8;
+           ns * staging(D) + 32 * 8 + 8 * 8;
   }
 };
 
@@ -139,7 +140,7 @@ struct RowSrc {
   uint2 loc;
 };
 
-template <int DIM, int MODEL, bool WJ, int CT, int NB, int MINB>
+template <int DIM, int MODEL, bool WJ, int CT, int NB, int NS, int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, unsigned long long *status,
@@ -160,8 +161,9 @@ __global__ void __launch_bounds__(CT, MINB)
   int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * L::stage() + NB * L::nodev(D, CAP));
   int4 *desc = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(cids) + L::cids(CAP));
   uint16_t *ents = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(desc) + L::desc());
-  double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(ents) +
-                                           L::ents(a.entry_cap));
+  unsigned char *stgx0 = reinterpret_cast<unsigned char *>(ents) + L::ents(a.entry_cap);
+  auto stgx = [&](int k) { return reinterpret_cast<double *>(stgx0 + k * L::staging(D)); };
+  double *red = reinterpret_cast<double *>(stgx0 + NS * L::staging(D));
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // record stages
   uint64_t *nfull = full + 2;                               // node-value buffers
   uint64_t *cfull = nfull + 2;                              // closure ids
@@ -362,8 +364,9 @@ __global__ void __launch_bounds__(CT, MINB)
             jsum += E.vol * density<DIM, MODEL>(F, mdl);
           }
         }
-        __syncthreads();  // every row of the stage has been read
-        double *stage_d = reinterpret_cast<double *>(stg(s));
+        // contributions -> staging buffer (separate from the record stages, so
+        // the TMA engine never overwrites generic-proxy writes: no proxy fence)
+        double *stage_d = stgx(NS == 2 ? (q & 1) : 0);
         if (valid && has_nodes) {
 #pragma unroll
           for (int l = 0; l < NV; ++l)
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(CT, MINB)
               stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
             }
         }
-        __syncthreads();  // contributions staged
+        __syncthreads();  // contributions staged; every record of stage s read
         if (my_node && !(mdl.dbg & 2)) {
           const int lim = c0 + CT;
           while (cur < end) {
@@ -388,12 +391,13 @@ __global__ void __launch_bounds__(CT, MINB)
             ++cur;
           }
         }
-        // the staging stores / record, descriptor and entry reads of this chunk
-        // must be ordered before the bulk copies that refill these buffers
-        fence_proxy_async();
-        __syncthreads();  // stage s, descriptors and entries free
+        // one staging buffer: it must be consumed before the next chunk writes
+        // it; two: the next chunk's barrier already orders this consumption
+        // before the write two chunks ahead
+        if (NS == 1) __syncthreads();
         comp.advance(a);
       }
+      if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
       if (my_node) {
         const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
         int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
@@ -411,52 +415,64 @@ __global__ void __launch_bounds__(CT, MINB)
   }
 }
 
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb) {
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns) {
   if (ct == 128)
-    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb)
-                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb);
-  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb)
-                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb);
+    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb, ns)
+                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb, ns);
+  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb, ns)
+                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb, ns);
 }
 
-template <int DIM, int MODEL, int CT, int NB, int MINB>
+template <int DIM, int MODEL, int CT, int NB, int NS>
 static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double *v,
                               const double *b, double *g, double *jpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB);
-  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, MINB>
-              : k_tile_exact<DIM, MODEL, false, CT, NB, MINB>;
+  constexpr int MINB = CT == 128 ? 4 : 2;  // <= 128 registers per thread
+  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB, NS);
+  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, NS, MINB>
+              : k_tile_exact<DIM, MODEL, false, CT, NB, NS, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, status, m);
   return cudaGetLastError();
 }
 
+template <int DIM, int MODEL, int CT>
+static cudaError_t launch_ct(const TileArgs &a, int grid, int nb, int ns, bool wj,
+                             const double *v, const double *b, double *g, double *jpart,
+                             unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
+  if (nb == 2 && ns == 2)
+    return launch_cfg<DIM, MODEL, CT, 2, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
+  if (nb == 2) return launch_cfg<DIM, MODEL, CT, 2, 1>(a, grid, wj, v, b, g, jpart, status, m, s);
+  if (ns == 2) return launch_cfg<DIM, MODEL, CT, 1, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
+  return launch_cfg<DIM, MODEL, CT, 1, 1>(a, grid, wj, v, b, g, jpart, status, m, s);
+}
+
 template <int DIM, int MODEL>
-static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, bool wj,
+static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, int ns, bool wj,
                                   const double *v, const double *b, double *g, double *jpart,
                                   unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
-  if (ct == 128) {
-    if (nb == 2) return launch_cfg<DIM, MODEL, 128, 2, 4>(a, grid, wj, v, b, g, jpart, status, m, s);
-    return launch_cfg<DIM, MODEL, 128, 1, 4>(a, grid, wj, v, b, g, jpart, status, m, s);
-  }
-  if (nb == 2) return launch_cfg<DIM, MODEL, 256, 2, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
-  return launch_cfg<DIM, MODEL, 256, 1, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
+  if (DIM == 3 && ct == 128)
+    return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, wj, v, b, g, jpart, status, m, s);
+  return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, wj, v, b, g, jpart, status, m, s);
 }
 
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
-                              bool wj, const double *v, const double *b, double *g,
+                              int ns, bool wj, const double *v, const double *b, double *g,
                               double *jpart, unsigned long long *status, const ModelArgs &m,
                               cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
+                                                m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
+                                                m, s);
   if (dim == 2)
-    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, wj, v, b, g, jpart, status, m,
-                                                  s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, wj, v, b, g, jpart, status, m, s);
+    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart,
+                                                  status, m, s);
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
+                                                m, s);
 }
 
 }  // namespace fm

@@ -10,11 +10,12 @@ namespace fm {
 
 // persistent pipelined fused J + exact gradient; grid = ctas_per_sm * #SMs, CONSUMERS threads
 // ct = threads per CTA = chunk size = max tile nodes (128 or 256); nb = node-value buffers
+// ns = staging buffers (2: one barrier per chunk, 1: two)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
-                              bool wj, const double *v, const double *b, double *g,
+                              int ns, bool wj, const double *v, const double *b, double *g,
                               double *jpart, unsigned long long *status, const ModelArgs &m,
                               cudaStream_t s);
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb);
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
                            size_t smem_entries, const double *v, const double *b, double eps,
