@@ -332,7 +332,7 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
                             const int32_t *owner_of, const uint64_t *ukeys, const int32_t *ptr,
                             const int32_t *entry_abs, const int32_t *entry_off,
                             const int32_t *free_node, const int32_t *free_out,
-                            const uint8_t *free_mask, uint16_t *entries, int4 *desc,
+                            const uint8_t *free_mask, int ct, uint16_t *entries, int4 *desc,
                             unsigned long long *overflow) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -362,7 +362,21 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
     }
     const int fo = free_out[r];
     if (fo >= (1 << OUT_MASK_SHIFT)) atomicAdd(overflow, 1ull);
-    desc[k] = make_int4(entry_off[k], n, free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
+    desc[2 * k] =
+        make_int4(entry_off[k], n, free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
+    // entries per chunk of ct tile elements: 16 chunks x 8 bits
+    unsigned cc[4] = {0, 0, 0, 0};
+    for (int p = 0; p < n; ++p) {
+      const int ch = (out[p] >> 2) / ct;
+      if (ch >= MAX_CHUNKS) {
+        atomicAdd(overflow, 1ull);
+        continue;
+      }
+      const unsigned sh = (ch & 3) * 8, old = (cc[ch >> 2] >> sh) & 255u;
+      if (old == 255u) atomicAdd(overflow, 1ull);
+      cc[ch >> 2] += 1u << sh;
+    }
+    desc[2 * k + 1] = make_int4((int)cc[0], (int)cc[1], (int)cc[2], (int)cc[3]);
   }
 }
 
@@ -466,8 +480,8 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->ne = m->ne;
   c->nfree = m->nfree;
   c->p_total = m->p_total;
-  // tile = CTA width: 128 nodes (3D, 8x4x4 boxes, 4 CTAs/SM) or 256 (2D, 16x16)
-  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : (dim == 3 ? 128 : 256);
+  // tile = CTA width: 256 nodes (3D 8x8x4 boxes, 2D 16x16) or 128 (3D 8x4x4)
+  int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : 256;
   NT = NT <= 128 ? 128 : 256;
   int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? (NT == 128 ? 4 : 8) : 16, dim == 3 ? 4 : 1};
   if (tiling)
@@ -848,7 +862,11 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(dmalloc(&c->meta, hm.size(), &B));
   CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
   CK(dmalloc(&c->flags, M + 16, &B));
-  CK(dmalloc(&c->node_desc, std::max<int64_t>(nfree, 1), &B));
+  CK(dmalloc(&c->node_desc, 2 * std::max<int64_t>(nfree, 1), &B));  // 2 x int4 per node
+  if (c->max_tile_elems > MAX_CHUNKS * c->tile_nodes) {
+    set_error("a node tile has more than 16 chunks of elements; use smaller tiles");
+    return fail(FM_INVALID_ARG);
+  }
   CK(dmalloc(&c->node_entries, entry_total + 8, &B));
   c->n_node_entries = entry_total;
   CK(cudaMemsetAsync(c->halo_ids, 0, (halo_total + 4) * 4, s));
@@ -877,8 +895,8 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     k_node_desc<<<grid_for(nfree, 256), 256, 0, s>>>(
         nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), m->p_prefix, m->p_elems, m->p_slot,
         owner_of.as<int32_t>(), ukeys.as<uint64_t>(), tptr.as<int32_t>(), eabs.as<int32_t>(),
-        eoff.as<int32_t>(), c->free_node, c->free_out, c->free_mask, c->node_entries,
-        c->node_desc, ovf.as<unsigned long long>());
+        eoff.as<int32_t>(), c->free_node, c->free_out, c->free_mask, c->tile_nodes,
+        c->node_entries, c->node_desc, ovf.as<unsigned long long>());
     CK(cudaGetLastError());
     unsigned long long h_ovf = 0;
     CK(cudaMemcpyAsync(&h_ovf, ovf.p, 8, cudaMemcpyDeviceToHost, s));

@@ -28,6 +28,7 @@ namespace fm {
 constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
 constexpr int CONSUMERS = 256;         // threads per tile CTA = chunk size = max tile nodes
 constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
+constexpr int MAX_CHUNKS = 16;         // per-chunk entry counts in node_desc[2k+1] (8 bits each)
 
 template <int DIM> struct RecBytes;
 template <> struct RecBytes<2> { static constexpr int value = 80; };
@@ -162,7 +163,8 @@ struct TileArgs {
   const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements
   const int32_t *closure;      // node ids of the tile closures
   const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
-  const int4 *node_desc;       // {entry_off, entry_count, node id, out | mask << 28}
+  const int4 *node_desc;       // 2 per node: {entry_off, entry_count, node id, out | mask << 28},
+                               // {entries per chunk, 8 bits x 16 chunks}
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
   const int32_t *rank_of;      // node -> free rank or -1
   int n_tiles;                 // node tiles

@@ -38,7 +38,7 @@ struct PipeLayout {
   __host__ __device__ static size_t stage() { return r16((size_t)CT * RB); }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
-  __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
+  __host__ __device__ static size_t desc() { return (size_t)CT * 32; }
   __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
   __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int ns) {
@@ -227,9 +227,6 @@ __global__ void __launch_bounds__(CT, MINB)
                  full + s);
     }
     if (tid >= n_own && tid < cnt) {
-      if ((mdl.dbg & 4) && (rs.src < 0 || !rs.halo))
-        printf("FMCHK src t=%d c0=%d tid=%d src=%d halo=%d own=%d ne=%d\n", x.t, x.c0, tid, rs.src,
-               rs.halo, x.tm.own_count, x.ne);
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
         cp_async16(stg(s) + tid * RB + c * 16, a.aos + (int64_t)rs.src * RB + c * 16);
@@ -262,7 +259,7 @@ __global__ void __launch_bounds__(CT, MINB)
       const TileMeta tm = comp.tm;
       // ---- tile start: descriptors + entries (single buffer: previous tile done)
       if (tid == 0) {
-        const uint32_t nb = (uint32_t)tm.node_count * 16;
+        const uint32_t nb = (uint32_t)tm.node_count * 32;
         const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
         mbar_arrive_expect_tx(tfull, nb + eb);
         if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
@@ -294,18 +291,16 @@ __global__ void __launch_bounds__(CT, MINB)
       mbar_wait(tfull, j & 1);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
-      int cur = 0, end = 0, outw = 0;
+      int cur = 0, outw = 0;
+      int4 cnts = make_int4(0, 0, 0, 0);  // this node's entries per chunk (8 bits each)
       double bj[D], acc[D];
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
       if (my_node) {
-        const int4 nd = desc[tid];
+        const int4 nd = desc[2 * tid];
+        cnts = desc[2 * tid + 1];
         cur = nd.x;
-        end = nd.x + nd.y;
         outw = nd.w;
-        if ((mdl.dbg & 4) && (nd.x < 0 || nd.x + nd.y > tm.entry_count || nd.z < 0))
-          printf("FMCHK desc t=%d tid=%d x=%d y=%d z=%d w=%d ecount=%d\n", comp.t, tid, nd.x,
-                 nd.y, nd.z, nd.w, tm.entry_count);
         if (b) {
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
@@ -332,14 +327,6 @@ __global__ void __launch_bounds__(CT, MINB)
             E.loc[1] = this_row.loc.x >> 16;
             E.loc[2] = this_row.loc.y & 0xffff;
             if constexpr (DIM == 3) E.loc[3] = this_row.loc.y >> 16;
-          }
-          if (mdl.dbg & 4) {  // bounds checks (debug)
-            for (int l = 0; l < NV; ++l)
-              if (E.loc[l] >= tm.clo_count) {
-                printf("FMCHK loc t=%d e=%d l=%d loc=%d clo=%d halo=%d own=%d\n", comp.t, e, l,
-                       E.loc[l], tm.clo_count, this_row.halo, tm.own_count);
-                E.loc[l] = 0;
-              }
           }
           double vv[D][NV];
 #pragma unroll
@@ -380,16 +367,33 @@ __global__ void __launch_bounds__(CT, MINB)
         }
         __syncthreads();  // contributions staged; every record of stage s read
         if (my_node && !(mdl.dbg & 2)) {
-          const int lim = c0 + CT;
-          while (cur < end) {
-            const int en = ents[cur];
-            const int te = en >> 2;
-            if (te >= lim) break;
-            const double *src = stage_d + (te - c0) + (en & 3) * D * CT;
+          // this node's entries of the chunk: a known count, so the loads of
+          // two entries are issued together; the order (ascending tile element)
+          // is the fixed summation order
+          const int ch = c0 / CT;
+          const int cword = ch < 4 ? cnts.x : ch < 8 ? cnts.y : ch < 12 ? cnts.z : cnts.w;
+          const int n = (cword >> ((ch & 3) * 8)) & 255;
+          int i = 0;
+          for (; i + 1 < n; i += 2) {
+            const int e0 = ents[cur + i], e1 = ents[cur + i + 1];
+            const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
+            const double *s1 = stage_d + ((e1 >> 2) - c0) + (e1 & 3) * D * CT;
+            double x0[D], x1[D];
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] += src[k * CT];
-            ++cur;
+            for (int k = 0; k < D; ++k) {
+              x0[k] = s0[k * CT];
+              x1[k] = s1[k * CT];
+            }
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc[k] = (acc[k] + x0[k]) + x1[k];
           }
+          if (i < n) {
+            const int e0 = ents[cur + i];
+            const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
+          }
+          cur += n;
         }
         // one staging buffer: it must be consumed before the next chunk writes
         // it; two: the next chunk's barrier already orders this consumption
