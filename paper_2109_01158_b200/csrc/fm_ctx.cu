@@ -362,21 +362,20 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
     }
     const int fo = free_out[r];
     if (fo >= (1 << OUT_MASK_SHIFT)) atomicAdd(overflow, 1ull);
-    desc[2 * k] =
-        make_int4(entry_off[k], n, free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
-    // entries per chunk of ct tile elements: 16 chunks x 8 bits
-    unsigned cc[4] = {0, 0, 0, 0};
+    // entries per chunk of ct tile elements (5 bits x MAX_CHUNKS) packed with the
+    // tile-local entry offset (13 bits): x = off | c0..c2 << 13, y = c3..c8
+    unsigned long long cc = 0;
     for (int p = 0; p < n; ++p) {
       const int ch = (out[p] >> 2) / ct;
-      if (ch >= MAX_CHUNKS) {
+      if (ch >= MAX_CHUNKS || ((cc >> (5 * ch)) & 31ull) == 31ull) {
         atomicAdd(overflow, 1ull);
         continue;
       }
-      const unsigned sh = (ch & 3) * 8, old = (cc[ch >> 2] >> sh) & 255u;
-      if (old == 255u) atomicAdd(overflow, 1ull);
-      cc[ch >> 2] += 1u << sh;
+      cc += 1ull << (5 * ch);
     }
-    desc[2 * k + 1] = make_int4((int)cc[0], (int)cc[1], (int)cc[2], (int)cc[3]);
+    if (entry_off[k] >= (1 << 13)) atomicAdd(overflow, 1ull);
+    desc[k] = make_int4(entry_off[k] | (int)((cc & 0x7fffull) << 13), (int)(cc >> 15),
+                        free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
   }
 }
 
@@ -862,9 +861,9 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(dmalloc(&c->meta, hm.size(), &B));
   CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
   CK(dmalloc(&c->flags, M + 16, &B));
-  CK(dmalloc(&c->node_desc, 2 * std::max<int64_t>(nfree, 1), &B));  // 2 x int4 per node
+  CK(dmalloc(&c->node_desc, std::max<int64_t>(nfree, 1), &B));
   if (c->max_tile_elems > MAX_CHUNKS * c->tile_nodes) {
-    set_error("a node tile has more than 16 chunks of elements; use smaller tiles");
+    set_error("a node tile has more than 9 chunks of elements; use smaller tile boxes");
     return fail(FM_INVALID_ARG);
   }
   CK(dmalloc(&c->node_entries, entry_total + 8, &B));

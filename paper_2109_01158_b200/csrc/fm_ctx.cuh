@@ -28,7 +28,15 @@ namespace fm {
 constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
 constexpr int CONSUMERS = 256;         // threads per tile CTA = chunk size = max tile nodes
 constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
-constexpr int MAX_CHUNKS = 16;         // per-chunk entry counts in node_desc[2k+1] (8 bits each)
+constexpr int MAX_CHUNKS = 9;          // per-chunk entry counts in node_desc.x/.y (5 bits each)
+constexpr int ENTRY_OFF_MASK = (1 << 13) - 1;  // node_desc.x bits 0..12: tile-local entry offset
+
+// entries of this node in chunk ch of its tile (node_desc packing, see k_node_desc)
+__device__ __forceinline__ int chunk_count(int4 nd, int ch) {
+  const unsigned long long cc =
+      ((unsigned long long)(unsigned)nd.y << 15) | ((unsigned)nd.x >> 13);
+  return (int)((cc >> (5 * ch)) & 31ull);
+}
 
 template <int DIM> struct RecBytes;
 template <> struct RecBytes<2> { static constexpr int value = 80; };
@@ -163,8 +171,8 @@ struct TileArgs {
   const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements
   const int32_t *closure;      // node ids of the tile closures
   const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
-  const int4 *node_desc;       // 2 per node: {entry_off, entry_count, node id, out | mask << 28},
-                               // {entries per chunk, 8 bits x 16 chunks}
+  const int4 *node_desc;       // {entry_off | chunk counts, chunk counts, node id,
+                               //  out | mask << 28} (see chunk_count)
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
   const int32_t *rank_of;      // node -> free rank or -1
   int n_tiles;                 // node tiles

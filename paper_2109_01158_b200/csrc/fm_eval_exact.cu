@@ -38,7 +38,7 @@ struct PipeLayout {
   __host__ __device__ static size_t stage() { return r16((size_t)CT * RB); }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
-  __host__ __device__ static size_t desc() { return (size_t)CT * 32; }
+  __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
   __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
   __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int ns) {
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(CT, MINB)
       const TileMeta tm = comp.tm;
       // ---- tile start: descriptors + entries (single buffer: previous tile done)
       if (tid == 0) {
-        const uint32_t nb = (uint32_t)tm.node_count * 32;
+        const uint32_t nb = (uint32_t)tm.node_count * 16;
         const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
         mbar_arrive_expect_tx(tfull, nb + eb);
         if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
@@ -292,14 +292,13 @@ __global__ void __launch_bounds__(CT, MINB)
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
       int cur = 0, outw = 0;
-      int4 cnts = make_int4(0, 0, 0, 0);  // this node's entries per chunk (8 bits each)
+      int4 nd = make_int4(0, 0, 0, 0);  // node descriptor (entry offset, per-chunk counts)
       double bj[D], acc[D];
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
       if (my_node) {
-        const int4 nd = desc[2 * tid];
-        cnts = desc[2 * tid + 1];
-        cur = nd.x;
+        nd = desc[tid];
+        cur = nd.x & ENTRY_OFF_MASK;
         outw = nd.w;
         if (b) {
 #pragma unroll
@@ -370,9 +369,7 @@ __global__ void __launch_bounds__(CT, MINB)
           // this node's entries of the chunk: a known count, so the loads of
           // two entries are issued together; the order (ascending tile element)
           // is the fixed summation order
-          const int ch = c0 / CT;
-          const int cword = ch < 4 ? cnts.x : ch < 8 ? cnts.y : ch < 12 ? cnts.z : cnts.w;
-          const int n = (cword >> ((ch & 3) * 8)) & 255;
+          const int n = chunk_count(nd, c0 / CT);
           int i = 0;
           for (; i + 1 < n; i += 2) {
             const int e0 = ents[cur + i], e1 = ents[cur + i + 1];

@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
     ents[q] = a.entries[tm.entry_begin + q];
   int cur = 0, end = 0, node = 0, outw = 0;
   if (has_node) {
-    const int4 nd = a.node_desc[2 * (tm.node_begin + threadIdx.x)];
-    cur = nd.x;
-    end = nd.x + nd.y;
+    const int4 nd = a.node_desc[tm.node_begin + threadIdx.x];
+    cur = nd.x & ENTRY_OFF_MASK;
+    end = cur;
+    for (int ch = 0; ch < MAX_CHUNKS; ++ch) end += chunk_count(nd, ch);
     node = nd.z;
     outw = nd.w;
   }
