@@ -403,6 +403,11 @@ static ModelArgs model_args(const fm_model *m) {
     return e ? atoi(e) : 0;
   }();
   a.dbg = ablate;
+  static const int pf = [] {
+    const char *e = getenv("FM_PF_TILES");
+    return e ? atoi(e) : 1;
+  }();
+  a.pf_tiles = pf;
   return a;
 }
 

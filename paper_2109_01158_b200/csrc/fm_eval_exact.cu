@@ -32,6 +32,7 @@ namespace fm {
 
 __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; }
 
+
 template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
@@ -264,6 +265,14 @@ __global__ void __launch_bounds__(CT, MINB)
         mbar_arrive_expect_tx(tfull, nb + eb);
         if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
         if (eb) bulk_g2s(ents, a.entries + tm.entry_begin, eb, tfull);
+        // L2 prefetch of the own records of a tile PF_TILES ahead (one bulk op):
+        // keeps DRAM busy beyond the two shared-memory stages
+        const int tp = comp.t + mdl.pf_tiles * gridDim.x;
+        if (mdl.pf_tiles > 0 && tp < a.n_tiles_all) {
+          const TileMeta tq = a.meta[tp];
+          if (tq.own_count)
+            bulk_prefetch_l2(a.aos + (int64_t)tq.own_begin * RB, (uint32_t)tq.own_count * RB);
+        }
       }
       const double *nv;
       if (NB == 2) {

@@ -73,6 +73,12 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
                : "memory");
 }
 
+// Bulk prefetch of a contiguous global range into L2 (no shared memory, no
+// completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Order this thread's generic-proxy shared-memory accesses before later
 // async-proxy (bulk copy / TMA) accesses to the same buffers: required before a
 // buffer that was written or read with ST/LD is refilled by cp.async.bulk.
