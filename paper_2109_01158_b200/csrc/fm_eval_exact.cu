@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(CT, MINB)
       gather_nodev(comp.tm.clo_count, 0);
       fence_proxy_async();  // cids reads before the bulk refill
       __syncthreads();
-      issue_clo(comp.t + gridDim.x, comp.tm_next);
+      issue_clo(comp.t + gridDim.x);
     }
     RowSrc cur_row = row_src(comp);
     issue_records(comp, 0, cur_row);
