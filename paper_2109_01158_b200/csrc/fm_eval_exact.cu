@@ -114,7 +114,7 @@ __device__ __forceinline__ void grad_F_fma(const double (&vv)[D][DIM + 1],
 template <int CT>
 struct Cursor {
   int t, c0, ne;
-  TileMeta tm, tm_next;  // tm_next: the following tile's meta, loaded one tile early
+  TileMeta tm;
   __device__ void load(const TileArgs &a) {
     if (t < a.n_tiles_all) {
       tm = a.meta[t];
@@ -122,7 +122,6 @@ struct Cursor {
     } else {
       ne = 0;
     }
-    if (t + (int)gridDim.x < a.n_tiles_all) tm_next = a.meta[t + gridDim.x];
   }
   __device__ bool valid(const TileArgs &a) const { return t < a.n_tiles_all; }
   __device__ void advance(const TileArgs &a) {
@@ -130,13 +129,7 @@ struct Cursor {
     if (c0 >= ne) {
       c0 = 0;
       t += gridDim.x;
-      if (t < a.n_tiles_all) {
-        tm = tm_next;  // no load latency on the tile crossing
-        ne = tm.own_count + tm.halo_count;
-        if (t + (int)gridDim.x < a.n_tiles_all) tm_next = a.meta[t + gridDim.x];
-      } else {
-        ne = 0;
-      }
+      load(a);
     }
   }
 };
@@ -188,8 +181,9 @@ __global__ void __launch_bounds__(CT, MINB)
   }
   __syncthreads();
 
-  auto issue_clo = [&](int t, const TileMeta &tm) {  // closure ids of tile t -> cids
+  auto issue_clo = [&](int t) {  // closure ids of tile t -> cids
     if (tid == 0 && t < a.n_tiles_all) {
+      const TileMeta tm = a.meta[t];
       const uint32_t bytes = (uint32_t)r16((size_t)tm.clo_count * 4);
       mbar_arrive_expect_tx(cfull, bytes);
       bulk_g2s(cids, a.closure + tm.clo_begin, bytes, cfull);
@@ -243,11 +237,11 @@ __global__ void __launch_bounds__(CT, MINB)
 
   double jsum = 0.0;
   bool bad_any = false;
-  Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}, TileMeta{}};
+  Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}};
   comp.load(a);
   if (comp.valid(a)) {
     // ---- prologue: closure ids (+ node values with NB = 2) and chunk 0 records
-    issue_clo(comp.t, comp.tm);
+    issue_clo(comp.t);
     if (NB == 2) {
       mbar_wait(cfull, 0);
       gather_nodev(comp.tm.clo_count, 0);
@@ -275,7 +269,7 @@ __global__ void __launch_bounds__(CT, MINB)
         // keeps DRAM busy beyond the two shared-memory stages
         const int tp = comp.t + mdl.pf_tiles * gridDim.x;
         if (mdl.pf_tiles > 0 && tp < a.n_tiles_all) {
-          const TileMeta tq = mdl.pf_tiles == 1 ? comp.tm_next : a.meta[tp];
+          const TileMeta tq = a.meta[tp];
           if (tq.own_count)
             bulk_prefetch_l2(a.aos + (int64_t)tq.own_begin * RB, (uint32_t)tq.own_count * RB);
         }
@@ -286,10 +280,10 @@ __global__ void __launch_bounds__(CT, MINB)
         const int tn = comp.t + gridDim.x;
         if (tn < a.n_tiles_all) {
           mbar_wait(cfull, (j + 1) & 1);
-          gather_nodev(comp.tm_next.clo_count, (j + 1) & 1);
+          gather_nodev(a.meta[tn].clo_count, (j + 1) & 1);
           fence_proxy_async();
           __syncthreads();  // cids consumed
-          if (tn + (int)gridDim.x < a.n_tiles_all) issue_clo(tn + gridDim.x, a.meta[tn + gridDim.x]);
+          issue_clo(tn + gridDim.x);
         }
         mbar_wait(nfull + (j & 1), (j >> 1) & 1);
         nv = nodev(j & 1);
@@ -300,7 +294,7 @@ __global__ void __launch_bounds__(CT, MINB)
         mbar_wait(nfull, j & 1);
         fence_proxy_async();
         __syncthreads();  // cids consumed, every thread's copies visible
-        issue_clo(comp.t + gridDim.x, comp.tm_next);
+        issue_clo(comp.t + gridDim.x);
         nv = nodev(0);
       }
       mbar_wait(tfull, j & 1);
