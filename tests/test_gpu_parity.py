@@ -279,3 +279,41 @@ def test_determinism_bitwise():
     for _ in range(3):
         assert torch.equal(pr.dm.exact_gradient(pr.v, pr.model, pr.b), a)
         assert torch.equal(pr.dm.energy(pr.v, pr.model, pr.b), Ja)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_field_stream_matches_serial(depth):
+    """streaming.FieldStream: overlapped H2D / kernel / D2H of distinct host
+    fields gives each field exactly its serial (J, grad J)."""
+    from paper_2109_01158_b200.streaming import FieldStream
+    pr = problems.beam(24, 12, 12, seed=5)
+    n = 7
+    gen = torch.Generator().manual_seed(depth)
+    fields = [(pr.v.cpu() + 1e-3 * torch.rand(pr.v.shape, generator=gen, dtype=torch.float64))
+              .pin_memory() for _ in range(n)]
+    grads = [torch.empty(pr.dm.nfree_dofs, dtype=torch.float64).pin_memory() for _ in range(n)]
+    Js = [torch.empty(3, dtype=torch.float64).pin_memory() for _ in range(n)]
+    fs = FieldStream(pr.dm, pr.model, pr.b, depth=depth)
+    fs.map(fields, grads, Js)
+    for i in range(n):
+        J = torch.empty(3, dtype=torch.float64, device="cuda")
+        g = pr.dm.exact_gradient(fields[i].cuda(), pr.model, pr.b, J=J)
+        assert torch.equal(grads[i], g.cpu()), i
+        assert torch.equal(Js[i], J.cpu()), i
+    t = fs.submit(fields[0], grads[1], Js[1])
+    fs.wait(t)
+    assert torch.equal(grads[1], grads[0])
+    fs.synchronize()
+
+
+def test_field_stream_latches_inadmissible():
+    from paper_2109_01158_b200.streaming import FieldStream
+    pr = problems.beam(8, 4, 4, seed=5)
+    bad = pr.v.cpu().clone()
+    bad.view(-1, 3)[:, 0] *= -1.0  # mirror x: det F < 0 everywhere
+    g = torch.empty(pr.dm.nfree_dofs, dtype=torch.float64).pin_memory()
+    fs = FieldStream(pr.dm, pr.model, pr.b)
+    fs.submit(pr.v.cpu().pin_memory(), g)
+    fs.submit(bad.pin_memory(), g)
+    with pytest.raises(fb.InadmissibleStateError):
+        fs.synchronize()
