@@ -236,8 +236,9 @@ template <int DIM>
 __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int64_t orph0,
                            int n_tiles, int ot, const int32_t *s2o, const int32_t *o2s,
                            const int64_t *conn, const uint64_t *ckeys, const int32_t *cstart,
-                           const int32_t *split, const int32_t *halo_begin, uint8_t *aos,
-                           uint2 *halo_loc, unsigned long long *overflow) {
+                           const int32_t *ptr, const int32_t *split, const int32_t *tpos,
+                           const int32_t *halo_begin, uint8_t *aos, uint2 *halo_loc,
+                           unsigned long long *overflow) {
   constexpr int NV = DIM + 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + n_orph;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -269,7 +270,7 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
       packed |= (uint64_t)(idx & 0xffff) << (16 * l);
     }
     if (halo) {
-      halo_loc[halo_begin[t] + (i - split[t])] =
+      halo_loc[halo_begin[t] + tpos[i] - (split[t] - ptr[t])] =
           make_uint2((unsigned)(packed & 0xffffffffull), (unsigned)(packed >> 32));
     } else {
       uint64_t *w = reinterpret_cast<uint64_t *>(aos + s * RecBytes<DIM>::value);
@@ -315,22 +316,99 @@ __global__ void k_tile_bounds(int n_tiles, int64_t M, const uint64_t *ukeys, int
   }
 }
 
-__global__ void k_halo_ids(int64_t M, const uint64_t *ukeys, const int32_t *split,
-                           const int32_t *halo_begin, const int32_t *o2s, int32_t *halo_ids) {
+// Tile element positions ("dealt" order).  The sorted (tile, halo?, element)
+// list puts spatial neighbours next to each other, so one node's elements
+// would crowd into one or two chunks of ct rows and that chunk's consume
+// step would wait on the node thread with the most entries.  Instead the
+// r-th element of the own (resp. halo) range [A, B) goes to the r-th position
+// of that range enumerated by (position mod ct, position div ct): consecutive
+// elements land in consecutive chunks, so each node meets about
+// (patch size / chunks) of its elements per chunk.  One block per tile,
+// thread s = row s of every chunk.  deal == 0 keeps the sorted order.
+__global__ void k_tile_deal(int n_tiles, const int32_t *ptr, const int32_t *split, int ct, int deal,
+                            int32_t *tpos) {
+  extern __shared__ int32_t cnt_s[];
+  const int t = blockIdx.x;
+  if (t >= n_tiles) return;
+  const int no = split[t] - ptr[t], nh = ptr[t + 1] - split[t];
+  for (int part = 0; part < 2; ++part) {
+    const int A = part ? no : 0, B = part ? no + nh : no;
+    const int64_t base = part ? split[t] : ptr[t];
+    if (!deal) {
+      for (int r = threadIdx.x; r < B - A; r += blockDim.x) tpos[base + r] = A + r;
+      continue;
+    }
+    // rows s of chunks k with A <= s + ct k < B
+    int kmin[4], kcnt[4];
+    for (int u = 0; u < 4; ++u) {
+      const int s = threadIdx.x + u * blockDim.x;
+      kmin[u] = kcnt[u] = 0;
+      if (s < ct) {
+        const int k0 = A > s ? (A - s + ct - 1) / ct : 0;
+        const int k1 = B - 1 >= s ? (B - 1 - s) / ct : -1;
+        kmin[u] = k0;
+        kcnt[u] = max(0, k1 - k0 + 1);
+        cnt_s[s] = kcnt[u];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan over rows (ct <= 1024)
+      int run = 0;
+      for (int s = 0; s < ct; ++s) {
+        const int x = cnt_s[s];
+        cnt_s[s] = run;
+        run += x;
+      }
+    }
+    __syncthreads();
+    for (int u = 0; u < 4; ++u) {
+      const int s = threadIdx.x + u * blockDim.x;
+      if (s < ct)
+        for (int j = 0; j < kcnt[u]; ++j) tpos[base + cnt_s[s] + j] = s + ct * (kmin[u] + j);
+    }
+    __syncthreads();
+  }
+}
+
+// own elements: storage position own_begin + tpos (storage order = dealt order)
+__global__ void k_deal_storage(int64_t M, const uint64_t *ukeys, const int32_t *ptr,
+                               const int32_t *own_ptr, const int32_t *tpos, int32_t *s2o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = ukeys[i];
+    if ((k >> 32) & 1) continue;
+    const int t = (int)(k >> 33);
+    s2o[own_ptr[t] + tpos[i]] = (int32_t)(k & 0xffffffffull);
+  }
+}
+
+// owned-slot masks in tile element (dealt) order
+__global__ void k_deal_flags(int64_t M, const uint64_t *ukeys, const int32_t *ptr,
+                             const int32_t *tpos, const uint8_t *umask, uint8_t *flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(ukeys[i] >> 33);
+    flags[ptr[t] + tpos[i]] = umask[i];
+  }
+}
+
+__global__ void k_halo_ids(int64_t M, const uint64_t *ukeys, const int32_t *ptr,
+                           const int32_t *split, const int32_t *tpos, const int32_t *halo_begin,
+                           const int32_t *o2s, int32_t *halo_ids) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = ukeys[i];
     if (!((k >> 32) & 1)) continue;
     const int t = (int)(k >> 33);
     const int64_t e = (int64_t)(k & 0xffffffffull);
-    halo_ids[halo_begin[t] + (i - split[t])] = o2s[e];
+    halo_ids[halo_begin[t] + tpos[i] - (split[t] - ptr[t])] = o2s[e];
   }
 }
 
 __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const int32_t *tile_of_rank,
                             const int64_t *prefix, const int64_t *elems, const int64_t *slot,
                             const int32_t *owner_of, const uint64_t *ukeys, const int32_t *ptr,
-                            const int32_t *entry_abs, const int32_t *entry_off,
+                            const int32_t *tpos, const int32_t *entry_abs, const int32_t *entry_off,
                             const int32_t *free_node, const int32_t *free_out,
                             const uint8_t *free_mask, int ct, uint16_t *entries, int4 *desc,
                             unsigned long long *overflow) {
@@ -350,8 +428,9 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
         int64_t mid = (lo + hi) >> 1;
         if (ukeys[mid] < key) lo = mid + 1; else hi = mid;
       }
-      const int64_t te = lo - lo0;
-      if (te >= MAX_TILE_ELEMS || lo >= hi0 || ukeys[lo] != key) atomicAdd(overflow, 1ull);
+      const bool found = lo < hi0 && ukeys[lo] == key;
+      const int64_t te = found ? tpos[lo] : 0;
+      if (te >= MAX_TILE_ELEMS || !found) atomicAdd(overflow, 1ull);
       uint16_t v = (uint16_t)((te << 2) | slot[q]);
       int p = n++;  // insertion sort by te (entries of one node are few)
       while (p > 0 && out[p - 1] > v) {
@@ -666,25 +745,12 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
                                                                   own_ptr.as<int32_t>());
     CK(cudaGetLastError());
   }
-  k_inverse<<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, o2s.as<int32_t>());
-  CK(cudaGetLastError());
   std::vector<int32_t> h_own(n_tiles + 2);
   CK(cudaMemcpyAsync(h_own.data(), own_ptr.p, (n_tiles + 2) * 4, cudaMemcpyDeviceToHost, s));
 
-  const int rb = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
-  CK(dmalloc(&c->aos, (size_t)ne * rb, &B));
-  CK(dmalloc(&c->conn4, ne, &B));
-  if (dim == 3)
-    k_build_aos<3><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
-                                                     m->dphi, c->aos, c->conn4);
-  else
-    k_build_aos<2><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
-                                                     m->dphi, c->aos, c->conn4);
-  CK(cudaGetLastError());
-
   // 4. tile element lists (own + halo) ----------------------------------------
   int64_t M = 0;
-  Scratch ukeys, umask, tptr, tsplit;
+  Scratch ukeys, umask, tptr, tsplit, tpos;
   CK(tptr.alloc((n_tiles + 1) * 4, s));
   CK(tsplit.alloc((n_tiles + 1) * 4, s));
   std::vector<int32_t> h_ptr(n_tiles + 1, 0), h_split(n_tiles + 1, 0);
@@ -721,7 +787,32 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_ptr.data(), tptr.p, (n_tiles + 1) * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_split.data(), tsplit.p, (n_tiles + 1) * 4, cudaMemcpyDeviceToHost, s));
+    // dealt tile element order; own elements are stored in it (FM_TILE_DEAL=0: sorted order)
+    static const int deal = [] {
+      const char *e = getenv("FM_TILE_DEAL");
+      return e ? atoi(e) : 1;
+    }();
+    CK(tpos.alloc(M * 4, s));
+    k_tile_deal<<<n_tiles, 256, NT * 4, s>>>(n_tiles, tptr.as<int32_t>(), tsplit.as<int32_t>(),
+                                             NT, deal, tpos.as<int32_t>());
+    CK(cudaGetLastError());
+    k_deal_storage<<<grid_for(M, 256), 256, 0, s>>>(M, uk, tptr.as<int32_t>(),
+                                                    own_ptr.as<int32_t>(), tpos.as<int32_t>(),
+                                                    c->storage_to_orig);
+    CK(cudaGetLastError());
   }
+  k_inverse<<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, o2s.as<int32_t>());
+  CK(cudaGetLastError());
+  const int rb = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
+  CK(dmalloc(&c->aos, (size_t)ne * rb, &B));
+  CK(dmalloc(&c->conn4, ne, &B));
+  if (dim == 3)
+    k_build_aos<3><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
+                                                     m->dphi, c->aos, c->conn4);
+  else
+    k_build_aos<2><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
+                                                     m->dphi, c->aos, c->conn4);
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   const int64_t n_orph = (int64_t)ne - h_own[n_tiles];
   // host-side tile metadata
@@ -847,13 +938,15 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     if (dim == 3)
       k_fill_loc<3><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
           M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
-          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tsplit.as<int32_t>(),
-          hb.as<int32_t>(), c->aos, c->halo_loc, ovf.as<unsigned long long>());
+          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tptr.as<int32_t>(),
+          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->aos, c->halo_loc,
+          ovf.as<unsigned long long>());
     else
       k_fill_loc<2><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
           M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
-          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tsplit.as<int32_t>(),
-          hb.as<int32_t>(), c->aos, c->halo_loc, ovf.as<unsigned long long>());
+          o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tptr.as<int32_t>(),
+          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->aos, c->halo_loc,
+          ovf.as<unsigned long long>());
     CK(cudaGetLastError());
     unsigned long long h_ovf = 0;
     CK(cudaMemcpyAsync(&h_ovf, ovf.p, 8, cudaMemcpyDeviceToHost, s));
@@ -876,11 +969,15 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(cudaMemsetAsync(c->halo_ids, 0, (halo_total + 4) * 4, s));
   CK(cudaMemsetAsync(c->node_entries, 0, (entry_total + 8) * 2, s));
   if (M) {
-    CK(cudaMemcpyAsync(c->flags, umask.p, M, cudaMemcpyDeviceToDevice, s));
+    k_deal_flags<<<grid_for(M, 256), 256, 0, s>>>(M, ukeys.as<uint64_t>(), tptr.as<int32_t>(),
+                                                  tpos.as<int32_t>(), umask.as<uint8_t>(),
+                                                  c->flags);
+    CK(cudaGetLastError());
     Scratch hb;
     CK(hb.alloc((n_tiles + 1) * 4, s));
     CK(cudaMemcpyAsync(hb.p, h_halo_begin.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
-    k_halo_ids<<<grid_for(M, 256), 256, 0, s>>>(M, ukeys.as<uint64_t>(), tsplit.as<int32_t>(),
+    k_halo_ids<<<grid_for(M, 256), 256, 0, s>>>(M, ukeys.as<uint64_t>(), tptr.as<int32_t>(),
+                                                 tsplit.as<int32_t>(), tpos.as<int32_t>(),
                                                  hb.as<int32_t>(), o2s.as<int32_t>(),
                                                  c->halo_ids);
     CK(cudaGetLastError());
@@ -898,7 +995,8 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaMemcpyAsync(eabs.p, h_entry_abs.data(), nfree * 4, cudaMemcpyHostToDevice, s));
     k_node_desc<<<grid_for(nfree, 256), 256, 0, s>>>(
         nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), m->p_prefix, m->p_elems, m->p_slot,
-        owner_of.as<int32_t>(), ukeys.as<uint64_t>(), tptr.as<int32_t>(), eabs.as<int32_t>(),
+        owner_of.as<int32_t>(), ukeys.as<uint64_t>(), tptr.as<int32_t>(), tpos.as<int32_t>(),
+        eabs.as<int32_t>(),
         eoff.as<int32_t>(), c->free_node, c->free_out, c->free_mask, c->tile_nodes,
         c->node_entries, c->node_desc, ovf.as<unsigned long long>());
     CK(cudaGetLastError());
