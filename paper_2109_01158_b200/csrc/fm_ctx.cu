@@ -279,6 +279,22 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
   }
 }
 
+// max over (tile, chunk) of the node entries falling in that chunk
+__global__ void k_chunk_entry_max(int n_tiles, const TileMeta *meta, const int4 *desc,
+                                  unsigned int *out) {
+  __shared__ unsigned int cnt[MAX_CHUNKS];
+  const int t = blockIdx.x;
+  if (threadIdx.x < MAX_CHUNKS) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const TileMeta tm = meta[t];
+  for (int k = threadIdx.x; k < tm.node_count; k += blockDim.x) {
+    const int4 nd = desc[tm.node_begin + k];
+    for (int ch = 0; ch < MAX_CHUNKS; ++ch) atomicAdd(&cnt[ch], (unsigned)chunk_count(nd, ch));
+  }
+  __syncthreads();
+  if (threadIdx.x < MAX_CHUNKS) atomicMax(out, cnt[threadIdx.x]);
+}
+
 // (tile, halo?, element) keys of every patch row: te order = own first, then halo
 __global__ void k_pair_keys(int64_t nfree, const int64_t *prefix, const int64_t *elems,
                             const int64_t *slot, const int32_t *tile_of_rank,
@@ -1007,6 +1023,16 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       set_error("internal error: patch entry not found in its tile or output offset overflow");
       return fail(FM_CUDA_ERROR);
     }
+    Scratch cmax;
+    CK(cmax.alloc(4, s));
+    CK(cudaMemsetAsync(cmax.p, 0, 4, s));
+    k_chunk_entry_max<<<n_tiles, 256, 0, s>>>(n_tiles, c->meta, c->node_desc,
+                                               cmax.as<unsigned int>());
+    CK(cudaGetLastError());
+    unsigned int h_cmax = 0;
+    CK(cudaMemcpyAsync(&h_cmax, cmax.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->chunk_entry_cap = ((int)h_cmax + 7) / 8 * 8;
   }
 
   // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads; shared memory
@@ -1160,8 +1186,13 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
   TimedLaunch tl(c, s);
+  const int dm = model->kind == FM_MODEL_NEOHOOKEAN ? c->dim : 1;
+  if (tile_fd_smem(c->dim, dm, c->clo_cap, c->chunk_entry_cap, c->tile_nodes) > 227 * 1024) {
+    set_error("FD tile staging exceeds shared memory; use smaller tiles");
+    return FM_INVALID_ARG;
+  }
   FM_CUDA(launch_tile_fd(c->dim, model->kind, c->tile_args(), c->n_tiles, c->tile_nodes,
-                         (size_t)c->entry_cap * 2 + 16, v, b, eps, g, c->status + 1, ma, s));
+                         c->chunk_entry_cap, v, b, eps, g, c->status + 1, ma, s));
   c->launches++;
   return FM_OK;
 }

@@ -249,9 +249,14 @@ __global__ void __launch_bounds__(CT, MINB)
       __syncthreads();
       issue_clo(comp.t + gridDim.x);
     }
-    RowSrc cur_row = row_src(comp);
-    issue_records(comp, 0, cur_row);
+    // chunks 0 and 1 go out now; chunk q + 2 is issued into stage q & 1 as soon
+    // as chunk q's records have been read (two chunks of lead, not one)
+    RowSrc row_a = row_src(comp);
+    issue_records(comp, 0, row_a);
     Cursor<CT> iss = comp;
+    iss.advance(a);
+    RowSrc row_b = row_src(iss);
+    issue_records(iss, 1, row_b);
     iss.advance(a);
     RowSrc next_row = row_src(iss);
     uint32_t q = 0, j = 0;
@@ -317,12 +322,8 @@ __global__ void __launch_bounds__(CT, MINB)
       const int ne_t = comp.ne;
       for (int c0 = 0; c0 < ne_t; c0 += CT, ++q) {
         const int s = q & 1;
-        // records of the next chunk into the other stage (freed by the last barrier)
-        issue_records(iss, s ^ 1, next_row);
-        const RowSrc this_row = cur_row;
-        cur_row = next_row;
-        iss.advance(a);
-        next_row = row_src(iss);
+        const RowSrc this_row = row_a;
+        row_a = row_b;
         mbar_wait(full + s, (q >> 1) & 1);
         const int e = c0 + tid;
         const bool valid = e < ne_t;
@@ -374,6 +375,11 @@ __global__ void __launch_bounds__(CT, MINB)
             }
         }
         __syncthreads();  // contributions staged; every record of stage s read
+        // stage s is free: records of chunk q + 2
+        issue_records(iss, s, next_row);
+        row_b = next_row;
+        iss.advance(a);
+        next_row = row_src(iss);
         if (my_node && !(mdl.dbg & 2)) {
           // this node's entries of the chunk: a known count, so the loads of
           // two entries are issued together; the order (ascending tile element)

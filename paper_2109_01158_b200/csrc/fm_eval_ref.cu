@@ -65,39 +65,98 @@ __global__ void __launch_bounds__(1024) k_finalize(const double *__restrict__ jp
 }
 
 // ----------------------------------------------------------------- FD
-// gradients.py:84-121.  For each tile element and each owned slot l, each
-// component j and each sign (-eps first), row j of F is recomputed from the
-// perturbed nodal values (v_l + s*eps, gradients.py:105-106) with the einsum
-// order, the other rows are the unperturbed F (evaluate_GG, gradients.py:35-51),
-// and vol*W is staged; node threads sum the minus and plus sides separately in
-// ascending element order, then g = (S+ - S-)/(2 eps) - b (gradients.py:118-120).
+// gradients.py:84-121.  One CTA per node tile; its element list (own + halo,
+// dealt order) in chunks of CT rows, three phases per chunk:
+//  rows   thread r loads record c0 + r (halo rows take this tile's closure
+//         indices from halo_loc), gathers v from the tile's node values
+//         (closure gathered once per tile) and forms the unperturbed F
+//         (einsum order); record and F go to shared memory.
+//  items  the chunk's node entries (te << 2 | slot) flattened in node order (a
+//         block scan of the per-chunk counts in node_desc), times the D
+//         components.  Item (j, f) recomputes row j of F from the perturbed
+//         nodal values v_l -/+ eps (gradients.py:105-106, einsum order); the
+//         other rows are the unperturbed F (evaluate_GG, gradients.py:35-51);
+//         vol*W of both signs is staged.  Work per thread is even whatever the
+//         mix of own / halo elements and owned slots.
+//  nodes  node thread n sums its entries' minus and plus values separately in
+//         ascending tile-element order; g = (S+ - S-)/(2 eps) - b
+//         (gradients.py:118-120).
 // A non-finite density latches the smallest key (sign, j, free rank, element),
 // i.e. the first offending stacked row in reference order (gradients.py:77-81).
-template <int DIM, int MODEL>
-__global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__restrict__ v,
-                                                 const double *__restrict__ b, double eps,
-                                                 double *__restrict__ g,
-                                                 unsigned long long *badkey, ModelArgs mdl) {
+template <int DIM, int CT>
+struct FdLayout {
+  static constexpr int RB = RecBytes<DIM>::value;
+  __host__ __device__ static size_t r16(size_t x) { return (x + 15) / 16 * 16; }
+  __host__ __device__ static size_t nodev(int D, int cap) { return r16((size_t)D * cap * 8); }
+  __host__ __device__ static size_t recs() { return (size_t)CT * RB; }
+  __host__ __device__ static size_t fbuf(int D) { return r16((size_t)CT * D * DIM * 8); }
+  __host__ __device__ static size_t stg(int D, int ech) { return (size_t)D * ech * 16; }
+  __host__ __device__ static size_t flat(int ech) { return r16((size_t)ech * 2); }
+  __host__ __device__ static size_t total(int D, int cap, int ech) {
+    return nodev(D, cap) + recs() + fbuf(D) + stg(D, ech) + flat(ech) + 32 * 4;
+  }
+};
+
+// exclusive block scan of x (CT threads); total in every thread
+template <int CT>
+__device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
+  constexpr int NW = CT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < NW ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < NW) wsum[lane] = t;
+  }
+  __syncthreads();
+  total = wsum[NW - 1];
+  return (w ? wsum[w - 1] : 0) + incl - x;
+}
+
+template <int DIM, int MODEL, int CT>
+__global__ void __launch_bounds__(CT, 512 / CT)
+    k_tile_fd(TileArgs a, const double *__restrict__ v, const double *__restrict__ b, double eps,
+              double *__restrict__ g, unsigned long long *badkey, ModelArgs mdl, int ech) {
   constexpr int NV = DIM + 1;
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *stage = reinterpret_cast<double *>(smem_raw);  // [blockDim][NV][D][2]
-  uint16_t *ents = reinterpret_cast<uint16_t *>(stage + blockDim.x * NV * D * 2);
+  constexpr int RB = RecBytes<DIM>::value;
+  constexpr int NQ = RB / 16;
+  constexpr int NF = D * DIM;
+  constexpr int LW = 1 + DIM * NV;  // record word holding the closure indices (odd)
+  using L = FdLayout<DIM, CT>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int CAP = a.clo_cap;
+  double *nodev = reinterpret_cast<double *>(smem);
+  unsigned char *recs = smem + L::nodev(D, CAP);
+  double *Fb = reinterpret_cast<double *>(recs + L::recs());
+  double2 *stg = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(Fb) + L::fbuf(D));
+  uint16_t *flat = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stg) +
+                                                L::stg(D, ech));
+  int *wsum = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(flat) + L::flat(ech));
+  const int tid = threadIdx.x;
 
   const TileMeta tm = a.meta[blockIdx.x];
   if (tm.node_count == 0) return;  // orphan tile: no free node, nothing to differentiate
-  const bool has_node = (int)threadIdx.x < tm.node_count;
-  for (int q = threadIdx.x; q < tm.entry_count; q += blockDim.x)
-    ents[q] = a.entries[tm.entry_begin + q];
-  int cur = 0, end = 0, node = 0, outw = 0;
-  if (has_node) {
-    const int4 nd = a.node_desc[tm.node_begin + threadIdx.x];
-    cur = nd.x & ENTRY_OFF_MASK;
-    end = cur;
-    for (int ch = 0; ch < MAX_CHUNKS; ++ch) end += chunk_count(nd, ch);
-    node = nd.z;
-    outw = nd.w;
+  for (int i = tid; i < tm.clo_count; i += CT) {
+    const double *src = v + (int64_t)__ldg(a.closure + tm.clo_begin + i) * D;
+#pragma unroll
+    for (int k = 0; k < D; ++k) nodev[k * CAP + i] = __ldg(src + k);
   }
+  const bool my_node = tid < tm.node_count;
+  int4 nd = make_int4(0, 0, 0, 0);
+  if (my_node) nd = a.node_desc[tm.node_begin + tid];
+  int cur = nd.x & ENTRY_OFF_MASK;
   double accm[D], accp[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) accm[j] = accp[j] = 0.0;
@@ -105,81 +164,127 @@ __global__ void __launch_bounds__(512) k_tile_fd(TileArgs a, const double *__res
   __syncthreads();
 
   const int ne_t = tm.own_count + tm.halo_count;
-  for (int c0 = 0; c0 < ne_t; c0 += blockDim.x) {
-    const int i = c0 + threadIdx.x;
-    if (i < ne_t) {
-      const int s = i < tm.own_count ? tm.own_begin + i : a.halo_ids[tm.halo_begin + i - tm.own_count];
-      const int fl = a.flags[tm.elem_begin + i];
+  for (int c0 = 0, ch = 0; c0 < ne_t; c0 += CT, ++ch) {
+    // ---- rows: record + unperturbed F of tile element c0 + tid
+    const int e = c0 + tid;
+    if (e < ne_t) {
+      const bool halo = e >= tm.own_count;
+      const int h = tm.halo_begin + e - tm.own_count;
+      const int64_t s = halo ? (int64_t)__ldg(a.halo_ids + h) : (int64_t)tm.own_begin + e;
+      const double2 *p = reinterpret_cast<const double2 *>(a.aos + s * RB);
+      double2 q[NQ];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
+      if (halo) {
+        const uint2 hl = __ldg(a.halo_loc + h);
+        q[LW / 2].y = __longlong_as_double((long long)(((unsigned long long)hl.y << 32) | hl.x));
+      }
+      double2 *dst = reinterpret_cast<double2 *>(recs + tid * RB);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) dst[k] = q[k];
       Elem<DIM> E;
-      load_elem<DIM>(a.aos, a.conn4, s, E);
+      decode_elem<DIM>(q, E);
       double vv[D][NV];
-      gather_v<DIM, D>(v, E.c, vv);
+#pragma unroll
+      for (int l = 0; l < NV; ++l)
+#pragma unroll
+        for (int k = 0; k < D; ++k) vv[k][l] = nodev[k * CAP + E.loc[l]];
       double F[D][DIM];
       grad_F<DIM, D>(vv, E.g, F);
-      double *row = stage + (size_t)threadIdx.x * NV * D * 2;
-#pragma unroll 1
-      for (int l = 0; l < NV; ++l) {
-        if (!(fl & (1 << l))) continue;
-#pragma unroll 1
-        for (int j = 0; j < D; ++j) {
 #pragma unroll
-          for (int sg = 0; sg < 2; ++sg) {
-            double ve[NV];
+      for (int j = 0; j < D; ++j)
 #pragma unroll
-            for (int k = 0; k < NV; ++k) ve[k] = vv[j][k];
-            ve[l] = vv[j][l] + (sg ? eps : -eps);
-            double Fp[D][DIM];
+        for (int m = 0; m < DIM; ++m) Fb[tid * NF + j * DIM + m] = F[j][m];
+    }
+    // ---- this chunk's entries, flattened in node order
+    const int cnt = my_node ? chunk_count(nd, ch) : 0;
+    int total;
+    const int base = block_excl_scan<CT>(cnt, wsum, total);  // (its barriers publish rows)
+    for (int k = 0; k < cnt; ++k) flat[base + k] = __ldg(a.entries + tm.entry_begin + cur + k);
+    __syncthreads();
+    // ---- items (j, f): both signs of one perturbed row
+    const int nit = D * total;
+    for (int i = tid; i < nit; i += CT) {
+      const int j = D == 1 ? 0 : (int)(i >= total) + (int)(D == 3 && i >= 2 * total);
+      const int f = i - j * total;
+      const int en = flat[f];
+      const int r = (en >> 2) - c0, l = en & 3;
+      Elem<DIM> E;
+      load_elem_smem<DIM>(recs, r, E);
+      double F[D][DIM];
 #pragma unroll
-            for (int jj = 0; jj < D; ++jj)
+      for (int jj = 0; jj < D; ++jj)
 #pragma unroll
-              for (int m = 0; m < DIM; ++m) Fp[jj][m] = F[jj][m];
+        for (int m = 0; m < DIM; ++m) F[jj][m] = Fb[r * NF + jj * DIM + m];
+      double vj[NV];
 #pragma unroll
-            for (int m = 0; m < DIM; ++m) Fp[j][m] = einsum_row<NV>(ve, E.g[m]);
-            double W = density<DIM, MODEL>(Fp, mdl);
-            if (!isfinite(W)) {
-              const int r = a.rank_of[E.c[l]];
-              unsigned long long key = ((unsigned long long)sg << 63) |
-                                       ((unsigned long long)j << 61) |
-                                       ((unsigned long long)r << 31) |
-                                       (unsigned long long)a.s2o[s];
-              mykey = key < mykey ? key : mykey;
-            }
-            row[(l * D + j) * 2 + sg] = E.vol * W;
-          }
+      for (int k = 0; k < NV; ++k) vj[k] = nodev[j * CAP + E.loc[k]];
+      double w[2];
+#pragma unroll
+      for (int sg = 0; sg < 2; ++sg) {
+        const double st = sg ? eps : -eps;
+        double ve[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) ve[k] = k == l ? vj[k] + st : vj[k];
+        double Fp[D][DIM];
+#pragma unroll
+        for (int jj = 0; jj < D; ++jj)
+#pragma unroll
+          for (int m = 0; m < DIM; ++m)
+            Fp[jj][m] = jj == j ? einsum_row<NV>(ve, E.g[m]) : F[jj][m];
+        const double W = density<DIM, MODEL>(Fp, mdl);
+        if (!isfinite(W)) {
+          int locl = E.loc[0];  // E.loc[l] without a dynamically indexed (local) array
+#pragma unroll
+          for (int k = 1; k < NV; ++k) locl = k == l ? E.loc[k] : locl;
+          const int node = __ldg(a.closure + tm.clo_begin + locl);
+          const int te = r + c0;
+          const int64_t s = te < tm.own_count
+                                ? (int64_t)tm.own_begin + te
+                                : (int64_t)__ldg(a.halo_ids + tm.halo_begin + te - tm.own_count);
+          const unsigned long long key = ((unsigned long long)sg << 63) |
+                                         ((unsigned long long)j << 61) |
+                                         ((unsigned long long)__ldg(a.rank_of + node) << 31) |
+                                         (unsigned long long)__ldg(a.s2o + s);
+          mykey = key < mykey ? key : mykey;
         }
+        w[sg] = E.vol * W;
       }
+      stg[j * ech + f] = make_double2(w[0], w[1]);
     }
     __syncthreads();
-    if (has_node) {
-      const int base = c0, lim = base + (int)blockDim.x;
-      while (cur < end) {
-        const int en = ents[cur];
-        const int te = en >> 2;
-        if (te >= lim) break;
-        const double *src = stage + (((size_t)(te - base) * NV + (en & 3)) * D) * 2;
+    // ---- nodes: ascending tile-element order, minus and plus separately
+    if (my_node) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          accm[j] += src[2 * j];
-          accp[j] += src[2 * j + 1];
+      for (int j = 0; j < D; ++j)
+        for (int k = 0; k < cnt; ++k) {
+          const double2 x = stg[j * ech + base + k];
+          accm[j] += x.x;
+          accp[j] += x.y;
         }
-        ++cur;
-      }
     }
+    cur += cnt;
     __syncthreads();
   }
   if (mykey != ~0ull) atomicMin(badkey, mykey);
-  if (has_node) {
-    const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
-    int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+  if (my_node) {
+    const int mask = (unsigned)nd.w >> OUT_MASK_SHIFT;
+    int o = nd.w & ((1 << OUT_MASK_SHIFT) - 1);
     const double inv = 2.0 * eps;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       if (mask & (1 << j)) {
-        double q = (accp[j] - accm[j]) / inv;
-        g[o++] = b ? q - __ldg(b + node * D + j) : q;
+        const double q = (accp[j] - accm[j]) / inv;
+        g[o++] = b ? q - __ldg(b + (int64_t)nd.z * D + j) : q;
       }
     }
   }
+}
+
+size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct) {
+  if (ct == 128)
+    return dim == 3 ? FdLayout<3, 128>::total(d, clo_cap, ech) : FdLayout<2, 128>::total(d, clo_cap, ech);
+  return dim == 3 ? FdLayout<3, 256>::total(d, clo_cap, ech) : FdLayout<2, 256>::total(d, clo_cap, ech);
 }
 
 // ----------------------------------------------------------------- descent
@@ -231,33 +336,36 @@ cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, 
   return cudaGetLastError();
 }
 
-template <int DIM, int MODEL>
-static cudaError_t fd_t(const TileArgs &a, int n_tiles, int threads, size_t smem_entries,
-                        const double *v, const double *b, double eps, double *g,
-                        unsigned long long *badkey, const ModelArgs &m, cudaStream_t s) {
+template <int DIM, int MODEL, int CT>
+static cudaError_t fd_t(const TileArgs &a, int n_tiles, int ech, const double *v, const double *b,
+                        double eps, double *g, unsigned long long *badkey, const ModelArgs &m,
+                        cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  size_t smem = smem_entries + (size_t)threads * (DIM + 1) * D * 2 * sizeof(double);
-  auto k = k_tile_fd<DIM, MODEL>;
+  const size_t smem = FdLayout<DIM, CT>::total(D, a.clo_cap, ech);
+  auto k = k_tile_fd<DIM, MODEL, CT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<n_tiles, threads, smem, s>>>(a, v, b, eps, g, badkey, m);
+  k<<<n_tiles, CT, smem, s>>>(a, v, b, eps, g, badkey, m, ech);
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
-                           size_t smem_entries, const double *v, const double *b, double eps,
-                           double *g, unsigned long long *badkey, const ModelArgs &m,
-                           cudaStream_t s) {
+template <int DIM, int MODEL>
+static cudaError_t fd_ct(const TileArgs &a, int n_tiles, int ct, int ech, const double *v,
+                         const double *b, double eps, double *g, unsigned long long *badkey,
+                         const ModelArgs &m, cudaStream_t s) {
+  if (ct == 128) return fd_t<DIM, MODEL, 128>(a, n_tiles, ech, v, b, eps, g, badkey, m, s);
+  return fd_t<DIM, MODEL, 256>(a, n_tiles, ech, v, b, eps, g, badkey, m, s);
+}
+
+cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
+                           const double *v, const double *b, double eps, double *g,
+                           unsigned long long *badkey, const ModelArgs &m, cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return fd_t<2, FM_MODEL_PLAPLACE>(a, n_tiles, threads, smem_entries, v, b, eps, g, badkey, m,
-                                      s);
+    return fd_ct<2, FM_MODEL_PLAPLACE>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return fd_t<3, FM_MODEL_PLAPLACE>(a, n_tiles, threads, smem_entries, v, b, eps, g, badkey, m,
-                                      s);
+    return fd_ct<3, FM_MODEL_PLAPLACE>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
   if (dim == 2)
-    return fd_t<2, FM_MODEL_NEOHOOKEAN>(a, n_tiles, threads, smem_entries, v, b, eps, g, badkey,
-                                        m, s);
-  return fd_t<3, FM_MODEL_NEOHOOKEAN>(a, n_tiles, threads, smem_entries, v, b, eps, g, badkey, m,
-                                      s);
+    return fd_ct<2, FM_MODEL_NEOHOOKEAN>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
+  return fd_ct<3, FM_MODEL_NEOHOOKEAN>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
 }
 
 cudaError_t launch_descent(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,

@@ -17,10 +17,11 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
                               cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns);
 
-cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int threads,
-                           size_t smem_entries, const double *v, const double *b, double eps,
-                           double *g, unsigned long long *badkey, const ModelArgs &m,
-                           cudaStream_t s);
+cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
+                           const double *v, const double *b, double eps, double *g,
+                           unsigned long long *badkey, const ModelArgs &m, cudaStream_t s);
+// shared memory of the FD tile kernel (ech = max node entries of one chunk)
+size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct);
 
 cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, int nblocks,
                           const double *v, double *part, double *dens, const ModelArgs &m,
