@@ -3,8 +3,9 @@
     python -m paper_2109_01158_b200.build        (or __graft_entry__.build())
 
 Plain nvcc, one object per translation unit, relinked only when a source or
-header changed.  The FD / energy unit is compiled with ``-fmad=false`` so its
-element arithmetic follows the reference's rounding order.
+header changed.  Element arithmetic that must follow the reference's rounding
+order uses explicit round-to-nearest intrinsics (fm_density.cuh), so every
+unit compiles with FMA contraction on.
 """
 
 from __future__ import annotations
@@ -27,7 +28,7 @@ UNITS = {
     "fm_prep.cu": [],
     "fm_ctx.cu": [],
     "fm_eval_exact.cu": [],
-    "fm_eval_ref.cu": ["-fmad=false"],
+    "fm_eval_ref.cu": [],
 }
 
 

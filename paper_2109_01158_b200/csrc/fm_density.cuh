@@ -6,23 +6,30 @@
 //   NH W         models.py:89-100   C1 (I1 - dim - 2 log det) + D1 (det-1)^2, +inf if det<=0
 //   NH dW/dF     models.py:103-120  C1 (2F - (2/det) cof) + 2 D1 (det-1) cof
 //   p-Laplace    models.py:123-138  |g|^p/p, |g|^(p-2) g (0 at g = 0 when p < 2)
-// Translation units compiled with -fmad=false reproduce the per-element
-// reference values bit-for-bit except for libm ulps in log/pow; the fused
-// exact-gradient unit allows FMA contraction.
+// Every multiply / add here is an explicit round-to-nearest intrinsic, which
+// the compiler never contracts into an FMA: the per-element values reproduce
+// the reference bit-for-bit (up to libm ulps in log/pow) in any translation
+// unit, while log/pow themselves keep their FMA-based implementations
+// (SURVEY §7.2 H3).  The fused exact-gradient kernel uses its own FMA forms.
 #pragma once
 
 #include "fm_ctx.cuh"
 
 namespace fm {
 
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+
 template <int NV>
 __device__ __forceinline__ double einsum_row(const double (&a)[NV], const double (&b)[NV]) {
   if constexpr (NV == 4) {
-    double p0 = a[0] * b[0], p1 = a[1] * b[1], p2 = a[2] * b[2], p3 = a[3] * b[3];
-    return (p0 + p2) + (p1 + p3);
+    double p0 = rmul(a[0], b[0]), p1 = rmul(a[1], b[1]), p2 = rmul(a[2], b[2]),
+           p3 = rmul(a[3], b[3]);
+    return radd(radd(p0, p2), radd(p1, p3));
   } else {
-    double p0 = a[0] * b[0], p1 = a[1] * b[1], p2 = a[2] * b[2];
-    return (p0 + p2) + p1;
+    double p0 = rmul(a[0], b[0]), p1 = rmul(a[1], b[1]), p2 = rmul(a[2], b[2]);
+    return radd(radd(p0, p2), p1);
   }
 }
 
@@ -38,15 +45,15 @@ __device__ __forceinline__ void grad_F(const double (&vv)[D][DIM + 1],
 template <int DIM>
 __device__ __forceinline__ double det_F(const double (&F)[DIM][DIM]) {
   if constexpr (DIM == 2) {
-    return F[0][0] * F[1][1] - F[0][1] * F[1][0];
+    return rsub(rmul(F[0][0], F[1][1]), rmul(F[0][1], F[1][0]));
   } else {
-    double a = F[0][0] * F[1][1] * F[2][2];
-    double b = F[0][2] * F[1][0] * F[2][1];
-    double c = F[0][1] * F[1][2] * F[2][0];
-    double d = F[0][2] * F[1][1] * F[2][0];
-    double e = F[0][1] * F[1][0] * F[2][2];
-    double f = F[0][0] * F[1][2] * F[2][1];
-    return ((((a + b) + c) - d) - e) - f;
+    double a = rmul(rmul(F[0][0], F[1][1]), F[2][2]);
+    double b = rmul(rmul(F[0][2], F[1][0]), F[2][1]);
+    double c = rmul(rmul(F[0][1], F[1][2]), F[2][0]);
+    double d = rmul(rmul(F[0][2], F[1][1]), F[2][0]);
+    double e = rmul(rmul(F[0][1], F[1][0]), F[2][2]);
+    double f = rmul(rmul(F[0][0], F[1][2]), F[2][1]);
+    return rsub(rsub(rsub(radd(radd(a, b), c), d), e), f);
   }
 }
 
@@ -64,7 +71,7 @@ __device__ __forceinline__ void cof_F(const double (&F)[DIM][DIM], double (&C)[D
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int m1 = m == 0 ? 1 : 0, m2 = m == 2 ? 1 : 2;
-        double minor = F[j1][m1] * F[j2][m2] - F[j1][m2] * F[j2][m1];
+        double minor = rsub(rmul(F[j1][m1], F[j2][m2]), rmul(F[j1][m2], F[j2][m1]));
         C[j][m] = ((j + m) & 1) ? -minor : minor;
       }
     }
@@ -77,20 +84,21 @@ __device__ __forceinline__ double density(const double (&F)[MODEL == FM_MODEL_NE
                                           const ModelArgs &m) {
   if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
     double det = det_F<DIM>(F);
-    double I1 = F[0][0] * F[0][0];
+    double I1 = rmul(F[0][0], F[0][0]);
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
 #pragma unroll
       for (int k = 0; k < DIM; ++k)
-        if (j + k > 0) I1 = I1 + F[j][k] * F[j][k];
+        if (j + k > 0) I1 = radd(I1, rmul(F[j][k], F[j][k]));
     if (!(det > 0.0)) return INFINITY;
     double ld = log(det);
-    double dm1 = det - 1.0;
-    return m.C1 * ((I1 - (double)DIM) - 2.0 * ld) + m.D1 * (dm1 * dm1);
+    double dm1 = rsub(det, 1.0);
+    return radd(rmul(m.C1, rsub(rsub(I1, (double)DIM), rmul(2.0, ld))),
+                rmul(m.D1, rmul(dm1, dm1)));
   } else {
-    double n2 = F[0][0] * F[0][0];
+    double n2 = rmul(F[0][0], F[0][0]);
 #pragma unroll
-    for (int k = 1; k < DIM; ++k) n2 = n2 + F[0][k] * F[0][k];
+    for (int k = 1; k < DIM; ++k) n2 = radd(n2, rmul(F[0][k], F[0][k]));
     return np_scalar_pow(n2, m.e_w) / m.p;
   }
 }
@@ -106,25 +114,26 @@ __device__ __forceinline__ void ddensity(const double (&F)[MODEL == FM_MODEL_NEO
     bad = !(det > 0.0);
     double C[DIM][DIM];
     cof_F<DIM>(F, C);
-    double dfac = 2.0 * m.D1 * (det - 1.0);
+    double dfac = rmul(rmul(2.0, m.D1), rsub(det, 1.0));
     double inv2 = 2.0 / det;
 #pragma unroll
     for (int j = 0; j < DIM; ++j)
 #pragma unroll
       for (int k = 0; k < DIM; ++k)
-        P[j][k] = m.C1 * (2.0 * F[j][k] - inv2 * C[j][k]) + dfac * C[j][k];
+        P[j][k] = radd(rmul(m.C1, rsub(rmul(2.0, F[j][k]), rmul(inv2, C[j][k]))),
+                       rmul(dfac, C[j][k]));
   } else {
     bad = false;
-    double n2 = F[0][0] * F[0][0];
+    double n2 = rmul(F[0][0], F[0][0]);
 #pragma unroll
-    for (int k = 1; k < DIM; ++k) n2 = n2 + F[0][k] * F[0][k];
+    for (int k = 1; k < DIM; ++k) n2 = radd(n2, rmul(F[0][k], F[0][k]));
     double fac;
     if (m.p >= 2.0)
       fac = np_scalar_pow(n2, m.e_dw);
     else
       fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) P[0][k] = fac * F[0][k];
+    for (int k = 0; k < DIM; ++k) P[0][k] = rmul(fac, F[0][k]);
   }
 }
 

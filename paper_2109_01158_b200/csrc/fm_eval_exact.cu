@@ -48,6 +48,29 @@ struct PipeLayout {
   }
 };
 
+// cofactors with one rounding per minor (fused; this kernel is not bound to
+// the reference's operation order)
+template <int DIM>
+__device__ __forceinline__ void cof_F_fma(const double (&F)[DIM][DIM], double (&C)[DIM][DIM]) {
+  if constexpr (DIM == 2) {
+    C[0][0] = F[1][1];
+    C[0][1] = -F[1][0];
+    C[1][0] = -F[0][1];
+    C[1][1] = F[0][0];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int j1 = j == 0 ? 1 : 0, j2 = j == 2 ? 1 : 2;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int m1 = m == 0 ? 1 : 0, m2 = m == 2 ? 1 : 2;
+        const double minor = fma(F[j1][m1], F[j2][m2], -(F[j1][m2] * F[j2][m1]));
+        C[j][m] = ((j + m) & 1) ? -minor : minor;
+      }
+    }
+  }
+}
+
 // NH: P' = vol * dW/dF = a F + b cof with a = 2 C1 vol, b = vol (2 D1 (det-1) - 2 C1/det)
 // (models.py:103-120 regrouped).  p-Laplace: P' = vol |g|^(p-2) g.
 template <int DIM, int MODEL>
@@ -57,7 +80,7 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
                                           double &W, bool &bad) {
   if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
     double C[DIM][DIM];
-    cof_F<DIM>(F, C);
+    cof_F_fma<DIM>(F, C);
     double det = 0.0;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) det = fma(F[0][k], C[0][k], det);

@@ -1,7 +1,7 @@
 // Energy-only streaming kernel and the nodal-patch finite-difference kernel.
-// Compiled with -fmad=false so that F, det, I1, W follow the reference's
-// rounding order exactly (assembly.py:35-49, models.py:59-126); only the
-// libm ulps of log/pow differ from numpy.
+// F, det, I1, W follow the reference's rounding order exactly through the
+// explicit round-to-nearest forms of fm_density.cuh (assembly.py:35-49,
+// models.py:59-126); only the libm ulps of log/pow differ from numpy.
 #include "fm_density.cuh"
 #include "fm_kernels.h"
 
@@ -202,55 +202,84 @@ __global__ void __launch_bounds__(CT, 512 / CT)
     const int base = block_excl_scan<CT>(cnt, wsum, total);  // (its barriers publish rows)
     for (int k = 0; k < cnt; ++k) flat[base + k] = __ldg(a.entries + tm.entry_begin + cur + k);
     __syncthreads();
-    // ---- items (j, f): both signs of one perturbed row
-    const int nit = D * total;
-    for (int i = tid; i < nit; i += CT) {
-      const int j = D == 1 ? 0 : (int)(i >= total) + (int)(D == 3 && i >= 2 * total);
-      const int f = i - j * total;
-      const int en = flat[f];
-      const int r = (en >> 2) - c0, l = en & 3;
-      Elem<DIM> E;
-      load_elem_smem<DIM>(recs, r, E);
-      double F[D][DIM];
+    // ---- items (j, f): both signs of one perturbed row.  j is a compile-time
+    // constant of each pass (no selects between rows); the entry's slot l is
+    // not, so the record words of slot l are addressed directly.  Row j of F
+    // keeps the einsum order (p0+p2)+(p1+p3) [NV = 3: (p0+p2)+p1]: the pair
+    // holding p_l is (p_l + partner), the other pair is unperturbed, and IEEE
+    // addition is commutative, so only p_l depends on the sign.
 #pragma unroll
-      for (int jj = 0; jj < D; ++jj)
-#pragma unroll
-        for (int m = 0; m < DIM; ++m) F[jj][m] = Fb[r * NF + jj * DIM + m];
-      double vj[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) vj[k] = nodev[j * CAP + E.loc[k]];
-      double w[2];
-#pragma unroll
-      for (int sg = 0; sg < 2; ++sg) {
-        const double st = sg ? eps : -eps;
-        double ve[NV];
-#pragma unroll
-        for (int k = 0; k < NV; ++k) ve[k] = k == l ? vj[k] + st : vj[k];
-        double Fp[D][DIM];
+    for (int j = 0; j < D; ++j) {
+      for (int f = tid; f < total; f += CT) {
+        const int en = flat[f];
+        const int r = (en >> 2) - c0, l = en & 3;
+        const unsigned char *rec = recs + r * RB;
+        const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
+        const unsigned long long lw = *reinterpret_cast<const unsigned long long *>(rec + LW * 8);
+        auto vat = [&](int k) { return nodev[j * CAP + (int)((lw >> (16 * k)) & 0xffffull)]; };
+        auto gat = [&](int m, int k) { return rd[1 + m * NV + k]; };
+        double F[D][DIM];
 #pragma unroll
         for (int jj = 0; jj < D; ++jj)
 #pragma unroll
-          for (int m = 0; m < DIM; ++m)
-            Fp[jj][m] = jj == j ? einsum_row<NV>(ve, E.g[m]) : F[jj][m];
-        const double W = density<DIM, MODEL>(Fp, mdl);
-        if (!isfinite(W)) {
-          int locl = E.loc[0];  // E.loc[l] without a dynamically indexed (local) array
+          for (int m = 0; m < DIM; ++m) F[jj][m] = jj == j ? 0.0 : Fb[r * NF + jj * DIM + m];
+        const double vl = vat(l);
+        double gl[DIM], q1[DIM], q2[DIM];
+        if constexpr (NV == 4) {
+          const int lp = l ^ 2, la = (l + 1) & 3, lb = (l + 3) & 3;
+          const double vp = vat(lp), va = vat(la), vb = vat(lb);
 #pragma unroll
-          for (int k = 1; k < NV; ++k) locl = k == l ? E.loc[k] : locl;
-          const int node = __ldg(a.closure + tm.clo_begin + locl);
-          const int te = r + c0;
-          const int64_t s = te < tm.own_count
-                                ? (int64_t)tm.own_begin + te
-                                : (int64_t)__ldg(a.halo_ids + tm.halo_begin + te - tm.own_count);
-          const unsigned long long key = ((unsigned long long)sg << 63) |
-                                         ((unsigned long long)j << 61) |
-                                         ((unsigned long long)__ldg(a.rank_of + node) << 31) |
-                                         (unsigned long long)__ldg(a.s2o + s);
-          mykey = key < mykey ? key : mykey;
+          for (int m = 0; m < DIM; ++m) {
+            gl[m] = gat(m, l);
+            q1[m] = rmul(vp, gat(m, lp));                               // partner of p_l
+            q2[m] = radd(rmul(va, gat(m, la)), rmul(vb, gat(m, lb)));  // the other pair
+          }
+        } else {
+          const int lp = l == 1 ? 0 : 2 - l, lo = l == 1 ? 2 : 1;
+          const double vp = vat(lp), vo = vat(lo);
+#pragma unroll
+          for (int m = 0; m < DIM; ++m) {
+            gl[m] = gat(m, l);
+            q1[m] = rmul(vp, gat(m, lp));
+            q2[m] = rmul(vo, gat(m, lo));
+          }
         }
-        w[sg] = E.vol * W;
+        double w[2];
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+          const double ve = radd(vl, sg ? eps : -eps);
+          double Fp[D][DIM];
+#pragma unroll
+          for (int jj = 0; jj < D; ++jj)
+#pragma unroll
+            for (int m = 0; m < DIM; ++m) Fp[jj][m] = F[jj][m];
+#pragma unroll
+          for (int m = 0; m < DIM; ++m) {
+            const double pl = rmul(ve, gl[m]);
+            if constexpr (NV == 4) {
+              Fp[j][m] = radd(radd(pl, q1[m]), q2[m]);
+            } else {  // (p0+p2)+p1: l = 1 is the lone term
+              Fp[j][m] = l == 1 ? radd(radd(q1[m], q2[m]), pl) : radd(radd(pl, q1[m]), q2[m]);
+            }
+          }
+          const double W = density<DIM, MODEL>(Fp, mdl);
+          if (!isfinite(W)) {
+            const int node =
+                __ldg(a.closure + tm.clo_begin + (int)((lw >> (16 * l)) & 0xffffull));
+            const int te = r + c0;
+            const int64_t s = te < tm.own_count
+                                  ? (int64_t)tm.own_begin + te
+                                  : (int64_t)__ldg(a.halo_ids + tm.halo_begin + te - tm.own_count);
+            const unsigned long long key = ((unsigned long long)sg << 63) |
+                                           ((unsigned long long)j << 61) |
+                                           ((unsigned long long)__ldg(a.rank_of + node) << 31) |
+                                           (unsigned long long)__ldg(a.s2o + s);
+            mykey = key < mykey ? key : mykey;
+          }
+          w[sg] = rmul(rd[0], W);
+        }
+        stg[j * ech + f] = make_double2(w[0], w[1]);
       }
-      stg[j * ech + f] = make_double2(w[0], w[1]);
     }
     __syncthreads();
     // ---- nodes: ascending tile-element order, minus and plus separately
@@ -297,7 +326,7 @@ __global__ void k_descent(int64_t nfree, int d, const int32_t *free_node, const 
     int o = free_out[r];
     for (int j = 0; j < d; ++j)
       if (mask & (1 << j)) {
-        v[node * d + j] = v[node * d + j] - alpha * g[o];
+        v[node * d + j] = rsub(v[node * d + j], rmul(alpha, g[o]));
         ++o;
       }
   }
