@@ -124,6 +124,10 @@ __device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
   return (w ? wsum[w - 1] : 0) + incl - x;
 }
 
+#ifndef FM_FD_PREFETCH
+#define FM_FD_PREFETCH 1
+#endif
+
 template <int DIM, int MODEL, int CT>
 __global__ void __launch_bounds__(CT, 512 / CT)
     k_tile_fd(TileArgs a, const double *__restrict__ v, const double *__restrict__ b, double eps,
@@ -164,13 +168,20 @@ __global__ void __launch_bounds__(CT, 512 / CT)
   __syncthreads();
 
   const int ne_t = tm.own_count + tm.halo_count;
+  // storage id of this thread's row of the next chunk, loaded one chunk ahead
+  auto row_src = [&](int e) -> int64_t {
+    if (e >= ne_t) return -1;
+    return e >= tm.own_count ? (int64_t)__ldg(a.halo_ids + tm.halo_begin + e - tm.own_count)
+                             : (int64_t)tm.own_begin + e;
+  };
+  int64_t s_next = row_src(tid);
   for (int c0 = 0, ch = 0; c0 < ne_t; c0 += CT, ++ch) {
     // ---- rows: record + unperturbed F of tile element c0 + tid
     const int e = c0 + tid;
+    const int64_t s = s_next;
     if (e < ne_t) {
       const bool halo = e >= tm.own_count;
       const int h = tm.halo_begin + e - tm.own_count;
-      const int64_t s = halo ? (int64_t)__ldg(a.halo_ids + h) : (int64_t)tm.own_begin + e;
       const double2 *p = reinterpret_cast<const double2 *>(a.aos + s * RB);
       double2 q[NQ];
 #pragma unroll
@@ -196,6 +207,13 @@ __global__ void __launch_bounds__(CT, 512 / CT)
 #pragma unroll
         for (int m = 0; m < DIM; ++m) Fb[tid * NF + j * DIM + m] = F[j][m];
     }
+    // next chunk: its storage ids now, its own records towards L2
+    s_next = row_src(e + CT);
+    if (FM_FD_PREFETCH && s_next >= 0 && e + CT < tm.own_count) {
+      const uint8_t *pn = a.aos + s_next * RB;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + RB - 1));
+    }
     // ---- this chunk's entries, flattened in node order
     const int cnt = my_node ? chunk_count(nd, ch) : 0;
     int total;
@@ -210,7 +228,9 @@ __global__ void __launch_bounds__(CT, 512 / CT)
     // addition is commutative, so only p_l depends on the sign.
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      for (int f = tid; f < total; f += CT) {
+      // thread tid takes the items i = j * total + f with i = tid (mod CT): the
+      // passes' remainders land on different threads
+      for (int f = (tid - j * total) & (CT - 1); f < total; f += CT) {
         const int en = flat[f];
         const int r = (en >> 2) - c0, l = en & 3;
         const unsigned char *rec = recs + r * RB;
