@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfemmin_b200.so")
+# FM_LIB_OVERRIDE: profiling builds of the same library (tools/trace_exact.py)
+LIB_PATH = os.environ.get("FM_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "libfemmin_b200.so")
 
 FM_OK, FM_INADMISSIBLE, FM_INVALID_ARG, FM_CUDA_ERROR, FM_DEGENERATE, FM_PATCH_STRUCTURE = range(6)
 FM_MODEL_PLAPLACE, FM_MODEL_NEOHOOKEAN = 0, 1

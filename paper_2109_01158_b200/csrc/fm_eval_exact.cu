@@ -28,6 +28,30 @@
 #include "fm_kernels.h"
 #include "fm_pipe.cuh"
 
+// Phase timeline for profiling builds only (tools/trace_exact.py compiles this
+// unit with -DFM_TRACE=1 into a separate library): clock64 stamps of warp
+// leaders of CTAs 0..3 per chunk.
+#ifndef FM_TRACE
+#define FM_TRACE 0
+#endif
+#if FM_TRACE
+constexpr int TR_CTAS = 4, TR_WARPS = 8, TR_CHUNKS = 160, TR_STAMPS = 8;
+__device__ long long g_trace[TR_CTAS * TR_WARPS * TR_CHUNKS * TR_STAMPS];
+#define TRACE(k)                                                                        \
+  do {                                                                                  \
+    if (blockIdx.x < TR_CTAS && (threadIdx.x & 31) == 0 && q < TR_CHUNKS)               \
+      g_trace[((blockIdx.x * TR_WARPS + (threadIdx.x >> 5)) * TR_CHUNKS + q) * TR_STAMPS + \
+              (k)] = clock64();                                                         \
+  } while (0)
+extern "C" int fm_trace_copy(long long *out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_trace, (size_t)n * sizeof(long long));
+}
+#else
+#define TRACE(k) \
+  do {           \
+  } while (0)
+#endif
+
 namespace fm {
 
 __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; }
@@ -214,7 +238,7 @@ __global__ void __launch_bounds__(CT, MINB)
   };
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
     double *dst = nodev(k);
-    for (int i = tid; i < clo_count; i += CT) {
+    for (int i = tid; i < clo_count && !(mdl.dbg & 32); i += CT) {  // 32: probe without gathers
       const double *src = v + (int64_t)cids[i] * D;
 #pragma unroll
       for (int kk = 0; kk < D; ++kk)
@@ -250,7 +274,7 @@ __global__ void __launch_bounds__(CT, MINB)
         bulk_g2s(stg(s), a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)n_own * RB,
                  full + s);
     }
-    if (tid >= n_own && tid < cnt) {
+    if (tid >= n_own && tid < cnt && !(mdl.dbg & 16)) {  // 16: probe without halo rows
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
         cp_async16(stg(s) + tid * RB + c * 16, a.aos + (int64_t)rs.src * RB + c * 16);
@@ -286,6 +310,7 @@ __global__ void __launch_bounds__(CT, MINB)
 
     while (comp.valid(a)) {
       const TileMeta tm = comp.tm;
+      TRACE(6);
       // ---- tile start: descriptors + entries (single buffer: previous tile done)
       if (tid == 0) {
         const uint32_t nb = (uint32_t)tm.node_count * 16;
@@ -326,6 +351,7 @@ __global__ void __launch_bounds__(CT, MINB)
         nv = nodev(0);
       }
       mbar_wait(tfull, j & 1);
+      TRACE(7);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
       int cur = 0, outw = 0;
@@ -347,9 +373,11 @@ __global__ void __launch_bounds__(CT, MINB)
         const int s = q & 1;
         const RowSrc this_row = row_a;
         row_a = row_b;
+        TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
+        TRACE(1);
         const int e = c0 + tid;
-        const bool valid = e < ne_t;
+        const bool valid = e < ne_t && !(mdl.dbg & 8);  // 8: data-movement-only probe
         double P[D][DIM];
         Elem<DIM> E;
         if (valid) {
@@ -397,7 +425,9 @@ __global__ void __launch_bounds__(CT, MINB)
               stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
             }
         }
+        TRACE(2);
         __syncthreads();  // contributions staged; every record of stage s read
+        TRACE(3);
         // stage s is free: records of chunk q + 2
         issue_records(iss, s, next_row);
         row_b = next_row;
@@ -433,7 +463,9 @@ __global__ void __launch_bounds__(CT, MINB)
         // one staging buffer: it must be consumed before the next chunk writes
         // it; two: the next chunk's barrier already orders this consumption
         // before the write two chunks ahead
+        TRACE(4);
         if (NS == 1) __syncthreads();
+        TRACE(5);
         comp.advance(a);
       }
       if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
