@@ -279,6 +279,76 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
   }
 }
 
+// storage index -> owner tile (own ranges are contiguous per tile)
+__global__ void k_storage_tile(int n_tiles, const int32_t *own_ptr, int32_t *stile) {
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x)
+    for (int s = own_ptr[t] + threadIdx.x; s < own_ptr[t + 1]; s += blockDim.x) stile[s] = t;
+}
+
+// per tile node: its cross entries (element owned by another tile) are the tail
+// of its sorted entry list, te >= own_count of its tile
+__global__ void k_cross_count(int64_t ntn, const int32_t *tile_node_rank,
+                              const int32_t *tile_of_rank, const TileMeta *meta, const int4 *desc,
+                              const uint16_t *entries, const int32_t *entry_abs, int32_t *xbase,
+                              int32_t *xn) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int t = tile_of_rank[tile_node_rank[k]];
+    const int own = meta[t].own_count;
+    const int4 nd = desc[k];
+    int len = 0;
+    for (int ch = 0; ch < MAX_CHUNKS; ++ch) len += chunk_count(nd, ch);
+    const uint16_t *en = entries + entry_abs[k];
+    int p = 0;
+    while (p < len && (en[p] >> 2) < own) ++p;
+    xbase[k] = entry_abs[k] + p;
+    xn[k] = len - p;
+  }
+}
+
+// the cross items: (owner tile, owner te, slot) -> entry index
+__global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
+                              const int32_t *tile_of_rank, const TileMeta *meta,
+                              const uint16_t *entries, const int32_t *xbase, const int32_t *xn,
+                              const int32_t *xoff, const int32_t *halo_ids, const int32_t *stile,
+                              uint64_t *keys, int32_t *vals) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int n = xn[k];
+    if (!n) continue;
+    const TileMeta tm = meta[tile_of_rank[tile_node_rank[k]]];
+    for (int p = 0; p < n; ++p) {
+      const int en = entries[xbase[k] + p];
+      const int st = halo_ids[tm.halo_begin + (en >> 2) - tm.own_count];
+      const int to = stile[st];
+      const int te = st - meta[to].own_begin;
+      keys[xoff[k] + p] = ((uint64_t)to << 16) | (uint64_t)((te << 2) | (en & 3));
+      vals[xoff[k] + p] = xbase[k] + p;
+    }
+  }
+}
+
+// first item of every chunk of every tile
+__global__ void k_xchunk(int n_tiles, int ct, int64_t X, const uint64_t *keys, int32_t *xchunk) {
+  const int n = n_tiles * (MAX_CHUNKS + 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t t = i / (MAX_CHUNKS + 1), ch = i % (MAX_CHUNKS + 1);
+    const uint64_t key = (t << 16) | ((ch * ct) << 2);
+    int64_t lo = 0, hi = X;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    xchunk[i] = (int32_t)lo;
+  }
+}
+
+__global__ void k_low16(int64_t n, const uint64_t *k, uint16_t *o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = (uint16_t)(k[i] & 0xffffull);
+}
+
 // max over (tile, chunk) of the node entries falling in that chunk
 __global__ void k_chunk_entry_max(int n_tiles, const TileMeta *meta, const int4 *desc,
                                   unsigned int *out) {
@@ -1033,6 +1103,66 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaMemcpyAsync(&h_cmax, cmax.p, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->chunk_entry_cap = ((int)h_cmax + 7) / 8 * 8;
+
+    // 5b. cross-tile exchange of the fused exact kernel ---------------------------
+    Scratch stile, xcnt, xoff, xk, xk2, xv, xv2, xsum;
+    CK(stile.alloc(ne * 4, s));
+    CK(cudaMemsetAsync(stile.p, 0, ne * 4, s));
+    k_storage_tile<<<std::min(n_tiles, 65535), 256, 0, s>>>(n_tiles, own_ptr.as<int32_t>(),
+                                                             stile.as<int32_t>());
+    CK(cudaGetLastError());
+    CK(dmalloc(&c->node_xbase, nfree, &B));
+    CK(dmalloc(&c->node_xn, nfree, &B));
+    k_cross_count<<<grid_for(nfree, 256), 256, 0, s>>>(
+        nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), c->meta, c->node_desc, c->node_entries,
+        eabs.as<int32_t>(), c->node_xbase, c->node_xn);
+    CK(cudaGetLastError());
+    CK(xoff.alloc((nfree + 1) * 4, s));
+    CK(xsum.alloc(8, s));
+    {
+      const int32_t *in = c->node_xn;
+      int32_t *outp = xoff.as<int32_t>();
+      CK(cub_call([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, in, outp, nfree, s);
+      }, s));
+      int32_t *tot = xsum.as<int32_t>();
+      CK(cub_call([&](void *t, size_t &b) { return cub::DeviceReduce::Sum(t, b, in, tot, nfree, s); },
+                  s));
+    }
+    int32_t hX = 0;
+    CK(cudaMemcpyAsync(&hX, xsum.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int64_t X = hX;
+    c->n_cross = X;
+    CK(xk.alloc(std::max<int64_t>(X, 1) * 8, s));
+    CK(xk2.alloc(std::max<int64_t>(X, 1) * 8, s));
+    CK(xv.alloc(std::max<int64_t>(X, 1) * 4, s));
+    CK(xv2.alloc(std::max<int64_t>(X, 1) * 4, s));
+    k_cross_items<<<grid_for(nfree, 256), 256, 0, s>>>(
+        nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), c->meta, c->node_entries, c->node_xbase,
+        c->node_xn, xoff.as<int32_t>(), c->halo_ids, stile.as<int32_t>(), xk.as<uint64_t>(),
+        xv.as<int32_t>());
+    CK(cudaGetLastError());
+    cub::DoubleBuffer<uint64_t> dk(xk.as<uint64_t>(), xk2.as<uint64_t>());
+    cub::DoubleBuffer<int32_t> dv(xv.as<int32_t>(), xv2.as<int32_t>());
+    if (X) {
+      const int end_bit = 16 + bits_for((uint64_t)n_tiles);
+      CK(cub_call([&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, X, 0, end_bit, s);
+      }, s));
+    }
+    CK(dmalloc(&c->xkey, X + 8, &B));
+    CK(dmalloc(&c->xpos, X + 8, &B));
+    CK(dmalloc(&c->xchunk, (size_t)n_tiles * (MAX_CHUNKS + 1), &B));
+    CK(dmalloc(&c->xbuf, (size_t)(entry_total + 8) * d, &B));
+    if (X) {
+      k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
+      CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    k_xchunk<<<grid_for((int64_t)n_tiles * (MAX_CHUNKS + 1), 256), 256, 0, s>>>(
+        n_tiles, c->tile_nodes, X, dk.Current(), c->xchunk);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
   }
 
   // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads; shared memory
@@ -1108,7 +1238,8 @@ int fm_ctx_destroy(fm_ctx *c) {
   void *ptrs[] = {c->aos,       c->conn4,     c->meta,      c->halo_ids,  c->halo_loc,
                   c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
-                  c->dotpart,   c->status};
+                  c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
+                  c->node_xbase, c->node_xn,  c->xbuf};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1161,6 +1292,11 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     TimedLaunch tl(c, s);
     FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
                               c->stage_bufs, wj, v, b, g, c->jpart, c->status, ma, s));
+    c->launches++;
+  }
+  if (c->n_cross > 0) {
+    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_desc, c->node_xbase, c->node_xn, c->xbuf,
+                                g, s));
     c->launches++;
   }
   if (wj) {

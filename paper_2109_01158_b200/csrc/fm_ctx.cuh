@@ -178,6 +178,14 @@ struct TileArgs {
                                //  out | mask << 28} (see chunk_count)
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
   const int32_t *rank_of;      // node -> free rank or -1
+  // cross-tile exchange of the fused exact kernel (elements computed once, by
+  // their owner tile): items (owner te << 2 | slot) -> global entry index,
+  // sorted by (owner tile, te); xchunk[t * (MAX_CHUNKS + 1) + c] = first item of
+  // chunk c of tile t; xbuf[entry * D + k] receives the contributions
+  const uint16_t *xkey;
+  const int32_t *xpos;
+  const int32_t *xchunk;
+  double *xbuf;
   int n_tiles;                 // node tiles
   int n_tiles_all;             // + orphan tiles (J only)
   int entry_cap;               // max entries of one tile, rounded up to 8
@@ -223,6 +231,11 @@ struct fm_ctx {
   int32_t *free_node = nullptr, *free_out = nullptr, *rank_of = nullptr;
   int32_t *storage_to_orig = nullptr;
   uint8_t *free_mask = nullptr;
+  uint16_t *xkey = nullptr;                        // cross-tile exchange (see TileArgs)
+  int32_t *xpos = nullptr, *xchunk = nullptr;
+  int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
+  double *xbuf = nullptr;
+  int64_t n_cross = 0;
   // scratch
   double *jpart = nullptr;        // per CTA (fused) / per block (energy)
   double *dotpart = nullptr;      // b.v partials
@@ -234,8 +247,9 @@ struct fm_ctx {
   fm_ctx_stats stats{};
 
   fm::TileArgs tile_args() const {
-    return fm::TileArgs{aos,     conn4,     storage_to_orig, meta,        halo_ids,
-                        halo_loc, closure,  flags,           node_desc,   node_entries,
-                        rank_of, n_tiles,   n_tiles_all,     entry_cap,   clo_cap};
+    return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
+                        closure, flags,   node_desc,       node_entries, rank_of,  xkey,
+                        xpos,    xchunk,  xbuf,            n_tiles,   n_tiles_all, entry_cap,
+                        clo_cap};
   }
 };

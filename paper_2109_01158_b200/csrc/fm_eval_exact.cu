@@ -165,27 +165,21 @@ struct Cursor {
   __device__ void load(const TileArgs &a) {
     if (t < a.n_tiles_all) {
       tm = a.meta[t];
-      ne = tm.own_count + tm.halo_count;
+      ne = tm.own_count;  // every element is computed once, by its owner tile
     } else {
       ne = 0;
     }
   }
   __device__ bool valid(const TileArgs &a) const { return t < a.n_tiles_all; }
+  // next chunk of the stream; tiles without own elements have no chunks
   __device__ void advance(const TileArgs &a) {
     c0 += CT;
-    if (c0 >= ne) {
+    while (c0 >= ne && t < a.n_tiles_all) {
       c0 = 0;
       t += gridDim.x;
       load(a);
     }
   }
-};
-
-// this thread's row of a chunk: record id, and for halo rows the closure indices
-struct RowSrc {
-  int src;
-  int halo;  // 1: loc below replaces the record's owner-tile loc
-  uint2 loc;
 };
 
 template <int DIM, int MODEL, bool WJ, int CT, int NB, int NS, int MINB>
@@ -218,8 +212,8 @@ __global__ void __launch_bounds__(CT, MINB)
   uint64_t *tfull = cfull + 1;                              // descriptors + entries
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(full, CT + 1);
-    mbar_init(full + 1, CT + 1);
+    mbar_init(full, 1);
+    mbar_init(full + 1, 1);
     mbar_init(nfull, CT);
     mbar_init(nfull + 1, CT);
     mbar_init(cfull, 1);
@@ -249,37 +243,12 @@ __global__ void __launch_bounds__(CT, MINB)
     }
     cp_async_arrive_noinc(nfull + k);
   };
-  auto row_src = [&](const Cursor<CT> &x) -> RowSrc {
-    RowSrc r{0, 0, make_uint2(0, 0)};
-    const int e = x.c0 + tid;
-    if (x.valid(a) && e < x.ne) {
-      if (e < x.tm.own_count) {
-        r.src = x.tm.own_begin + e;
-      } else {
-        const int h = x.tm.halo_begin + e - x.tm.own_count;
-        r.src = __ldg(a.halo_ids + h);
-        r.loc = __ldg(a.halo_loc + h);
-        r.halo = 1;
-      }
-    }
-    return r;
-  };
-  auto issue_records = [&](const Cursor<CT> &x, int s, const RowSrc &rs) {
-    if (!x.valid(a)) return;
+  auto issue_records = [&](const Cursor<CT> &x, int s) {  // own rows: one bulk copy
+    if (!x.valid(a) || tid != 0) return;
     const int cnt = min(CT, x.ne - x.c0);
-    const int n_own = max(0, min(cnt, x.tm.own_count - x.c0));
-    if (tid == 0) {
-      mbar_arrive_expect_tx(full + s, (uint32_t)n_own * RB);
-      if (n_own)
-        bulk_g2s(stg(s), a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)n_own * RB,
-                 full + s);
-    }
-    if (tid >= n_own && tid < cnt && !(mdl.dbg & 16)) {  // 16: probe without halo rows
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        cp_async16(stg(s) + tid * RB + c * 16, a.aos + (int64_t)rs.src * RB + c * 16);
-    }
-    cp_async_arrive_noinc(full + s);
+    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB);
+    if (cnt)
+      bulk_g2s(stg(s), a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)cnt * RB, full + s);
   };
 
   double jsum = 0.0;
@@ -298,14 +267,13 @@ __global__ void __launch_bounds__(CT, MINB)
     }
     // chunks 0 and 1 go out now; chunk q + 2 is issued into stage q & 1 as soon
     // as chunk q's records have been read (two chunks of lead, not one)
-    RowSrc row_a = row_src(comp);
-    issue_records(comp, 0, row_a);
     Cursor<CT> iss = comp;
+    iss.c0 = -CT;
     iss.advance(a);
-    RowSrc row_b = row_src(iss);
-    issue_records(iss, 1, row_b);
+    issue_records(iss, 0);
     iss.advance(a);
-    RowSrc next_row = row_src(iss);
+    issue_records(iss, 1);
+    iss.advance(a);
     uint32_t q = 0, j = 0;
 
     while (comp.valid(a)) {
@@ -371,8 +339,14 @@ __global__ void __launch_bounds__(CT, MINB)
       const int ne_t = comp.ne;
       for (int c0 = 0; c0 < ne_t; c0 += CT, ++q) {
         const int s = q & 1;
-        const RowSrc this_row = row_a;
-        row_a = row_b;
+        // cross items of this chunk: contributions of own elements to nodes of
+        // other tiles, written to xbuf for the finishing pass
+        int xb = 0, xe = 0;  // (none in J-only orphan tiles)
+        if (comp.t < a.n_tiles) {
+          const int xi = comp.t * (MAX_CHUNKS + 1) + c0 / CT;
+          xb = __ldg(a.xchunk + xi);
+          xe = __ldg(a.xchunk + xi + 1);
+        }
         TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
         TRACE(1);
@@ -382,12 +356,6 @@ __global__ void __launch_bounds__(CT, MINB)
         Elem<DIM> E;
         if (valid) {
           load_elem_smem<DIM>(stg(s), tid, E);
-          if (this_row.halo) {
-            E.loc[0] = this_row.loc.x & 0xffff;
-            E.loc[1] = this_row.loc.x >> 16;
-            E.loc[2] = this_row.loc.y & 0xffff;
-            if constexpr (DIM == 3) E.loc[3] = this_row.loc.y >> 16;
-          }
           double vv[D][NV];
 #pragma unroll
           for (int l = 0; l < NV; ++l)
@@ -395,7 +363,7 @@ __global__ void __launch_bounds__(CT, MINB)
             for (int k = 0; k < D; ++k) vv[k][l] = nv[k * CAP + E.loc[l]];
           double F[D][DIM];
           grad_F_fma<DIM, D>(vv, E.g, F);
-          const bool own = e < tm.own_count;
+          const bool own = true;
           if (mdl.dbg & 1) {  // ablation: no constitutive work
 #pragma unroll
             for (int k = 0; k < D; ++k)
@@ -429,10 +397,14 @@ __global__ void __launch_bounds__(CT, MINB)
         __syncthreads();  // contributions staged; every record of stage s read
         TRACE(3);
         // stage s is free: records of chunk q + 2
-        issue_records(iss, s, next_row);
-        row_b = next_row;
+        issue_records(iss, s);
         iss.advance(a);
-        next_row = row_src(iss);
+        // first cross item of this thread (loads in flight during the consume)
+        int xkey0 = 0, xpos0 = 0;
+        if (xb + tid < xe) {
+          xkey0 = __ldg(a.xkey + xb + tid);
+          xpos0 = __ldg(a.xpos + xb + tid);
+        }
         if (my_node && !(mdl.dbg & 2)) {
           // this node's entries of the chunk: a known count, so the loads of
           // two entries are issued together; the order (ascending tile element)
@@ -441,6 +413,7 @@ __global__ void __launch_bounds__(CT, MINB)
           int i = 0;
           for (; i + 1 < n; i += 2) {
             const int e0 = ents[cur + i], e1 = ents[cur + i + 1];
+            if ((e1 >> 2) >= ne_t) break;  // cross entries (finishing pass) from here on
             const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
             const double *s1 = stage_d + ((e1 >> 2) - c0) + (e1 & 3) * D * CT;
             double x0[D], x1[D];
@@ -455,10 +428,19 @@ __global__ void __launch_bounds__(CT, MINB)
           if (i < n) {
             const int e0 = ents[cur + i];
             const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
+            if ((e0 >> 2) < ne_t) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
+              for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
+            }
           }
           cur += n;
+        }
+        for (int i = xb + tid; i < xe; i += CT) {
+          const int key = i == xb + tid ? xkey0 : (int)__ldg(a.xkey + i);
+          const int64_t pos = i == xb + tid ? xpos0 : __ldg(a.xpos + i);
+          const double *sp = stage_d + ((key >> 2) - c0) + (key & 3) * D * CT;
+#pragma unroll
+          for (int k = 0; k < D; ++k) a.xbuf[pos * D + k] = sp[k * CT];
         }
         // one staging buffer: it must be consumed before the next chunk writes
         // it; two: the next chunk's barrier already orders this consumption
@@ -466,7 +448,6 @@ __global__ void __launch_bounds__(CT, MINB)
         TRACE(4);
         if (NS == 1) __syncthreads();
         TRACE(5);
-        comp.advance(a);
       }
       if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
       if (my_node) {
@@ -477,6 +458,9 @@ __global__ void __launch_bounds__(CT, MINB)
           if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
       }
       ++j;
+      comp.t += gridDim.x;  // every tile is visited (outputs), even without chunks
+      comp.c0 = 0;
+      comp.load(a);
     }
   }
   if (bad_any) atomicOr(status, 1ull);
@@ -484,6 +468,48 @@ __global__ void __launch_bounds__(CT, MINB)
     double r = block_sum(jsum, red);
     if (tid == 0) jpart[blockIdx.x] = r;
   }
+}
+
+// Finishing pass: a node's cross entries (elements owned by other tiles, the
+// tail of its sorted entry list) were written by their owner tiles into xbuf at
+// the entries' global indices; add them in ascending tile-element order.
+template <int D>
+__global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn, const int4 *__restrict__ desc,
+                                                      const int32_t *__restrict__ xbase,
+                                                      const int32_t *__restrict__ xn,
+                                                      const double *__restrict__ xbuf,
+                                                      double *__restrict__ g) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int n = xn[k];
+    if (!n) continue;
+    const int w = desc[k].w;
+    const int mask = (unsigned)w >> OUT_MASK_SHIFT;
+    int o = w & ((1 << OUT_MASK_SHIFT) - 1);
+    const double *x = xbuf + (int64_t)xbase[k] * D;
+    double sum[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) sum[j] = 0.0;
+    for (int p = 0; p < n; ++p)  // the node's entries are contiguous: D doubles each
+#pragma unroll
+      for (int j = 0; j < D; ++j) sum[j] += __ldg(x + p * D + j);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      if (mask & (1 << j)) {
+        g[o] += sum[j];
+        ++o;
+      }
+  }
+}
+
+cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *desc, const int32_t *xbase,
+                                const int32_t *xn, const double *xbuf, double *g,
+                                cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((ntn + 255) / 256, 148 * 16);
+  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
+  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
+  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
+  return cudaGetLastError();
 }
 
 size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns) {
