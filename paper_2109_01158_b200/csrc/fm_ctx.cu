@@ -323,7 +323,7 @@ __global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
       const int to = stile[st];
       const int te = st - meta[to].own_begin;
       keys[xoff[k] + p] = ((uint64_t)to << 16) | (uint64_t)((te << 2) | (en & 3));
-      vals[xoff[k] + p] = xbase[k] + p;
+      vals[xoff[k] + p] = xoff[k] + p;  // dense exchange slot, node-major
     }
   }
 }
@@ -1154,7 +1154,9 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(dmalloc(&c->xkey, X + 8, &B));
     CK(dmalloc(&c->xpos, X + 8, &B));
     CK(dmalloc(&c->xchunk, (size_t)n_tiles * (MAX_CHUNKS + 1), &B));
-    CK(dmalloc(&c->xbuf, (size_t)(entry_total + 8) * d, &B));
+    CK(dmalloc(&c->xbuf, (size_t)(X + 8) * d, &B));
+    // the finishing pass reads each node's exchange slots from its dense offset
+    CK(cudaMemcpyAsync(c->node_xbase, xoff.p, nfree * 4, cudaMemcpyDeviceToDevice, s));
     if (X) {
       k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
       CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));

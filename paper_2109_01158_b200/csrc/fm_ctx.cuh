@@ -179,9 +179,10 @@ struct TileArgs {
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
   const int32_t *rank_of;      // node -> free rank or -1
   // cross-tile exchange of the fused exact kernel (elements computed once, by
-  // their owner tile): items (owner te << 2 | slot) -> global entry index,
-  // sorted by (owner tile, te); xchunk[t * (MAX_CHUNKS + 1) + c] = first item of
-  // chunk c of tile t; xbuf[entry * D + k] receives the contributions
+  // their owner tile): items (owner te << 2 | slot) -> exchange slot, sorted by
+  // (owner tile, te); xchunk[t * (MAX_CHUNKS + 1) + c] = first item of chunk c
+  // of tile t; xbuf[slot * D + k] receives the contributions (slots are dense
+  // and node-major: a node's cross entries are consecutive, in te order)
   const uint16_t *xkey;
   const int32_t *xpos;
   const int32_t *xchunk;
