@@ -279,6 +279,12 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
   }
 }
 
+__global__ void k_not_free(int64_t nn, const int32_t *rank_of, uint8_t *flag) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn;
+       n += (int64_t)gridDim.x * blockDim.x)
+    flag[n] = rank_of[n] < 0;
+}
+
 // storage index -> owner tile (own ranges are contiguous per tile)
 __global__ void k_storage_tile(int n_tiles, const int32_t *own_ptr, int32_t *stile) {
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x)
@@ -698,6 +704,28 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaMemcpyAsync(&nfd, c->free_out + nfree, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->nfree_dofs = nfd;
+    // nodes outside every tile (all components fixed): their b.v goes to the
+    // fused path's finalize
+    Scratch fl, nsel;
+    CK(fl.alloc(m->nn, s));
+    CK(nsel.alloc(8, s));
+    CK(dmalloc(&c->fixed_nodes, m->nn - nfree + 1, &B));
+    k_not_free<<<grid_for(m->nn, 256), 256, 0, s>>>(m->nn, c->rank_of, fl.as<uint8_t>());
+    CK(cudaGetLastError());
+    {
+      cub::CountingInputIterator<int32_t> it(0);
+      const uint8_t *flp = fl.as<uint8_t>();
+      int32_t *ns = nsel.as<int32_t>();
+      int32_t *outp = c->fixed_nodes;
+      const int64_t nn = m->nn;
+      CK(cub_call([&](void *t, size_t &b) {
+        return cub::DeviceSelect::Flagged(t, b, it, flp, outp, ns, nn, s);
+      }, s));
+      int32_t hn = 0;
+      CK(cudaMemcpyAsync(&hn, nsel.p, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      c->n_fixed_nodes = hn;
+    }
   }
 
   // 2. node tiles (Morton-ordered boxes) -------------------------------------
@@ -1209,7 +1237,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->n_dot_blocks = 148 * 2;
   c->n_part = std::max(c->n_sm, c->n_energy_blocks);
   CK(dmalloc(&c->jpart, c->n_part, &B));
-  CK(dmalloc(&c->dotpart, c->n_dot_blocks, &B));
+  CK(dmalloc(&c->dotpart, std::max(c->n_part, c->n_dot_blocks), &B));
   CK(dmalloc(&c->status, 2, &B));
   unsigned long long init[2] = {0ull, ~0ull};
   CK(cudaMemcpyAsync(c->status, init, 16, cudaMemcpyHostToDevice, s));
@@ -1241,7 +1269,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
-                  c->node_xbase, c->node_xn,  c->xbuf};
+                  c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1293,7 +1321,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
     FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
-                              c->stage_bufs, wj, v, b, g, c->jpart, c->status, ma, s));
+                              c->stage_bufs, wj, v, b, g, c->jpart, c->dotpart, c->status, ma,
+                              s));
     c->launches++;
   }
   if (c->n_cross > 0) {
@@ -1301,14 +1330,9 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
                                 g, s));
     c->launches++;
   }
-  if (wj) {
-    int nd = 0;
-    if (b) {
-      FM_CUDA(launch_dot(v, b, c->nn * c->d, c->n_dot_blocks, c->dotpart, s));
-      nd = c->n_dot_blocks;
-      c->launches++;
-    }
-    FM_CUDA(launch_finalize(c->jpart, ta.n_tiles_all > 0 ? grid : 0, c->dotpart, nd, J_out, s));
+  if (wj) {  // b.v of the tile nodes came with the tile kernel's partials
+    FM_CUDA(launch_finalize_tiles(c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0,
+                                  c->fixed_nodes, c->n_fixed_nodes, b, v, c->d, J_out, s));
     c->launches++;
   }
   return FM_OK;

@@ -237,6 +237,8 @@ struct fm_ctx {
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
   double *xbuf = nullptr;
   int64_t n_cross = 0;
+  int32_t *fixed_nodes = nullptr;  // nodes without a free dof (b.v in the fused finalize)
+  int64_t n_fixed_nodes = 0;
   // scratch
   double *jpart = nullptr;        // per CTA (fused) / per block (energy)
   double *dotpart = nullptr;      // b.v partials

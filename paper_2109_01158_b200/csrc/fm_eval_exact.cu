@@ -185,8 +185,8 @@ struct Cursor {
 template <int DIM, int MODEL, bool WJ, int CT, int NB, int NS, int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
-                 double *__restrict__ g, double *__restrict__ jpart, unsigned long long *status,
-                 ModelArgs mdl) {
+                 double *__restrict__ g, double *__restrict__ jpart, double *__restrict__ bvpart,
+                 unsigned long long *status, ModelArgs mdl) {
   constexpr int NV = DIM + 1;
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int RB = RecBytes<DIM>::value;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(CT, MINB)
       bulk_g2s(stg(s), a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)cnt * RB, full + s);
   };
 
-  double jsum = 0.0;
+  double jsum = 0.0, bvsum = 0.0;  // vol*W of own elements; b.v of the tile nodes' dofs
   bool bad_any = false;
   Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}};
   comp.load(a);
@@ -450,6 +450,10 @@ __global__ void __launch_bounds__(CT, MINB)
         TRACE(5);
       }
       if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
+      if (WJ && my_node && b) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) bvsum += bj[k] * __ldg(v + (int64_t)nd.z * D + k);
+      }
       if (my_node) {
         const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
         int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
@@ -465,8 +469,12 @@ __global__ void __launch_bounds__(CT, MINB)
   }
   if (bad_any) atomicOr(status, 1ull);
   if (WJ) {
-    double r = block_sum(jsum, red);
-    if (tid == 0) jpart[blockIdx.x] = r;
+    const double r = block_sum(jsum, red);
+    const double r2 = block_sum(bvsum, red);
+    if (tid == 0) {
+      jpart[blockIdx.x] = r;
+      bvpart[blockIdx.x] = r2;
+    }
   }
 }
 
@@ -522,7 +530,7 @@ size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int n
 
 template <int DIM, int MODEL, int CT, int NB, int NS>
 static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double *v,
-                              const double *b, double *g, double *jpart,
+                              const double *b, double *g, double *jpart, double *bvpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int MINB = CT == 128 ? 4 : 2;  // <= 128 registers per thread
@@ -530,46 +538,47 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double
   auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, NS, MINB>
               : k_tile_exact<DIM, MODEL, false, CT, NB, NS, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, status, m);
+  k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, bvpart, status, m);
   return cudaGetLastError();
 }
 
 template <int DIM, int MODEL, int CT>
 static cudaError_t launch_ct(const TileArgs &a, int grid, int nb, int ns, bool wj,
                              const double *v, const double *b, double *g, double *jpart,
-                             unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
+                             double *bvpart, unsigned long long *status, const ModelArgs &m,
+                             cudaStream_t s) {
   if (nb == 2 && ns == 2)
-    return launch_cfg<DIM, MODEL, CT, 2, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
-  if (nb == 2) return launch_cfg<DIM, MODEL, CT, 2, 1>(a, grid, wj, v, b, g, jpart, status, m, s);
-  if (ns == 2) return launch_cfg<DIM, MODEL, CT, 1, 2>(a, grid, wj, v, b, g, jpart, status, m, s);
-  return launch_cfg<DIM, MODEL, CT, 1, 1>(a, grid, wj, v, b, g, jpart, status, m, s);
+    return launch_cfg<DIM, MODEL, CT, 2, 2>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
+  if (nb == 2) return launch_cfg<DIM, MODEL, CT, 2, 1>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
+  if (ns == 2) return launch_cfg<DIM, MODEL, CT, 1, 2>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
+  return launch_cfg<DIM, MODEL, CT, 1, 1>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
 }
 
 template <int DIM, int MODEL>
 static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, int ns, bool wj,
                                   const double *v, const double *b, double *g, double *jpart,
-                                  unsigned long long *status, const ModelArgs &m,
+                                  double *bvpart, unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
   if (DIM == 3 && ct == 128)
-    return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, wj, v, b, g, jpart, status, m, s);
-  return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, wj, v, b, g, jpart, status, m, s);
+    return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
+  return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
 }
 
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
                               int ns, bool wj, const double *v, const double *b, double *g,
-                              double *jpart, unsigned long long *status, const ModelArgs &m,
-                              cudaStream_t s) {
+                              double *jpart, double *bvpart, unsigned long long *status,
+                              const ModelArgs &m, cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
-                                                m, s);
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+                                                status, m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
-                                                m, s);
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+                                                status, m, s);
   if (dim == 2)
     return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart,
-                                                  status, m, s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart, status,
-                                                m, s);
+                                                  bvpart, status, m, s);
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+                                                status, m, s);
 }
 
 }  // namespace fm

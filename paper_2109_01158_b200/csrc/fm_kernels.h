@@ -13,8 +13,8 @@ namespace fm {
 // ns = staging buffers (2: one barrier per chunk, 1: two)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
                               int ns, bool wj, const double *v, const double *b, double *g,
-                              double *jpart, unsigned long long *status, const ModelArgs &m,
-                              cudaStream_t s);
+                              double *jpart, double *bvpart, unsigned long long *status,
+                              const ModelArgs &m, cudaStream_t s);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *desc, const int32_t *xbase,
                                 const int32_t *xn, const double *xbuf, double *g,
                                 cudaStream_t s);
@@ -33,6 +33,9 @@ cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, i
 cudaError_t launch_dot(const double *a, const double *b, int64_t n, int nblocks, double *part,
                        cudaStream_t s);
 
+cudaError_t launch_finalize_tiles(const double *jp, const double *bvp, int n,
+                                  const int32_t *fixed_nodes, int64_t nfixed, const double *b,
+                                  const double *v, int d, double *out, cudaStream_t s);
 cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, double *out,
                             cudaStream_t s);
 
