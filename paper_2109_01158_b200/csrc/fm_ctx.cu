@@ -165,7 +165,21 @@ __global__ void k_lower_bounds_u32(int n, int64_t len, const uint32_t *sorted, i
   }
 }
 
-// records (vol | dphi | closure indices, filled by k_fill_loc) + conn4 in storage order
+// dphi[m][:, 0] == -(dphi[m][:, 1:].sum()) bit for bit (mesh.py:100-101)?
+template <int DIM>
+__global__ void k_dphi0_check(int64_t ne, const double *dphi, unsigned long long *bad) {
+  constexpr int NV = DIM + 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x)
+    for (int m = 0; m < DIM; ++m) {
+      const double *g = dphi + ((int64_t)m * ne + e) * NV;
+      double r = __dadd_rn(g[1], g[2]);
+      if (DIM == 3) r = __dadd_rn(r, g[3]);
+      if (!(g[0] == -r)) atomicMin(bad, (unsigned long long)e);
+    }
+}
+
+// records (vol | dphi[m][1..]) + conn4 in storage order
 template <int DIM>
 __global__ void k_build_aos(int64_t ne, const int32_t *s2o, const int64_t *conn, const double *vol,
                             const double *dphi, uint8_t *aos, int4 *conn4) {
@@ -177,8 +191,8 @@ __global__ void k_build_aos(int64_t ne, const int32_t *s2o, const int64_t *conn,
     double *dd = reinterpret_cast<double *>(aos + s * RecBytes<DIM>::value);
     dd[0] = vol[e];
     for (int m = 0; m < DIM; ++m)
-      for (int l = 0; l < NV; ++l) dd[1 + m * NV + l] = dphi[((int64_t)m * ne + e) * NV + l];
-    for (int k = 1 + DIM * NV; k < NF; ++k) dd[k] = 0.0;
+      for (int l = 1; l < NV; ++l) dd[1 + m * DIM + l - 1] = dphi[((int64_t)m * ne + e) * NV + l];
+    for (int k = 1 + DIM * DIM; k < NF; ++k) dd[k] = 0.0;
     int4 c;
     c.x = (int)conn[e * NV];
     c.y = (int)conn[e * NV + 1];
@@ -237,7 +251,7 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
                            int n_tiles, int ot, const int32_t *s2o, const int32_t *o2s,
                            const int64_t *conn, const uint64_t *ckeys, const int32_t *cstart,
                            const int32_t *ptr, const int32_t *split, const int32_t *tpos,
-                           const int32_t *halo_begin, uint8_t *aos, uint2 *halo_loc,
+                           const int32_t *halo_begin, uint2 *loc, uint2 *halo_loc,
                            unsigned long long *overflow) {
   constexpr int NV = DIM + 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + n_orph;
@@ -273,8 +287,7 @@ __global__ void k_fill_loc(int64_t M, const uint64_t *ukeys, int64_t n_orph, int
       halo_loc[halo_begin[t] + tpos[i] - (split[t] - ptr[t])] =
           make_uint2((unsigned)(packed & 0xffffffffull), (unsigned)(packed >> 32));
     } else {
-      uint64_t *w = reinterpret_cast<uint64_t *>(aos + s * RecBytes<DIM>::value);
-      w[1 + DIM * NV] = packed;  // the 8 bytes after vol | dphi
+      loc[s] = make_uint2((unsigned)(packed & 0xffffffffull), (unsigned)(packed >> 32));
     }
   }
 }
@@ -917,8 +930,29 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   }
   k_inverse<<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, o2s.as<int32_t>());
   CK(cudaGetLastError());
+  {
+    Scratch bad;
+    CK(bad.alloc(8, s));
+    CK(cudaMemsetAsync(bad.p, 0xff, 8, s));
+    if (dim == 3)
+      k_dphi0_check<3><<<grid_for(ne, 256), 256, 0, s>>>(ne, m->dphi, bad.as<unsigned long long>());
+    else
+      k_dphi0_check<2><<<grid_for(ne, 256), 256, 0, s>>>(ne, m->dphi, bad.as<unsigned long long>());
+    CK(cudaGetLastError());
+    unsigned long long hb = 0;
+    CK(cudaMemcpyAsync(&hb, bad.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hb != ~0ull) {
+      set_error("element " + std::to_string(hb) +
+                ": dphi[m][k, 0] differs from -dphi[m][k, 1:].sum() (compute_p1_gradients, "
+                "mesh.py:100-101, makes them equal; the records store only columns 1..dim)");
+      return fail(FM_INVALID_ARG);
+    }
+  }
   const int rb = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
   CK(dmalloc(&c->aos, (size_t)ne * rb, &B));
+  CK(dmalloc(&c->loc, ne + 2, &B));
+  CK(cudaMemsetAsync(c->loc, 0, (ne + 2) * 8, s));
   CK(dmalloc(&c->conn4, ne, &B));
   if (dim == 3)
     k_build_aos<3><<<grid_for(ne, 256), 256, 0, s>>>(ne, c->storage_to_orig, m->conn, m->volumes,
@@ -1053,13 +1087,13 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       k_fill_loc<3><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
           M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
           o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tptr.as<int32_t>(),
-          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->aos, c->halo_loc,
+          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->loc, c->halo_loc,
           ovf.as<unsigned long long>());
     else
       k_fill_loc<2><<<grid_for(M + n_orph, 256), 256, 0, s>>>(
           M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
           o2s.as<int32_t>(), m->conn, cuk, cstart.as<int32_t>(), tptr.as<int32_t>(),
-          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->aos, c->halo_loc,
+          tsplit.as<int32_t>(), tpos.as<int32_t>(), hb.as<int32_t>(), c->loc, c->halo_loc,
           ovf.as<unsigned long long>());
     CK(cudaGetLastError());
     unsigned long long h_ovf = 0;
@@ -1265,7 +1299,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
 
 int fm_ctx_destroy(fm_ctx *c) {
   if (!c) return FM_OK;
-  void *ptrs[] = {c->aos,       c->conn4,     c->meta,      c->halo_ids,  c->halo_loc,
+  void *ptrs[] = {c->aos,       c->conn4,     c->meta,      c->halo_ids,  c->halo_loc, c->loc,
                   c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,

@@ -5,11 +5,15 @@
 // Element records (AoS, storage order = grouped by owner tile, 16-B multiples
 // with an ODD number of 16-B chunks so that lane i reading record i from shared
 // memory is bank-conflict free):
-//   3D: 112 B = f64 vol | f64 dphi[3][4] | u16 loc[4]
-//   2D:  80 B = f64 vol | f64 dphi[2][3] | u16 loc[3] | pad
-// loc are the element's nodes as indices into its OWNER tile's node closure
-// (sorted distinct nodes of all elements the tile visits); global node ids live
-// in conn4 (int4 per element, storage order) for the streaming kernels.
+//   3D: 80 B = f64 vol | f64 dphi[3][1..3]
+//   2D: 48 B = f64 vol | f64 dphi[2][1..2] | pad
+// dphi[m][0] is not stored: compute_p1_gradients makes it -(sum of the other
+// columns) (mesh.py:100-101), and the context build checks that identity bit
+// for bit before dropping it, so decode_elem rebuilds the exact reference value.
+// loc (u16 x 4 per element, storage order) are the element's nodes as indices
+// into its OWNER tile's node closure (sorted distinct nodes of all elements the
+// tile visits); global node ids live in conn4 (int4 per element, storage order)
+// for the streaming kernels.
 //
 // Node tiles: each tile owns <= 256 free nodes of a spatial box.  Its element
 // list is [own elements (contiguous storage range, the tile is their J owner)]
@@ -39,8 +43,8 @@ __device__ __forceinline__ int chunk_count(int4 nd, int ch) {
 }
 
 template <int DIM> struct RecBytes;
-template <> struct RecBytes<2> { static constexpr int value = 80; };
-template <> struct RecBytes<3> { static constexpr int value = 112; };
+template <> struct RecBytes<2> { static constexpr int value = 48; };
+template <> struct RecBytes<3> { static constexpr int value = 80; };
 
 struct TileMeta {
   int own_begin, own_count;      // storage range of the elements the tile owns
@@ -54,8 +58,8 @@ struct TileMeta {
 static_assert(sizeof(TileMeta) == 48, "TileMeta layout");
 
 template <int DIM> struct Elem {
-  int c[DIM + 1];    // global node ids (streaming kernels)
-  int loc[DIM + 1];  // owner-tile closure indices (tile kernel)
+  int c[DIM + 1];  // global node ids (streaming kernels)
+  int loc[4];      // closure indices (tile kernels; decode_loc)
   double vol;
   double g[DIM][DIM + 1];  // dphi[m][l]
 };
@@ -77,29 +81,42 @@ __device__ __forceinline__ int4 ld_stream_i4(const int4 *p) {
   return r;
 }
 
+// dphi[m][0] = -((dphi[m][1] + dphi[m][2]) + dphi[m][3]) as numpy's sum over
+// the row (mesh.py:101); negation is exact
+template <int DIM>
+__device__ __forceinline__ double dphi0(const double (&g)[DIM + 1]) {
+  if constexpr (DIM == 3)
+    return -__dadd_rn(__dadd_rn(g[1], g[2]), g[3]);
+  else
+    return -__dadd_rn(g[1], g[2]);
+}
+
 template <int DIM>
 __device__ __forceinline__ void decode_elem(const double2 (&q)[RecBytes<DIM>::value / 16],
                                             Elem<DIM> &E) {
   E.vol = q[0].x;
-  long long lb;
   if constexpr (DIM == 3) {
-    const double f[12] = {q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x,
-                          q[3].y, q[4].x, q[4].y, q[5].x, q[5].y, q[6].x};
+    const double f[9] = {q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x, q[3].y, q[4].x, q[4].y};
 #pragma unroll
     for (int m = 0; m < 3; ++m)
 #pragma unroll
-      for (int l = 0; l < 4; ++l) E.g[m][l] = f[m * 4 + l];
-    lb = __double_as_longlong(q[6].y);
+      for (int l = 1; l < 4; ++l) E.g[m][l] = f[m * 3 + l - 1];
   } else {
-    const double f[6] = {q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x};
+    const double f[4] = {q[0].y, q[1].x, q[1].y, q[2].x};
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int l = 0; l < 3; ++l) E.g[m][l] = f[m * 3 + l];
-    lb = __double_as_longlong(q[3].y);
+      for (int l = 1; l < 3; ++l) E.g[m][l] = f[m * 2 + l - 1];
   }
 #pragma unroll
-  for (int l = 0; l < DIM + 1; ++l) E.loc[l] = (int)((lb >> (16 * l)) & 0xffff);
+  for (int m = 0; m < DIM; ++m) E.g[m][0] = dphi0<DIM>(E.g[m]);
+}
+
+__device__ __forceinline__ void decode_loc(uint2 w, int (&loc)[4]) {
+  loc[0] = (int)(w.x & 0xffffu);
+  loc[1] = (int)(w.x >> 16);
+  loc[2] = (int)(w.y & 0xffffu);
+  loc[3] = (int)(w.y >> 16);
 }
 
 // record + global connectivity from global memory (streaming kernels)
@@ -172,6 +189,7 @@ struct TileArgs {
   const TileMeta *meta;        // n_tiles_all
   const int32_t *halo_ids;     // storage index of halo elements
   const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements
+  const uint2 *loc;            // closure indices (u16 x 4) w.r.t. the owner tile, storage order
   const int32_t *closure;      // node ids of the tile closures
   const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
   const int4 *node_desc;       // {entry_off | chunk counts, chunk counts, node id,
@@ -225,7 +243,7 @@ struct fm_ctx {
   int4 *conn4 = nullptr;
   fm::TileMeta *meta = nullptr;
   int32_t *halo_ids = nullptr, *closure = nullptr;
-  uint2 *halo_loc = nullptr;
+  uint2 *halo_loc = nullptr, *loc = nullptr;
   uint8_t *flags = nullptr;
   int4 *node_desc = nullptr;
   uint16_t *node_entries = nullptr;
@@ -251,7 +269,7 @@ struct fm_ctx {
 
   fm::TileArgs tile_args() const {
     return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
-                        closure, flags,   node_desc,       node_entries, rank_of,  xkey,
+                        loc,     closure, flags,   node_desc,       node_entries, rank_of,  xkey,
                         xpos,    xchunk,  xbuf,            n_tiles,   n_tiles_all, entry_cap,
                         clo_cap};
   }

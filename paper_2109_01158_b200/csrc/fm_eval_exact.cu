@@ -60,7 +60,8 @@ __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; 
 template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
-  __host__ __device__ static size_t stage() { return r16((size_t)CT * RB); }
+  // records, then the rows' closure indices (u16 x 4)
+  __host__ __device__ static size_t stage() { return r16((size_t)CT * RB) + (size_t)(CT + 2) * 8; }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
   __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
@@ -192,7 +193,6 @@ __global__ void __launch_bounds__(CT, MINB)
   constexpr int RB = RecBytes<DIM>::value;
   constexpr int NCH = RB / 16;
   using L = PipeLayout<DIM, CT>;
-  static_assert((size_t)CT * NV * D * 8 <= (size_t)CT * RB, "staging fits a stage");
   extern __shared__ __align__(16) unsigned char smem[];
   const int CAP = a.clo_cap;
   // stage s at smem + s * stage(); node-value buffer k at nodev0 + k * nodev()
@@ -243,12 +243,20 @@ __global__ void __launch_bounds__(CT, MINB)
     }
     cp_async_arrive_noinc(nfull + k);
   };
-  auto issue_records = [&](const Cursor<CT> &x, int s) {  // own rows: one bulk copy
+  // own rows: records and their closure indices, one bulk copy each (the
+  // 8-byte index range is widened to 16-byte alignment: row r sits at
+  // position r + (r0 & 1) of the stage's index array)
+  auto issue_records = [&](const Cursor<CT> &x, int s) {
     if (!x.valid(a) || tid != 0) return;
     const int cnt = min(CT, x.ne - x.c0);
-    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB);
-    if (cnt)
-      bulk_g2s(stg(s), a.aos + (int64_t)(x.tm.own_begin + x.c0) * RB, (uint32_t)cnt * RB, full + s);
+    const int64_t r0 = (int64_t)x.tm.own_begin + x.c0;
+    const int64_t l0 = r0 & ~1ll;
+    const uint32_t nl = (uint32_t)((cnt + (r0 - l0) + 1) & ~1);
+    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB + nl * 8);
+    if (cnt) {
+      bulk_g2s(stg(s), a.aos + r0 * RB, (uint32_t)cnt * RB, full + s);
+      bulk_g2s(stg(s) + r16((size_t)CT * RB), a.loc + l0, nl * 8, full + s);
+    }
   };
 
   double jsum = 0.0, bvsum = 0.0;  // vol*W of own elements; b.v of the tile nodes' dofs
@@ -356,6 +364,9 @@ __global__ void __launch_bounds__(CT, MINB)
         Elem<DIM> E;
         if (valid) {
           load_elem_smem<DIM>(stg(s), tid, E);
+          decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + r16((size_t)CT * RB) +
+                                                       (tid + ((tm.own_begin + c0) & 1)) * 8),
+                     E.loc);
           double vv[D][NV];
 #pragma unroll
           for (int l = 0; l < NV; ++l)

@@ -121,10 +121,11 @@ cudaError_t launch_finalize_tiles(const double *jp, const double *bvp, int n,
 // i.e. the first offending stacked row in reference order (gradients.py:77-81).
 template <int DIM, int CT>
 struct FdLayout {
-  static constexpr int RB = RecBytes<DIM>::value;
+  // expanded shared-memory rows: vol | dphi[DIM][DIM + 1] | loc word
+  static constexpr int FRB = 8 * (2 + DIM * (DIM + 1));
   __host__ __device__ static size_t r16(size_t x) { return (x + 15) / 16 * 16; }
   __host__ __device__ static size_t nodev(int D, int cap) { return r16((size_t)D * cap * 8); }
-  __host__ __device__ static size_t recs() { return (size_t)CT * RB; }
+  __host__ __device__ static size_t recs() { return (size_t)CT * FRB; }
   __host__ __device__ static size_t fbuf(int D) { return r16((size_t)CT * D * DIM * 8); }
   __host__ __device__ static size_t stg(int D, int ech) { return (size_t)D * ech * 16; }
   __host__ __device__ static size_t flat(int ech) { return r16((size_t)ech * 2); }
@@ -173,8 +174,9 @@ __global__ void __launch_bounds__(CT, 512 / CT)
   constexpr int RB = RecBytes<DIM>::value;
   constexpr int NQ = RB / 16;
   constexpr int NF = D * DIM;
-  constexpr int LW = 1 + DIM * NV;  // record word holding the closure indices (odd)
   using L = FdLayout<DIM, CT>;
+  constexpr int FRB = L::FRB;
+  constexpr int LW = 1 + DIM * NV;  // shared row word holding the closure indices
   extern __shared__ __align__(16) unsigned char smem[];
   const int CAP = a.clo_cap;
   double *nodev = reinterpret_cast<double *>(smem);
@@ -222,15 +224,17 @@ __global__ void __launch_bounds__(CT, 512 / CT)
       double2 q[NQ];
 #pragma unroll
       for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
-      if (halo) {
-        const uint2 hl = __ldg(a.halo_loc + h);
-        q[LW / 2].y = __longlong_as_double((long long)(((unsigned long long)hl.y << 32) | hl.x));
-      }
-      double2 *dst = reinterpret_cast<double2 *>(recs + tid * RB);
-#pragma unroll
-      for (int k = 0; k < NQ; ++k) dst[k] = q[k];
+      const uint2 lw = halo ? __ldg(a.halo_loc + h) : __ldg(a.loc + s);
       Elem<DIM> E;
       decode_elem<DIM>(q, E);
+      decode_loc(lw, E.loc);
+      double *dst = reinterpret_cast<double *>(recs + tid * FRB);
+      dst[0] = E.vol;
+#pragma unroll
+      for (int m = 0; m < DIM; ++m)
+#pragma unroll
+        for (int l = 0; l < NV; ++l) dst[1 + m * NV + l] = E.g[m][l];
+      *reinterpret_cast<uint2 *>(dst + LW) = lw;
       double vv[D][NV];
 #pragma unroll
       for (int l = 0; l < NV; ++l)
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(CT, 512 / CT)
       for (int f = (tid - j * total) & (CT - 1); f < total; f += CT) {
         const int en = flat[f];
         const int r = (en >> 2) - c0, l = en & 3;
-        const unsigned char *rec = recs + r * RB;
+        const unsigned char *rec = recs + r * FRB;
         const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
         const unsigned long long lw = *reinterpret_cast<const unsigned long long *>(rec + LW * 8);
         auto vat = [&](int k) { return nodev[j * CAP + (int)((lw >> (16 * k)) & 0xffffull)]; };
