@@ -325,6 +325,14 @@ __global__ void k_cross_count(int64_t ntn, const int32_t *tile_node_rank,
   }
 }
 
+__global__ void k_mark_cross(int64_t ntn, const int32_t *xn, int4 *desc, int32_t *outw) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    outw[k] = desc[k].w;
+    if (xn[k]) desc[k].w = (int)((unsigned)desc[k].w | CROSS_FLAG);
+  }
+}
+
 // the cross items: (owner tile, owner te, slot) -> entry index
 __global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
                               const int32_t *tile_of_rank, const TileMeta *meta,
@@ -1173,7 +1181,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     k_storage_tile<<<std::min(n_tiles, 65535), 256, 0, s>>>(n_tiles, own_ptr.as<int32_t>(),
                                                              stile.as<int32_t>());
     CK(cudaGetLastError());
-    CK(dmalloc(&c->node_xbase, nfree, &B));
+    CK(dmalloc(&c->node_xbase, nfree + 1, &B));
     CK(dmalloc(&c->node_xn, nfree, &B));
     k_cross_count<<<grid_for(nfree, 256), 256, 0, s>>>(
         nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(), c->meta, c->node_desc, c->node_entries,
@@ -1196,6 +1204,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaStreamSynchronize(s));
     const int64_t X = hX;
     c->n_cross = X;
+    CK(cudaMemcpyAsync(xoff.as<int32_t>() + nfree, xsum.p, 4, cudaMemcpyDeviceToDevice, s));
     CK(xk.alloc(std::max<int64_t>(X, 1) * 8, s));
     CK(xk2.alloc(std::max<int64_t>(X, 1) * 8, s));
     CK(xv.alloc(std::max<int64_t>(X, 1) * 4, s));
@@ -1218,7 +1227,14 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(dmalloc(&c->xchunk, (size_t)n_tiles * (MAX_CHUNKS + 1), &B));
     CK(dmalloc(&c->xbuf, (size_t)(X + 8) * d, &B));
     // the finishing pass reads each node's exchange slots from its dense offset
-    CK(cudaMemcpyAsync(c->node_xbase, xoff.p, nfree * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->node_xbase, xoff.p, (nfree + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    // nodes with cross entries: flagged in their descriptor (the tile kernel
+    // then leaves a dense partial sum instead of g), outputs for the finish
+    CK(dmalloc(&c->node_outw, nfree, &B));
+    CK(dmalloc(&c->partial, (size_t)nfree * d, &B));
+    k_mark_cross<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->node_xn, c->node_desc,
+                                                       c->node_outw);
+    CK(cudaGetLastError());
     if (X) {
       k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
       CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));
@@ -1303,7 +1319,8 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
-                  c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes};
+                  c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
+                  c->partial};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1360,7 +1377,7 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     c->launches++;
   }
   if (c->n_cross > 0) {
-    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_desc, c->node_xbase, c->node_xn, c->xbuf,
+    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_xbase, c->node_outw, c->xbuf, c->partial,
                                 g, s));
     c->launches++;
   }

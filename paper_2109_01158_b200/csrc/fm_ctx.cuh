@@ -32,6 +32,7 @@ namespace fm {
 constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
 constexpr int CONSUMERS = 256;         // threads per tile CTA = chunk size = max tile nodes
 constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
+constexpr unsigned CROSS_FLAG = 1u << 31;  // node_desc.w: the node has cross entries
 constexpr int MAX_CHUNKS = 9;          // per-chunk entry counts in node_desc.x/.y (5 bits each)
 constexpr int ENTRY_OFF_MASK = (1 << 13) - 1;  // node_desc.x bits 0..12: tile-local entry offset
 
@@ -205,6 +206,7 @@ struct TileArgs {
   const int32_t *xpos;
   const int32_t *xchunk;
   double *xbuf;
+  double *partial;             // tile node x D: own-element sums of nodes with cross entries
   int n_tiles;                 // node tiles
   int n_tiles_all;             // + orphan tiles (J only)
   int entry_cap;               // max entries of one tile, rounded up to 8
@@ -253,7 +255,8 @@ struct fm_ctx {
   uint16_t *xkey = nullptr;                        // cross-tile exchange (see TileArgs)
   int32_t *xpos = nullptr, *xchunk = nullptr;
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
-  double *xbuf = nullptr;
+  double *xbuf = nullptr, *partial = nullptr;
+  int32_t *node_outw = nullptr;  // per tile node: out offset | mask << 28
   int64_t n_cross = 0;
   int32_t *fixed_nodes = nullptr;  // nodes without a free dof (b.v in the fused finalize)
   int64_t n_fixed_nodes = 0;
@@ -270,7 +273,7 @@ struct fm_ctx {
   fm::TileArgs tile_args() const {
     return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
                         loc,     closure, flags,   node_desc,       node_entries, rank_of,  xkey,
-                        xpos,    xchunk,  xbuf,            n_tiles,   n_tiles_all, entry_cap,
-                        clo_cap};
+                        xpos,    xchunk,  xbuf,            partial,   n_tiles,     n_tiles_all,
+                        entry_cap, clo_cap};
   }
 };

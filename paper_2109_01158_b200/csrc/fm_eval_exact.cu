@@ -466,11 +466,18 @@ __global__ void __launch_bounds__(CT, MINB)
         for (int k = 0; k < D; ++k) bvsum += bj[k] * __ldg(v + (int64_t)nd.z * D + k);
       }
       if (my_node) {
-        const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
-        int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+        if ((unsigned)outw & CROSS_FLAG) {
+          // cross entries follow in the finishing pass: dense partial by tile node
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-          if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+          for (int k = 0; k < D; ++k)
+            a.partial[(int64_t)(tm.node_begin + tid) * D + k] = acc[k] - bj[k];
+        } else {
+          const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
+          int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+        }
       }
       ++j;
       comp.t += gridDim.x;  // every tile is visited (outputs), even without chunks
@@ -489,45 +496,42 @@ __global__ void __launch_bounds__(CT, MINB)
   }
 }
 
-// Finishing pass: a node's cross entries (elements owned by other tiles, the
-// tail of its sorted entry list) were written by their owner tiles into xbuf at
-// the entries' global indices; add them in ascending tile-element order.
+// Finishing pass: a node's cross entries (elements owned by other tiles) were
+// written by their owner tiles into xbuf at the node's dense exchange slots
+// [xbase[k], xbase[k + 1]) (consecutive nodes back to back); the tile kernel
+// left the node's own-element sum (minus b) in partial.  g = partial + the
+// cross entries in ascending tile-element order.
 template <int D>
-__global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn, const int4 *__restrict__ desc,
+__global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int32_t *__restrict__ xbase,
-                                                      const int32_t *__restrict__ xn,
+                                                      const int32_t *__restrict__ outw,
                                                       const double *__restrict__ xbuf,
+                                                      const double *__restrict__ partial,
                                                       double *__restrict__ g) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int n = xn[k];
-    if (!n) continue;
-    const int w = desc[k].w;
+  // one thread per (node, component): the D threads of a node read adjacent
+  // doubles of each exchange slot
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntn * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / D;
+    const int j = (int)(i - k * D);
+    const int lo = __ldg(xbase + k), hi = __ldg(xbase + k + 1);
+    if (hi == lo) continue;
+    const int w = __ldg(outw + k);
     const int mask = (unsigned)w >> OUT_MASK_SHIFT;
-    int o = w & ((1 << OUT_MASK_SHIFT) - 1);
-    const double *x = xbuf + (int64_t)xbase[k] * D;
-    double sum[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) sum[j] = 0.0;
-    for (int p = 0; p < n; ++p)  // the node's entries are contiguous: D doubles each
-#pragma unroll
-      for (int j = 0; j < D; ++j) sum[j] += __ldg(x + p * D + j);
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-      if (mask & (1 << j)) {
-        g[o] += sum[j];
-        ++o;
-      }
+    if (!(mask & (1 << j))) continue;
+    double sum = partial[i];
+    for (int p = lo; p < hi; ++p) sum += __ldg(xbuf + (int64_t)p * D + j);
+    g[(w & ((1 << OUT_MASK_SHIFT) - 1)) + __popc(mask & ((1 << j) - 1))] = sum;
   }
 }
 
-cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *desc, const int32_t *xbase,
-                                const int32_t *xn, const double *xbuf, double *g,
+cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
+                                const double *xbuf, const double *partial, double *g,
                                 cudaStream_t s) {
-  const int grid = (int)std::min<int64_t>((ntn + 255) / 256, 148 * 16);
-  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
-  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
-  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, desc, xbase, xn, xbuf, g);
+  const int grid = (int)std::min<int64_t>((ntn * d + 255) / 256, 148 * 32);
+  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
+  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
+  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
   return cudaGetLastError();
 }
 
