@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(CT, MINB)
     issue_records(iss, 1);
     iss.advance(a);
     uint32_t q = 0, j = 0;
+    int xp_t = -1, xp_c = 0, xp_b = 0, xp_e = 0;  // exchange range prefetched for the next chunk
 
     while (comp.valid(a)) {
       const TileMeta tm = comp.tm;
@@ -349,11 +350,30 @@ __global__ void __launch_bounds__(CT, MINB)
         const int s = q & 1;
         // cross items of this chunk: contributions of own elements to nodes of
         // other tiles, written to xbuf for the finishing pass
-        int xb = 0, xe = 0;  // (none in J-only orphan tiles)
-        if (comp.t < a.n_tiles) {
+        // (none in J-only orphan tiles).  Their range was prefetched one chunk
+        // ahead; the first item of each thread is loaded now, used after the
+        // first barrier.
+        int xb = 0, xe = 0;
+        if (comp.t == xp_t && c0 / CT == xp_c) {
+          xb = xp_b;
+          xe = xp_e;
+        } else if (comp.t < a.n_tiles) {
           const int xi = comp.t * (MAX_CHUNKS + 1) + c0 / CT;
           xb = __ldg(a.xchunk + xi);
           xe = __ldg(a.xchunk + xi + 1);
+        }
+        int xkey0 = 0, xpos0 = 0;
+        if (xb + tid < xe) {
+          xkey0 = __ldg(a.xkey + xb + tid);
+          xpos0 = __ldg(a.xpos + xb + tid);
+        }
+        xp_t = c0 + CT < ne_t ? comp.t : comp.t + (int)gridDim.x;
+        xp_c = c0 + CT < ne_t ? c0 / CT + 1 : 0;
+        xp_b = xp_e = 0;
+        if (xp_t < a.n_tiles) {
+          const int xi = xp_t * (MAX_CHUNKS + 1) + xp_c;
+          xp_b = __ldg(a.xchunk + xi);
+          xp_e = __ldg(a.xchunk + xi + 1);
         }
         TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
@@ -410,12 +430,6 @@ __global__ void __launch_bounds__(CT, MINB)
         // stage s is free: records of chunk q + 2
         issue_records(iss, s);
         iss.advance(a);
-        // first cross item of this thread (loads in flight during the consume)
-        int xkey0 = 0, xpos0 = 0;
-        if (xb + tid < xe) {
-          xkey0 = __ldg(a.xkey + xb + tid);
-          xpos0 = __ldg(a.xpos + xb + tid);
-        }
         if (my_node && !(mdl.dbg & 2)) {
           // this node's entries of the chunk: a known count, so the loads of
           // two entries are issued together; the order (ascending tile element)
