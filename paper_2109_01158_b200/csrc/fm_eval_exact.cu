@@ -588,7 +588,7 @@ static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, i
                                   const double *v, const double *b, double *g, double *jpart,
                                   double *bvpart, unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
-  if (DIM == 3 && ct == 128)
+  if (ct == 128)
     return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
   return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
 }

@@ -317,3 +317,36 @@ def test_field_stream_latches_inadmissible():
     fs.submit(bad.pin_memory(), g)
     with pytest.raises(fb.InadmissibleStateError):
         fs.synchronize()
+
+
+@pytest.mark.parametrize("kind,tiling", [
+    ("beam", (256, [4, 4, 4])), ("beam", (256, [2, 2, 2])), ("beam", (128, [4, 4, 2])),
+    ("beam", (256, [16, 8, 2])), ("rect", (256, [8, 8, 1])), ("rect", (128, [32, 4, 1])),
+    ("lshape", (256, [4, 4, 1]))])
+def test_tilings_vs_oracle(kind, tiling):
+    """The owner-computes exchange (cross entries, finishing pass, tiles with
+    few or no own elements) under tile shapes other than the default."""
+    if kind == "beam":
+        pr = problems.beam(12, 6, 6, seed=9, tiling=tiling)
+        om, omodel, b, v = O.problem_beam(12, 6, 6, seed=9)
+    elif kind == "rect":
+        pr = problems.rect(48, 24, seed=9, tiling=tiling)
+        om, omodel, b, v = O.problem_rect(48, 24, seed=9)
+    else:
+        pr = problems.lshape(4, 3.0, seed=9, tiling=tiling)
+        om, omodel, b, v = O.problem_lshape(4, 3.0, seed=9)
+    ref_p = O.build_patches(om)
+    bd = torch.from_numpy(b).cuda()
+    J = torch.empty(3, dtype=torch.float64, device="cuda")
+    gg = pr.dm.exact_gradient(pr.v, pr.model, bd, J=J).cpu().numpy()
+    pr.dm.check()
+    go = O.exact_gradient(v, om, ref_p, omodel, b)
+    assert _grel(gg, go) < G_TOL
+    assert _rel(float(J[0]), O.energy(v, om, omodel, b)[0]) < J_TOL
+    g2 = pr.dm.exact_gradient(pr.v, pr.model, bd).cpu().numpy()  # gradient only
+    assert np.array_equal(g2, gg)
+    eps = 1e-6 if kind == "lshape" else 1e-8
+    gn = pr.dm.numeric_gradient(pr.v, pr.model, bd, eps).cpu().numpy()
+    pr.dm.check()
+    gd, scale = O.numeric_gradient_direct(v, om, ref_p, omodel, b, eps)
+    assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
