@@ -269,7 +269,9 @@ def test_mid_size_vs_oracle(kind, size):
     gn = pr.dm.numeric_gradient(pr.v, pr.model, bd, eps).cpu().numpy()
     pr.dm.check()
     gd, scale = O.numeric_gradient_direct(v, om, ref_p, omodel, b, eps)
-    assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
+    ratio = np.abs(gn - gd) / (FD_FACTOR * scale + 1e-300)
+    assert ratio.max() <= 1.0, (ratio.max(), int(ratio.argmax()), gn[ratio.argmax()],
+                                gd[ratio.argmax()], int((ratio > 1).sum()))
 
 
 def test_determinism_bitwise():
@@ -325,13 +327,15 @@ def test_field_stream_latches_inadmissible():
     ("lshape", (256, [4, 4, 1]))])
 def test_tilings_vs_oracle(kind, tiling):
     """The owner-computes exchange (cross entries, finishing pass, tiles with
-    few or no own elements) under tile shapes other than the default."""
+    few or no own elements) under tile shapes other than the default.  Grid
+    widths are powers of two, so the GPU-built P1 gradients (closed form) and
+    the oracle's (LU inverse) agree bit for bit and the FD bound stays tight."""
     if kind == "beam":
-        pr = problems.beam(12, 6, 6, seed=9, tiling=tiling)
-        om, omodel, b, v = O.problem_beam(12, 6, 6, seed=9)
+        pr = problems.beam(16, 8, 8, seed=9, tiling=tiling)
+        om, omodel, b, v = O.problem_beam(16, 8, 8, seed=9)
     elif kind == "rect":
-        pr = problems.rect(48, 24, seed=9, tiling=tiling)
-        om, omodel, b, v = O.problem_rect(48, 24, seed=9)
+        pr = problems.rect(64, 32, seed=9, tiling=tiling)
+        om, omodel, b, v = O.problem_rect(64, 32, seed=9)
     else:
         pr = problems.lshape(4, 3.0, seed=9, tiling=tiling)
         om, omodel, b, v = O.problem_lshape(4, 3.0, seed=9)
@@ -349,4 +353,6 @@ def test_tilings_vs_oracle(kind, tiling):
     gn = pr.dm.numeric_gradient(pr.v, pr.model, bd, eps).cpu().numpy()
     pr.dm.check()
     gd, scale = O.numeric_gradient_direct(v, om, ref_p, omodel, b, eps)
-    assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
+    ratio = np.abs(gn - gd) / (FD_FACTOR * scale + 1e-300)
+    assert ratio.max() <= 1.0, (ratio.max(), int(ratio.argmax()), gn[ratio.argmax()],
+                                gd[ratio.argmax()], int((ratio > 1).sum()))
