@@ -357,9 +357,9 @@ __global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
 
 // first item of every chunk of every tile
 __global__ void k_xchunk(int n_tiles, int ct, int64_t X, const uint64_t *keys, int32_t *xchunk) {
-  const int n = n_tiles * (MAX_CHUNKS + 1);
+  const int n = n_tiles * XCH_STRIDE;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint64_t t = i / (MAX_CHUNKS + 1), ch = i % (MAX_CHUNKS + 1);
+    const uint64_t t = i / XCH_STRIDE, ch = min(i % XCH_STRIDE, MAX_CHUNKS);
     const uint64_t key = (t << 16) | ((ch * ct) << 2);
     int64_t lo = 0, hi = X;
     while (lo < hi) {
@@ -1224,7 +1224,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
     CK(dmalloc(&c->xkey, X + 8, &B));
     CK(dmalloc(&c->xpos, X + 8, &B));
-    CK(dmalloc(&c->xchunk, (size_t)n_tiles * (MAX_CHUNKS + 1), &B));
+    CK(dmalloc(&c->xchunk, (size_t)n_tiles * XCH_STRIDE, &B));
     CK(dmalloc(&c->xbuf, (size_t)(X + 8) * d, &B));
     // the finishing pass reads each node's exchange slots from its dense offset
     CK(cudaMemcpyAsync(c->node_xbase, xoff.p, (nfree + 1) * 4, cudaMemcpyDeviceToDevice, s));
@@ -1239,7 +1239,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
       CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));
     }
-    k_xchunk<<<grid_for((int64_t)n_tiles * (MAX_CHUNKS + 1), 256), 256, 0, s>>>(
+    k_xchunk<<<grid_for((int64_t)n_tiles * XCH_STRIDE, 256), 256, 0, s>>>(
         n_tiles, c->tile_nodes, X, dk.Current(), c->xchunk);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));

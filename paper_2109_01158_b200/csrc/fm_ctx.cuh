@@ -35,6 +35,7 @@ constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask <
 constexpr unsigned CROSS_FLAG = 1u << 31;  // node_desc.w: the node has cross entries
 constexpr int MAX_CHUNKS = 9;          // per-chunk entry counts in node_desc.x/.y (5 bits each)
 constexpr int ENTRY_OFF_MASK = (1 << 13) - 1;  // node_desc.x bits 0..12: tile-local entry offset
+constexpr int XCH_STRIDE = 12;  // ints per tile in xchunk (MAX_CHUNKS + 1, padded to 16 B)
 
 // entries of this node in chunk ch of its tile (node_desc packing, see k_node_desc)
 __device__ __forceinline__ int chunk_count(int4 nd, int ch) {
@@ -199,7 +200,7 @@ struct TileArgs {
   const int32_t *rank_of;      // node -> free rank or -1
   // cross-tile exchange of the fused exact kernel (elements computed once, by
   // their owner tile): items (owner te << 2 | slot) -> exchange slot, sorted by
-  // (owner tile, te); xchunk[t * (MAX_CHUNKS + 1) + c] = first item of chunk c
+  // (owner tile, te); xchunk[t * XCH_STRIDE + c] = first item of chunk c
   // of tile t; xbuf[slot * D + k] receives the contributions (slots are dense
   // and node-major: a node's cross entries are consecutive, in te order)
   const uint16_t *xkey;

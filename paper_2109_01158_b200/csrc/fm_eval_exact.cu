@@ -69,7 +69,7 @@ struct PipeLayout {
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
   __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int ns) {
     return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() + ents(entry_cap) +
-           ns * staging(D) + 32 * 8 + 8 * 8;
+           ns * staging(D) + 32 * 8 + 8 * 8 + XCH_STRIDE * 4;
   }
 };
 
@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(CT, MINB)
   unsigned char *stgx0 = reinterpret_cast<unsigned char *>(ents) + L::ents(a.entry_cap);
   auto stgx = [&](int k) { return reinterpret_cast<double *>(stgx0 + k * L::staging(D)); };
   double *red = reinterpret_cast<double *>(stgx0 + NS * L::staging(D));
+  int *xch = reinterpret_cast<int *>(red + 32 + 8);  // this tile's exchange-item chunk starts
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // record stages
   uint64_t *nfull = full + 2;                               // node-value buffers
   uint64_t *cfull = nfull + 2;                              // closure ids
@@ -283,7 +284,6 @@ __global__ void __launch_bounds__(CT, MINB)
     issue_records(iss, 1);
     iss.advance(a);
     uint32_t q = 0, j = 0;
-    int xp_t = -1, xp_c = 0, xp_b = 0, xp_e = 0;  // exchange range prefetched for the next chunk
 
     while (comp.valid(a)) {
       const TileMeta tm = comp.tm;
@@ -292,9 +292,11 @@ __global__ void __launch_bounds__(CT, MINB)
       if (tid == 0) {
         const uint32_t nb = (uint32_t)tm.node_count * 16;
         const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
-        mbar_arrive_expect_tx(tfull, nb + eb);
+        const uint32_t xb_ = comp.t < a.n_tiles ? XCH_STRIDE * 4 : 0;
+        mbar_arrive_expect_tx(tfull, nb + eb + xb_);
         if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
         if (eb) bulk_g2s(ents, a.entries + tm.entry_begin, eb, tfull);
+        if (xb_) bulk_g2s(xch, a.xchunk + (int64_t)comp.t * XCH_STRIDE, xb_, tfull);
         // L2 prefetch of the own records of a tile PF_TILES ahead (one bulk op):
         // keeps DRAM busy beyond the two shared-memory stages
         const int tp = comp.t + mdl.pf_tiles * gridDim.x;
@@ -350,30 +352,17 @@ __global__ void __launch_bounds__(CT, MINB)
         const int s = q & 1;
         // cross items of this chunk: contributions of own elements to nodes of
         // other tiles, written to xbuf for the finishing pass
-        // (none in J-only orphan tiles).  Their range was prefetched one chunk
-        // ahead; the first item of each thread is loaded now, used after the
-        // first barrier.
+        // (none in J-only orphan tiles); the first item of each thread is loaded
+        // now, used after the first barrier
         int xb = 0, xe = 0;
-        if (comp.t == xp_t && c0 / CT == xp_c) {
-          xb = xp_b;
-          xe = xp_e;
-        } else if (comp.t < a.n_tiles) {
-          const int xi = comp.t * (MAX_CHUNKS + 1) + c0 / CT;
-          xb = __ldg(a.xchunk + xi);
-          xe = __ldg(a.xchunk + xi + 1);
+        if (comp.t < a.n_tiles) {
+          xb = xch[c0 / CT];
+          xe = xch[c0 / CT + 1];
         }
         int xkey0 = 0, xpos0 = 0;
         if (xb + tid < xe) {
           xkey0 = __ldg(a.xkey + xb + tid);
           xpos0 = __ldg(a.xpos + xb + tid);
-        }
-        xp_t = c0 + CT < ne_t ? comp.t : comp.t + (int)gridDim.x;
-        xp_c = c0 + CT < ne_t ? c0 / CT + 1 : 0;
-        xp_b = xp_e = 0;
-        if (xp_t < a.n_tiles) {
-          const int xi = xp_t * (MAX_CHUNKS + 1) + xp_c;
-          xp_b = __ldg(a.xchunk + xi);
-          xp_e = __ldg(a.xchunk + xi + 1);
         }
         TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
