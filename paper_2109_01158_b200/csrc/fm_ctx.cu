@@ -325,6 +325,23 @@ __global__ void k_cross_count(int64_t ntn, const int32_t *tile_node_rank,
   }
 }
 
+// tile node -> index of its node id in the tile's sorted node closure
+__global__ void k_node_clo(int64_t ntn, const int32_t *tile_node_rank, const int32_t *tile_of_rank,
+                           const TileMeta *meta, const int4 *desc, const int32_t *closure,
+                           uint16_t *out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const TileMeta tm = meta[tile_of_rank[tile_node_rank[k]]];
+    const int node = desc[k].z;
+    int lo = 0, hi = tm.clo_count;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (closure[tm.clo_begin + mid] < node) lo = mid + 1; else hi = mid;
+    }
+    out[k] = (uint16_t)lo;
+  }
+}
+
 __global__ void k_mark_cross(int64_t ntn, const int32_t *xn, int4 *desc, int32_t *outw) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -1235,6 +1252,11 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     k_mark_cross<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->node_xn, c->node_desc,
                                                        c->node_outw);
     CK(cudaGetLastError());
+    CK(dmalloc(&c->node_clo, nfree + 8, &B));
+    k_node_clo<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(),
+                                                     c->meta, c->node_desc, c->closure,
+                                                     c->node_clo);
+    CK(cudaGetLastError());
     if (X) {
       k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
       CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));
@@ -1320,7 +1342,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
-                  c->partial};
+                  c->partial,   c->node_clo};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;

@@ -208,6 +208,7 @@ struct TileArgs {
   const int32_t *xchunk;
   double *xbuf;
   double *partial;             // tile node x D: own-element sums of nodes with cross entries
+  const uint16_t *node_clo;    // tile node -> its index in the tile's node closure
   int n_tiles;                 // node tiles
   int n_tiles_all;             // + orphan tiles (J only)
   int entry_cap;               // max entries of one tile, rounded up to 8
@@ -258,6 +259,7 @@ struct fm_ctx {
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
   double *xbuf = nullptr, *partial = nullptr;
   int32_t *node_outw = nullptr;  // per tile node: out offset | mask << 28
+  uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
   int64_t n_cross = 0;
   int32_t *fixed_nodes = nullptr;  // nodes without a free dof (b.v in the fused finalize)
   int64_t n_fixed_nodes = 0;
@@ -274,7 +276,7 @@ struct fm_ctx {
   fm::TileArgs tile_args() const {
     return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
                         loc,     closure, flags,   node_desc,       node_entries, rank_of,  xkey,
-                        xpos,    xchunk,  xbuf,            partial,   n_tiles,     n_tiles_all,
-                        entry_cap, clo_cap};
+                        xpos,    xchunk,  xbuf,            partial,   node_clo,    n_tiles,
+                        n_tiles_all, entry_cap, clo_cap};
   }
 };

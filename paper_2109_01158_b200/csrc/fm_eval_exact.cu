@@ -338,7 +338,9 @@ __global__ void __launch_bounds__(CT, MINB)
       double bj[D], acc[D];
 #pragma unroll
       for (int k = 0; k < D; ++k) acc[k] = bj[k] = 0.0;
+      int cl = 0;  // the node's index in this tile's closure (its v is in nv)
       if (my_node) {
+        cl = __ldg(a.node_clo + tm.node_begin + tid);
         nd = desc[tid];
         cur = nd.x & ENTRY_OFF_MASK;
         outw = nd.w;
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(CT, MINB)
       if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
       if (WJ && my_node && b) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) bvsum += bj[k] * __ldg(v + (int64_t)nd.z * D + k);
+        for (int k = 0; k < D; ++k) bvsum += bj[k] * nv[k * CAP + cl];
       }
       if (my_node) {
         if ((unsigned)outw & CROSS_FLAG) {
