@@ -1259,7 +1259,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaGetLastError());
     if (X) {
       k_low16<<<grid_for(X, 256), 256, 0, s>>>(X, dk.Current(), c->xkey);
-      CK(cudaMemcpyAsync(c->xpos, dv.Current(), X * 4, cudaMemcpyDeviceToDevice, s));
+      // the owner tiles write item i to xbuf slot i (coalesced); the finishing
+      // pass reads node-major slot p through xinv[p] = i
+      k_inverse<<<grid_for(X, 256), 256, 0, s>>>(X, dv.Current(), c->xpos);
+      CK(cudaGetLastError());
     }
     k_xchunk<<<grid_for((int64_t)n_tiles * XCH_STRIDE, 256), 256, 0, s>>>(
         n_tiles, c->tile_nodes, X, dk.Current(), c->xchunk);
@@ -1399,8 +1402,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     c->launches++;
   }
   if (c->n_cross > 0) {
-    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_xbase, c->node_outw, c->xbuf, c->partial,
-                                g, s));
+    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_xbase, c->node_outw, c->xpos, c->xbuf,
+                                c->partial, g, s));
     c->launches++;
   }
   if (wj) {  // b.v of the tile nodes came with the tile kernel's partials

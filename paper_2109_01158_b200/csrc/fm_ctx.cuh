@@ -204,7 +204,7 @@ struct TileArgs {
   // of tile t; xbuf[slot * D + k] receives the contributions (slots are dense
   // and node-major: a node's cross entries are consecutive, in te order)
   const uint16_t *xkey;
-  const int32_t *xpos;
+  const int32_t *xpos;          // node-major exchange slot -> item index (finishing pass)
   const int32_t *xchunk;
   double *xbuf;
   double *partial;             // tile node x D: own-element sums of nodes with cross entries

@@ -361,11 +361,8 @@ __global__ void __launch_bounds__(CT, MINB)
           xb = xch[c0 / CT];
           xe = xch[c0 / CT + 1];
         }
-        int xkey0 = 0, xpos0 = 0;
-        if (xb + tid < xe) {
-          xkey0 = __ldg(a.xkey + xb + tid);
-          xpos0 = __ldg(a.xpos + xb + tid);
-        }
+        int xkey0 = 0;
+        if (xb + tid < xe) xkey0 = __ldg(a.xkey + xb + tid);
         TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
         TRACE(1);
@@ -453,7 +450,7 @@ __global__ void __launch_bounds__(CT, MINB)
         }
         for (int i = xb + tid; i < xe; i += CT) {
           const int key = i == xb + tid ? xkey0 : (int)__ldg(a.xkey + i);
-          const int64_t pos = i == xb + tid ? xpos0 : __ldg(a.xpos + i);
+          const int64_t pos = i;  // item i -> exchange slot i (coalesced stores)
           const double *sp = stage_d + ((key >> 2) - c0) + (key & 3) * D * CT;
 #pragma unroll
           for (int k = 0; k < D; ++k) a.xbuf[pos * D + k] = sp[k * CT];
@@ -510,6 +507,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int32_t *__restrict__ xbase,
                                                       const int32_t *__restrict__ outw,
+                                                      const int32_t *__restrict__ xinv,
                                                       const double *__restrict__ xbuf,
                                                       const double *__restrict__ partial,
                                                       double *__restrict__ g) {
@@ -525,18 +523,18 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     const int mask = (unsigned)w >> OUT_MASK_SHIFT;
     if (!(mask & (1 << j))) continue;
     double sum = partial[i];
-    for (int p = lo; p < hi; ++p) sum += __ldg(xbuf + (int64_t)p * D + j);
+    for (int p = lo; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
     g[(w & ((1 << OUT_MASK_SHIFT) - 1)) + __popc(mask & ((1 << j) - 1))] = sum;
   }
 }
 
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
-                                const double *xbuf, const double *partial, double *g,
-                                cudaStream_t s) {
+                                const int32_t *xinv, const double *xbuf, const double *partial,
+                                double *g, cudaStream_t s) {
   const int grid = (int)std::min<int64_t>((ntn * d + 255) / 256, 148 * 32);
-  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
-  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
-  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xbuf, partial, g);
+  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
+  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
+  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
   return cudaGetLastError();
 }
 

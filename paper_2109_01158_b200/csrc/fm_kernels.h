@@ -16,8 +16,8 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
-                                const double *xbuf, const double *partial, double *g,
-                                cudaStream_t s);
+                                const int32_t *xinv, const double *xbuf, const double *partial,
+                                double *g, cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
