@@ -349,7 +349,7 @@ def main():
                        "l2": "inputs (3.3 GB per eval) larger than the 126 MB L2; no flush",
                        "tiles": {k: dm.stats[k] for k in (
                            "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
-                           "ctas_per_sm", "node_bufs", "stage_bufs", "entry_cap",
+                           "ctas_per_sm", "node_bufs", "stage_bufs", "entry_cap", "cross_entries",
                            "closure_cap")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

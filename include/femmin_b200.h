@@ -157,6 +157,7 @@ typedef struct {
   double redundancy;           /* tile element visits / ne                      */
   int32_t tile_threads, ctas_per_sm, node_bufs, stage_bufs;  /* tile-kernel launch shape */
   int32_t entry_cap, closure_cap;                            /* per-tile table capacities */
+  int64_t cross_entries;       /* node entries whose element another tile computes */
 } fm_ctx_stats;
 
 int fm_ctx_create(const fm_mesh_desc *desc, const fm_tiling *tiling, void *stream,

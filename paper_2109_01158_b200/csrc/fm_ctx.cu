@@ -1334,6 +1334,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   st.stage_bufs = c->stage_bufs;
   st.entry_cap = c->entry_cap;
   st.closure_cap = c->clo_cap;
+  st.cross_entries = c->n_cross;
   *out = c;
   return FM_OK;
 }
