@@ -353,7 +353,8 @@ def main():
                            "closure_cap")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_tile_exact<3,NH,J,256,1,1,2>", "kernel_ms": kms,
+                         "kernel": "k_tile_exact<3,NH,J,256,NB=%d,NS=%d,2>" % (
+                             dm.stats["node_bufs"], dm.stats["stage_bufs"]), "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": alg,
                          "bytes_per_elem": alg / dm.ne, "peak_source": peak_src,
                          "frac_of_8TBs_nominal": achieved / 8000.0,
