@@ -260,48 +260,59 @@ __global__ void __launch_bounds__(CT, 512 / CT)
     const int base = block_excl_scan<CT>(cnt, wsum, total);  // (its barriers publish rows)
     for (int k = 0; k < cnt; ++k) flat[base + k] = __ldg(a.entries + tm.entry_begin + cur + k);
     __syncthreads();
-    // ---- items (j, f): both signs of one perturbed row.  j is a compile-time
-    // constant of each pass (no selects between rows); the entry's slot l is
-    // not, so the record words of slot l are addressed directly.  Row j of F
-    // keeps the einsum order (p0+p2)+(p1+p3) [NV = 3: (p0+p2)+p1]: the pair
-    // holding p_l is (p_l + partner), the other pair is unperturbed, and IEEE
-    // addition is commutative, so only p_l depends on the sign.
+    // ---- items f (one entry: element row r, slot l), all D components and both
+    // signs.  The row's data (dphi, unperturbed F, closure indices) are read
+    // once per entry; j is a compile-time constant of each unrolled pass (no
+    // selects between rows), the slot l is not, so the words of slot l are
+    // addressed directly.  Row j of F keeps the einsum order (p0+p2)+(p1+p3)
+    // [NV = 3: (p0+p2)+p1]: the pair holding p_l is (p_l + partner), the other
+    // pair is unperturbed, and IEEE addition is commutative, so only p_l
+    // depends on the sign.
+    for (int f = tid; f < total; f += CT) {
+      const int en = flat[f];
+      const int r = (en >> 2) - c0, l = en & 3;
+      const unsigned char *rec = recs + r * FRB;
+      const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
+      const unsigned long long lw = *reinterpret_cast<const unsigned long long *>(rec + LW * 8);
+      auto gat = [&](int m, int k) { return rd[1 + m * NV + k]; };
+      double F0[D][DIM];
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      // thread tid takes the items i = j * total + f with i = tid (mod CT): the
-      // passes' remainders land on different threads
-      for (int f = (tid - j * total) & (CT - 1); f < total; f += CT) {
-        const int en = flat[f];
-        const int r = (en >> 2) - c0, l = en & 3;
-        const unsigned char *rec = recs + r * FRB;
-        const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
-        const unsigned long long lw = *reinterpret_cast<const unsigned long long *>(rec + LW * 8);
-        auto vat = [&](int k) { return nodev[j * CAP + (int)((lw >> (16 * k)) & 0xffffull)]; };
-        auto gat = [&](int m, int k) { return rd[1 + m * NV + k]; };
-        double F[D][DIM];
+      for (int jj = 0; jj < D; ++jj)
 #pragma unroll
-        for (int jj = 0; jj < D; ++jj)
+        for (int m = 0; m < DIM; ++m) F0[jj][m] = Fb[r * NF + jj * DIM + m];
+      int lp, la = 0, lb = 0;
+      if constexpr (NV == 4) {
+        lp = l ^ 2;
+        la = (l + 1) & 3;
+        lb = (l + 3) & 3;
+      } else {
+        lp = l == 1 ? 0 : 2 - l;
+        la = l == 1 ? 2 : 1;
+      }
+      double gl[DIM];
 #pragma unroll
-          for (int m = 0; m < DIM; ++m) F[jj][m] = jj == j ? 0.0 : Fb[r * NF + jj * DIM + m];
-        const double vl = vat(l);
-        double gl[DIM], q1[DIM], q2[DIM];
+      for (int m = 0; m < DIM; ++m) gl[m] = gat(m, l);
+      const int cl = (int)((lw >> (16 * l)) & 0xffffull), cp = (int)((lw >> (16 * lp)) & 0xffffull);
+      const int ca = (int)((lw >> (16 * la)) & 0xffffull), cb = (int)((lw >> (16 * lb)) & 0xffffull);
+      const double vol = rd[0];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double *nvj = nodev + j * CAP;
+        const double vl = nvj[cl];
+        double q1[DIM], q2[DIM];
         if constexpr (NV == 4) {
-          const int lp = l ^ 2, la = (l + 1) & 3, lb = (l + 3) & 3;
-          const double vp = vat(lp), va = vat(la), vb = vat(lb);
+          const double vp = nvj[cp], va = nvj[ca], vb = nvj[cb];
 #pragma unroll
           for (int m = 0; m < DIM; ++m) {
-            gl[m] = gat(m, l);
             q1[m] = rmul(vp, gat(m, lp));                               // partner of p_l
             q2[m] = radd(rmul(va, gat(m, la)), rmul(vb, gat(m, lb)));  // the other pair
           }
         } else {
-          const int lp = l == 1 ? 0 : 2 - l, lo = l == 1 ? 2 : 1;
-          const double vp = vat(lp), vo = vat(lo);
+          const double vp = nvj[cp], vo = nvj[ca];
 #pragma unroll
           for (int m = 0; m < DIM; ++m) {
-            gl[m] = gat(m, l);
             q1[m] = rmul(vp, gat(m, lp));
-            q2[m] = rmul(vo, gat(m, lo));
+            q2[m] = rmul(vo, gat(m, la));
           }
         }
         double w[2];
@@ -312,7 +323,7 @@ __global__ void __launch_bounds__(CT, 512 / CT)
 #pragma unroll
           for (int jj = 0; jj < D; ++jj)
 #pragma unroll
-            for (int m = 0; m < DIM; ++m) Fp[jj][m] = F[jj][m];
+            for (int m = 0; m < DIM; ++m) Fp[jj][m] = F0[jj][m];
 #pragma unroll
           for (int m = 0; m < DIM; ++m) {
             const double pl = rmul(ve, gl[m]);
@@ -324,8 +335,7 @@ __global__ void __launch_bounds__(CT, 512 / CT)
           }
           const double W = density<DIM, MODEL>(Fp, mdl);
           if (!isfinite(W)) {
-            const int node =
-                __ldg(a.closure + tm.clo_begin + (int)((lw >> (16 * l)) & 0xffffull));
+            const int node = __ldg(a.closure + tm.clo_begin + cl);
             const int te = r + c0;
             const int64_t s = te < tm.own_count
                                   ? (int64_t)tm.own_begin + te
@@ -336,7 +346,7 @@ __global__ void __launch_bounds__(CT, 512 / CT)
                                            (unsigned long long)__ldg(a.s2o + s);
             mykey = key < mykey ? key : mykey;
           }
-          w[sg] = rmul(rd[0], W);
+          w[sg] = rmul(vol, W);
         }
         stg[j * ech + f] = make_double2(w[0], w[1]);
       }
