@@ -349,12 +349,12 @@ def main():
                        "l2": "inputs (3.3 GB per eval) larger than the 126 MB L2; no flush",
                        "tiles": {k: dm.stats[k] for k in (
                            "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
-                           "ctas_per_sm", "node_bufs", "stage_bufs", "entry_cap", "cross_entries",
+                           "ctas_per_sm", "node_bufs", "table_bufs", "entry_cap", "cross_entries",
                            "closure_cap")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_tile_exact<3,NH,J,256,NB=%d,NS=%d,2>" % (
-                             dm.stats["node_bufs"], dm.stats["stage_bufs"]), "kernel_ms": kms,
+                         "kernel": "k_tile_exact<3,NH,J,256,NB=%d,TB=%d,2>" % (
+                             dm.stats["node_bufs"], dm.stats["table_bufs"]), "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": alg,
                          "bytes_per_elem": alg / dm.ne, "peak_source": peak_src,
                          "frac_of_8TBs_nominal": achieved / 8000.0,

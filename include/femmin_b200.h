@@ -155,7 +155,7 @@ typedef struct {
   int64_t n_tiles, n_orphan_tiles, tile_elems_total, node_entries_total;
   int64_t max_tile_elems, max_tile_entries, bytes_device;
   double redundancy;           /* tile element visits / ne                      */
-  int32_t tile_threads, ctas_per_sm, node_bufs, stage_bufs;  /* tile-kernel launch shape */
+  int32_t tile_threads, ctas_per_sm, node_bufs, table_bufs;  /* tile-kernel launch shape */
   int32_t entry_cap, closure_cap;                            /* per-tile table capacities */
   int64_t cross_entries;       /* node entries whose element another tile computes */
 } fm_ctx_stats;

@@ -41,7 +41,7 @@ class FmCtxStats(C.Structure):
                 ("node_entries_total", i64), ("max_tile_elems", i64),
                 ("max_tile_entries", i64), ("bytes_device", i64), ("redundancy", dbl),
                 ("tile_threads", i32), ("ctas_per_sm", i32), ("node_bufs", i32),
-                ("stage_bufs", i32), ("entry_cap", i32), ("closure_cap", i32),
+                ("table_bufs", i32), ("entry_cap", i32), ("closure_cap", i32),
                 ("cross_entries", i64)]
 
 

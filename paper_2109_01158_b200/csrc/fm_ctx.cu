@@ -1275,30 +1275,30 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   // buffers (one tile of lead) when that does not cost a CTA
   {
     const int regs_cap = c->tile_nodes == 128 ? 4 : 2;
-    auto fit = [&](int nb, int ns) {
-      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb, ns);
+    auto fit = [&](int nb, int tb) {
+      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb, tb);
       return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));
     };
-    // most CTAs per SM first, then one barrier per chunk (ns = 2), then a tile
-    // of node-value lead (nb = 2); FM_TILE_CFG="nb,ns" forces a variant
+    // most CTAs per SM first, then the next tile's node values a tile ahead
+    // (nb = 2), then its tables (tb = 2); FM_TILE_CFG="nb,tb" forces a variant
     int best = -1;
     for (int nb = 2; nb >= 1; --nb)
-      for (int ns = 2; ns >= 1; --ns) {
-        const int f = fit(nb, ns);
-        const int score = f * 4 + (ns == 2) * 2 + (nb == 2);
+      for (int tb = 2; tb >= 1; --tb) {
+        const int f = fit(nb, tb);
+        const int score = f * 4 + (nb == 2) * 2 + (tb == 2);
         if (f > 0 && score > best) {
           best = score;
           c->node_bufs = nb;
-          c->stage_bufs = ns;
+          c->table_bufs = tb;
           c->ctas_per_sm = f;
         }
       }
     if (const char *e = getenv("FM_TILE_CFG")) {
-      int nb = 0, ns = 0;
-      if (sscanf(e, "%d,%d", &nb, &ns) == 2 && fit(nb, ns) > 0) {
+      int nb = 0, tb = 0;
+      if (sscanf(e, "%d,%d", &nb, &tb) == 2 && fit(nb, tb) > 0) {
         c->node_bufs = nb;
-        c->stage_bufs = ns;
-        c->ctas_per_sm = fit(nb, ns);
+        c->table_bufs = tb;
+        c->ctas_per_sm = fit(nb, tb);
       }
     }
     if (best < 0) {
@@ -1331,7 +1331,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   st.tile_threads = c->tile_nodes;
   st.ctas_per_sm = c->ctas_per_sm;
   st.node_bufs = c->node_bufs;
-  st.stage_bufs = c->stage_bufs;
+  st.table_bufs = c->table_bufs;
   st.entry_cap = c->entry_cap;
   st.closure_cap = c->clo_cap;
   st.cross_entries = c->n_cross;
@@ -1398,7 +1398,7 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
     FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
-                              c->stage_bufs, wj, v, b, g, c->jpart, c->dotpart, c->status, ma,
+                              c->table_bufs, wj, v, b, g, c->jpart, c->dotpart, c->status, ma,
                               s));
     c->launches++;
   }

@@ -242,7 +242,7 @@ struct fm_ctx {
   int64_t n_tile_elems = 0, n_node_entries = 0;
   int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, clo_cap = 0;
   int chunk_entry_cap = 0;  // max node entries of one chunk of one tile (FD staging)
-  int n_sm = 148, ctas_per_sm = 2, node_bufs = 2, stage_bufs = 2;
+  int n_sm = 148, ctas_per_sm = 2, node_bufs = 2, table_bufs = 2;
   uint8_t *aos = nullptr;
   int4 *conn4 = nullptr;
   fm::TileMeta *meta = nullptr;

@@ -67,9 +67,11 @@ struct PipeLayout {
   __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
   __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
-  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int ns) {
-    return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() + ents(entry_cap) +
-           ns * staging(D) + 32 * 8 + 8 * 8 + XCH_STRIDE * 4;
+  // nb node-value buffers; tb buffers of entries + chunk starts (2: the next
+  // tile's tables load during this tile)
+  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int tb) {
+    return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() +
+           tb * (ents(entry_cap) + XCH_STRIDE * 4) + staging(D) + 32 * 8 + 8 * 8;
   }
 };
 
@@ -183,7 +185,7 @@ struct Cursor {
   }
 };
 
-template <int DIM, int MODEL, bool WJ, int CT, int NB, int NS, int MINB>
+template <int DIM, int MODEL, bool WJ, int CT, int NB, int TB, int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, double *__restrict__ bvpart,
@@ -202,15 +204,19 @@ __global__ void __launch_bounds__(CT, MINB)
   };
   int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * L::stage() + NB * L::nodev(D, CAP));
   int4 *desc = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(cids) + L::cids(CAP));
-  uint16_t *ents = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(desc) + L::desc());
-  unsigned char *stgx0 = reinterpret_cast<unsigned char *>(ents) + L::ents(a.entry_cap);
-  auto stgx = [&](int k) { return reinterpret_cast<double *>(stgx0 + k * L::staging(D)); };
-  double *red = reinterpret_cast<double *>(stgx0 + NS * L::staging(D));
-  int *xch = reinterpret_cast<int *>(red + 32 + 8);  // this tile's exchange-item chunk starts
+  unsigned char *tabs0 = reinterpret_cast<unsigned char *>(desc) + L::desc();
+  const size_t tabsz = L::ents(a.entry_cap) + XCH_STRIDE * 4;
+  auto ents_of = [&](int k) { return reinterpret_cast<uint16_t *>(tabs0 + k * tabsz); };
+  auto xch_of = [&](int k) {  // the tile's exchange-item chunk starts
+    return reinterpret_cast<int *>(tabs0 + k * tabsz + L::ents(a.entry_cap));
+  };
+  double *stage_d = reinterpret_cast<double *>(tabs0 + TB * tabsz);
+  double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stage_d) +
+                                           L::staging(D));
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // record stages
   uint64_t *nfull = full + 2;                               // node-value buffers
   uint64_t *cfull = nfull + 2;                              // closure ids
-  uint64_t *tfull = cfull + 1;                              // descriptors + entries
+  uint64_t *tfull = cfull + 1;                              // tables (x TB)
   const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(full, 1);
@@ -219,6 +225,7 @@ __global__ void __launch_bounds__(CT, MINB)
     mbar_init(nfull + 1, CT);
     mbar_init(cfull, 1);
     mbar_init(tfull, 1);
+    mbar_init(tfull + 1, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -230,6 +237,18 @@ __global__ void __launch_bounds__(CT, MINB)
       mbar_arrive_expect_tx(cfull, bytes);
       bulk_g2s(cids, a.closure + tm.clo_begin, bytes, cfull);
     }
+  };
+  // descriptors, entries and exchange chunk starts of tile t -> table buffer k
+  auto issue_tables = [&](int t, int k) {
+    if (tid != 0 || t >= a.n_tiles_all) return;
+    const TileMeta tm = a.meta[t];
+    const uint32_t nb = (uint32_t)tm.node_count * 16;
+    const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
+    const uint32_t xb_ = t < a.n_tiles ? XCH_STRIDE * 4 : 0;
+    mbar_arrive_expect_tx(tfull + k, nb + eb + xb_);
+    if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull + k);
+    if (eb) bulk_g2s(ents_of(k), a.entries + tm.entry_begin, eb, tfull + k);
+    if (xb_) bulk_g2s(xch_of(k), a.xchunk + (int64_t)t * XCH_STRIDE, xb_, tfull + k);
   };
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
     double *dst = nodev(k);
@@ -265,7 +284,9 @@ __global__ void __launch_bounds__(CT, MINB)
   Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}};
   comp.load(a);
   if (comp.valid(a)) {
-    // ---- prologue: closure ids (+ node values with NB = 2) and chunk 0 records
+    // ---- prologue: tables (TB = 2), closure ids (+ node values with NB = 2),
+    // chunk 0 and 1 records
+    if (TB == 2) issue_tables(comp.t, 0);
     issue_clo(comp.t);
     if (NB == 2) {
       mbar_wait(cfull, 0);
@@ -288,24 +309,9 @@ __global__ void __launch_bounds__(CT, MINB)
     while (comp.valid(a)) {
       const TileMeta tm = comp.tm;
       TRACE(6);
-      // ---- tile start: descriptors + entries (single buffer: previous tile done)
-      if (tid == 0) {
-        const uint32_t nb = (uint32_t)tm.node_count * 16;
-        const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
-        const uint32_t xb_ = comp.t < a.n_tiles ? XCH_STRIDE * 4 : 0;
-        mbar_arrive_expect_tx(tfull, nb + eb + xb_);
-        if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull);
-        if (eb) bulk_g2s(ents, a.entries + tm.entry_begin, eb, tfull);
-        if (xb_) bulk_g2s(xch, a.xchunk + (int64_t)comp.t * XCH_STRIDE, xb_, tfull);
-        // L2 prefetch of the own records of a tile PF_TILES ahead (one bulk op):
-        // keeps DRAM busy beyond the two shared-memory stages
-        const int tp = comp.t + mdl.pf_tiles * gridDim.x;
-        if (mdl.pf_tiles > 0 && tp < a.n_tiles_all) {
-          const TileMeta tq = a.meta[tp];
-          if (tq.own_count)
-            bulk_prefetch_l2(a.aos + (int64_t)tq.own_begin * RB, (uint32_t)tq.own_count * RB);
-        }
-      }
+      // ---- tile start: with TB = 1 the tables load now (previous tile done)
+      const int tb = TB == 2 ? (int)(j & 1) : 0;
+      if (TB == 1) issue_tables(comp.t, 0);
       const double *nv;
       if (NB == 2) {
         // node values of the NEXT tile (one tile of lead), then its successor's ids
@@ -329,8 +335,10 @@ __global__ void __launch_bounds__(CT, MINB)
         issue_clo(comp.t + gridDim.x);
         nv = nodev(0);
       }
-      mbar_wait(tfull, j & 1);
+      mbar_wait(tfull + tb, TB == 2 ? (j >> 1) & 1 : j & 1);
       TRACE(7);
+      const uint16_t *ents = ents_of(tb);
+      const int *xch = xch_of(tb);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
       int cur = 0, outw = 0;
@@ -348,6 +356,10 @@ __global__ void __launch_bounds__(CT, MINB)
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
         }
+      }
+      if (TB == 2) {
+        __syncthreads();  // every descriptor read: the next tile's tables load now
+        issue_tables(comp.t + gridDim.x, tb ^ 1);
       }
       const int ne_t = comp.ne;
       for (int c0 = 0; c0 < ne_t; c0 += CT, ++q) {
@@ -400,7 +412,6 @@ __global__ void __launch_bounds__(CT, MINB)
         }
         // contributions -> staging buffer (separate from the record stages, so
         // the TMA engine never overwrites generic-proxy writes: no proxy fence)
-        double *stage_d = stgx(NS == 2 ? (q & 1) : 0);
         if (valid && has_nodes) {
 #pragma unroll
           for (int l = 0; l < NV; ++l)
@@ -459,10 +470,9 @@ __global__ void __launch_bounds__(CT, MINB)
         // it; two: the next chunk's barrier already orders this consumption
         // before the write two chunks ahead
         TRACE(4);
-        if (NS == 1) __syncthreads();
+        __syncthreads();
         TRACE(5);
       }
-      if (NS == 2) __syncthreads();  // entries / descriptors consumed before the refill
       if (WJ && my_node && b) {
 #pragma unroll
         for (int k = 0; k < D; ++k) bvsum += bj[k] * nv[k * CAP + cl];
@@ -538,23 +548,23 @@ cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const 
   return cudaGetLastError();
 }
 
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns) {
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int tb) {
   if (ct == 128)
-    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb, ns)
-                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb, ns);
-  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb, ns)
-                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb, ns);
+    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb, tb)
+                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb, tb);
+  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb, tb)
+                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb, tb);
 }
 
-template <int DIM, int MODEL, int CT, int NB, int NS>
+template <int DIM, int MODEL, int CT, int NB, int TB>
 static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double *v,
                               const double *b, double *g, double *jpart, double *bvpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int MINB = CT == 128 ? 4 : 2;  // <= 128 registers per thread
-  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB, NS);
-  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, NS, MINB>
-              : k_tile_exact<DIM, MODEL, false, CT, NB, NS, MINB>;
+  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB, TB);
+  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, TB, MINB>
+              : k_tile_exact<DIM, MODEL, false, CT, NB, TB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, bvpart, status, m);
   return cudaGetLastError();

@@ -10,15 +10,15 @@ namespace fm {
 
 // persistent pipelined fused J + exact gradient; grid = ctas_per_sm * #SMs, CONSUMERS threads
 // ct = threads per CTA = chunk size = max tile nodes (128 or 256); nb = node-value buffers
-// ns = staging buffers (2: one barrier per chunk, 1: two)
+// tb = table buffers (2: the next tile's descriptors / entries load a tile ahead)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
-                              int ns, bool wj, const double *v, const double *b, double *g,
+                              int tb, bool wj, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
                                 const int32_t *xinv, const double *xbuf, const double *partial,
                                 double *g, cudaStream_t s);
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int ns);
+size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int tb);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
                            const double *v, const double *b, double eps, double *g,
