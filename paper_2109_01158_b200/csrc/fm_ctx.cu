@@ -612,11 +612,6 @@ static ModelArgs model_args(const fm_model *m) {
     return e ? atoi(e) : 0;
   }();
   a.dbg = ablate;
-  static const int pf = [] {
-    const char *e = getenv("FM_PF_TILES");
-    return e ? atoi(e) : 0;  // measured: lead 1 costs ~2.5% at config 4
-  }();
-  a.pf_tiles = pf;
   return a;
 }
 

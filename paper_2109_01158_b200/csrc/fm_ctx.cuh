@@ -169,9 +169,8 @@ struct ModelArgs {
   // (ndarray ** scalar: 0.5 -> sqrt, 1 -> copy, 2 -> square, -1 -> reciprocal)
   double e_w, e_dw;  // p/2 and (p-2)/2
   int dbg;           // profiling ablations of the tile kernel (FM_TILE_ABLATE, tools/ablate.py:
-                     // 1 no constitutive, 2 no consume, 8 no compute, 16 no halo rows,
-                     // 32 no closure gathers; results are wrong on purpose), 0 = off
-  int pf_tiles;      // tiles of L2 prefetch lead for own records (FM_PF_TILES, default 1)
+                     // 1 no constitutive, 2 no consume, 8 no compute, 32 no closure
+                     // gathers; results are wrong on purpose), 0 = off
 };
 
 __device__ __forceinline__ double np_scalar_pow(double x, double e) {

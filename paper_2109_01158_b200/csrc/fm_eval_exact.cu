@@ -1,29 +1,32 @@
 // Fused energy + exact gradient (gradients.py:124-149 with assembly.py:94-106)
-// as one persistent, pipelined kernel; several CT-thread CTAs per SM.
+// as one persistent, pipelined kernel; two 256-thread CTAs per SM.
 //
 // Each CTA walks its node tiles (t = blockIdx.x, += gridDim.x; tiles are in
-// Morton order of their spatial boxes so concurrently running CTAs share halo
-// elements through L2).  Per tile (<= CT free nodes, one node per thread):
-//   node values   the tile's node closure (sorted distinct nodes of all its
-//                 elements) is gathered ONCE into shared memory (8-byte
-//                 LDGSTS; with NB = 2 buffers one tile ahead); elements address
-//                 it with 16-bit closure indices, so no per-element global
-//                 gathers of v remain.
-//   records       chunks of CT elements, double-buffered: the own elements are
-//                 a contiguous storage range -> one 1D bulk copy (TMA engine,
-//                 mbarrier complete_tx); halo records -> 16-byte LDGSTS by the
-//                 thread that owns the row.  Records are 112 B (3D) / 80 B (2D):
-//                 an odd number of 16-B chunks, so row-per-lane reads are
-//                 bank-conflict free without swizzling.
+// Morton order of their spatial boxes).  Every element is computed ONCE, by
+// its owner tile (the tile of its first free node).  Per tile (<= CT free
+// nodes, one node per thread):
+//   tables        descriptors, entries and the exchange-item chunk starts by
+//                 bulk copy (TB = 2: a tile ahead).
+//   node values   the tile's node closure (sorted distinct nodes of its
+//                 elements) gathered ONCE into shared memory (8-byte LDGSTS;
+//                 NB = 2: a tile ahead); elements address it with 16-bit
+//                 closure indices, so no per-element global gathers of v.
+//   records       the own elements, chunks of CT, double-buffered and issued
+//                 two chunks ahead: one 1D bulk copy (TMA engine, mbarrier
+//                 complete_tx) for the records (80 B 3D / 48 B 2D: an odd
+//                 number of 16-B chunks, so row-per-lane reads are bank-
+//                 conflict free) and one for their closure indices.
 //   compute       thread c: F = grad v, P' = vol * dW/dF = a F + b cof, the
-//                 contributions P' . grad phi_l of its local nodes, vol * W when
-//                 the tile owns the element; contributions are staged over the
-//                 (consumed) record buffer.
-//   assemble      node threads consume this chunk's entries (sorted by tile
-//                 element) into registers: fixed summation order, no
-//                 floating-point atomics.
+//                 contributions P' . grad phi_l of its 4 (3) nodes, vol * W;
+//                 contributions staged [slot][comp][row].
+//   assemble      node threads add this chunk's entries of their own tile's
+//                 elements (sorted by tile element; fixed order, no atomics);
+//                 entries whose node belongs to another tile ("cross") are
+//                 stored to the exchange buffer (coalesced: slots in owner-tile
+//                 item order) and added by k_finish_cross.
 // J: per-thread partials over a static tile assignment -> fixed block tree ->
-// one partial per CTA, reduced in CTA order by k_finalize.
+// one partial per CTA (vol * W, and b.v of the tile nodes from the closure
+// values), reduced in CTA order by k_finalize_tiles.
 #include "fm_density.cuh"
 #include "fm_kernels.h"
 #include "fm_pipe.cuh"
