@@ -186,7 +186,41 @@ def case_small_shapes():
     save("lshape_meshes", **out)
 
 
+def case_minimize():
+    """The reference minimizers (solver.py) on its unit-test fixture
+    lshape_problem(1): p-Laplace p = 3 (trust region and L-BFGS) and p = 2
+    (against the direct Poisson solve), f = -10, v0 = 0."""
+    from femmin.solver import SolveOptions, minimize
+    m = bench.lshape_problem(1)
+    pt = femmin.build_patches(m)
+    out = {}
+    for p in (3.0, 2.0):
+        model = PLaplacian(PLaplaceParams(p=p), dim=2)
+        load = LinearLoad.assemble(m, -10.0, d=1)
+
+        def J(v):
+            return energy(v, m, model, load)[0]
+
+        def g(v):
+            return exact_gradient(v, m, pt, model, load)
+
+        res = minimize(J, g, np.zeros(m.nn), m.dofs_minim, SolveOptions())
+        tag = f"p{p:g}"
+        out.update({f"tr_u_{tag}": res.u, f"tr_J_{tag}": np.float64(res.J_u),
+                    f"tr_iters_{tag}": np.int64(res.iters),
+                    f"tr_ngrad_{tag}": np.int64(res.n_grad),
+                    f"tr_status_{tag}": np.array(res.status)})
+        if p == 3.0:
+            lb = minimize(J, g, np.zeros(m.nn), m.dofs_minim,
+                          SolveOptions(solver="lbfgs", tol_g=1e-8, tol_f=1e-12, tol_step=1e-8))
+            out.update({"lbfgs_u_p3": lb.u, "lbfgs_J_p3": np.float64(lb.J_u)})
+    out["direct_J_p2"] = np.float64(bench.poisson_solve_energy(m, f=-10.0)[1])
+    out["b"] = LinearLoad.assemble(m, -10.0, d=1).b
+    save("minimize_lshape1", **out)
+
+
 if __name__ == "__main__":
+    case_minimize()
     case_small_shapes()
     case_lshape1_tests()
     case_lshape(4, 3.0, 2109, "cfg1_lshape4_p3")
