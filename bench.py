@@ -263,9 +263,25 @@ def main():
             return a0.elapsed_time(a1) / n
         e_ms = timed(lambda: dm.energy(v, model, b, out=J), 20)
         fd_ms = timed(lambda: dm.numeric_gradient(v, model, b, 1e-8, g=torch.empty_like(g)), 3)
+        go_ms = timed(lambda: dm.exact_gradient(v, model, b, g=g), 20)
         extras = {"energy_only_ms": e_ms, "energy_only_Melem_s": ne_total / e_ms / 1e3,
-                  "fd_grad_ms": fd_ms, "fd_grad_Melem_s": ne_total / fd_ms / 1e3}
+                  "fd_grad_ms": fd_ms, "fd_grad_Melem_s": ne_total / fd_ms / 1e3,
+                  "grad_only_ms": go_ms,
+                  "fd_W_evals_per_s": 2 * dm.d * dm.stats["node_entries_total"] / (fd_ms * 1e-3)}
         dm.check()
+        if "dofs_minim" in pr.meta:
+            # a few trust-region iterations of the device-resident minimizer
+            # from the benchmark field: wall time per
+            # gradient call (each CG step is one Hessian-vector product = 2)
+            from paper_2109_01158_b200.solver import SolveOptions, minimize_device
+            minimize_device(dm, model, b, v, pr.meta["dofs_minim"],  # warm-up (module loads)
+                            SolveOptions(max_iters=1, max_cg=2))
+            res = minimize_device(dm, model, b, v, pr.meta["dofs_minim"],
+                                  SolveOptions(max_iters=3, max_cg=20))
+            extras.update({"tr_3iters_s": res.time, "tr_grad_calls": res.n_grad,
+                           "tr_energy_calls": res.n_energy,
+                           "tr_ms_per_grad_call": res.time / max(1, res.n_grad) * 1e3,
+                           "tr_J_start_end": [float(dm.energy(v, model, b)[0]), res.J_u]})
 
     # ---- end to end through the public device API, host buffers ----------
     v_host = v.cpu().pin_memory()

@@ -290,10 +290,11 @@ def minimize_device(dm, model, b, v0: torch.Tensor, dofs_minim: torch.Tensor,
     template = v0.detach().to(torch.float64).clone()
     dofs = dofs_minim.to(device=template.device, dtype=torch.int64)
     J3 = torch.empty(3, dtype=torch.float64, device=template.device)
+    work = template.clone()  # full field the kernels read; only free dofs are rewritten
     count = {"f": 0, "g": 0}
 
     def embed(x):
-        return template.index_copy(0, dofs, x)
+        return work.index_copy_(0, dofs, x)
 
     def fx(x):
         count["f"] += 1
@@ -308,7 +309,7 @@ def minimize_device(dm, model, b, v0: torch.Tensor, dofs_minim: torch.Tensor,
     t0 = time.perf_counter()
     x, f, it, gn, conv, status = _run(fx, gx, template.index_select(0, dofs), opts)
     torch.cuda.synchronize()
-    return MinimizeResult(u=embed(x), J_u=f, iters=it, grad_norm=gn,
+    return MinimizeResult(u=template.index_copy(0, dofs, x), J_u=f, iters=it, grad_norm=gn,
                           time=time.perf_counter() - t0, converged=conv, status=status,
                           n_energy=count["f"], n_grad=count["g"])
 
