@@ -395,7 +395,7 @@ __global__ void k_low16(int64_t n, const uint64_t *k, uint16_t *o) {
 
 // max over (tile, chunk) of the node entries falling in that chunk
 __global__ void k_chunk_entry_max(int n_tiles, const TileMeta *meta, const int4 *desc,
-                                  unsigned int *out) {
+                                  unsigned int *out, int32_t *per_chunk) {
   __shared__ unsigned int cnt[MAX_CHUNKS];
   const int t = blockIdx.x;
   if (threadIdx.x < MAX_CHUNKS) cnt[threadIdx.x] = 0;
@@ -406,7 +406,50 @@ __global__ void k_chunk_entry_max(int n_tiles, const TileMeta *meta, const int4 
     for (int ch = 0; ch < MAX_CHUNKS; ++ch) atomicAdd(&cnt[ch], (unsigned)chunk_count(nd, ch));
   }
   __syncthreads();
-  if (threadIdx.x < MAX_CHUNKS) atomicMax(out, cnt[threadIdx.x]);
+  if (threadIdx.x < MAX_CHUNKS) {
+    atomicMax(out, cnt[threadIdx.x]);
+    per_chunk[t * MAX_CHUNKS + threadIdx.x] = (int32_t)cnt[threadIdx.x];
+  }
+}
+
+// Chunk-major entry blocks: one CTA per tile, thread per node; per chunk a
+// block scan of the nodes' counts gives the header offsets, then each node
+// copies its entries of the chunk (they are contiguous in its te-sorted list).
+__global__ void k_chunk_blocks(int n_tiles, const TileMeta *meta, const int4 *desc,
+                               const uint16_t *entries, int ct, uint16_t *blocks) {
+  __shared__ int wsum[32];
+  const int t = blockIdx.x;
+  const TileMeta tm = meta[t];
+  const int nch = (tm.own_count + tm.halo_count + ct - 1) / ct;
+  const int k = threadIdx.x;  // blockDim.x >= node_count (<= 256)
+  const bool my = k < tm.node_count;
+  const int4 nd = my ? desc[tm.node_begin + k] : make_int4(0, 0, 0, 0);
+  int cur = nd.x & ENTRY_OFF_MASK;
+  const int H = blk_header(tm.node_count);
+  const int lane = k & 31, w = k >> 5, nw = blockDim.x >> 5;
+  for (int ch = 0; ch < nch; ++ch) {
+    uint16_t *blk = blocks + tm.blk_base + (int64_t)ch * tm.blk_stride;
+    const int cnt = my ? chunk_count(nd, ch) : 0;
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int u = 0; u < w; ++u) before += wsum[u];
+    int total = 0;
+    for (int u = 0; u < nw; ++u) total += wsum[u];
+    const int base = before + incl - cnt;
+    if (my) {
+      blk[k] = (uint16_t)base;
+      for (int e = 0; e < cnt; ++e) blk[H + base + e] = entries[tm.entry_begin + cur + e];
+      cur += cnt;
+    }
+    if (k == 0) blk[tm.node_count] = (uint16_t)total;
+    __syncthreads();
+  }
 }
 
 // (tile, halo?, element) keys of every patch row: te order = own first, then halo
@@ -1175,16 +1218,41 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       set_error("internal error: patch entry not found in its tile or output offset overflow");
       return fail(FM_CUDA_ERROR);
     }
-    Scratch cmax;
+    Scratch cmax, pch;
     CK(cmax.alloc(4, s));
+    CK(pch.alloc((size_t)n_tiles * MAX_CHUNKS * 4, s));
     CK(cudaMemsetAsync(cmax.p, 0, 4, s));
     k_chunk_entry_max<<<n_tiles, 256, 0, s>>>(n_tiles, c->meta, c->node_desc,
-                                               cmax.as<unsigned int>());
+                                               cmax.as<unsigned int>(), pch.as<int32_t>());
     CK(cudaGetLastError());
     unsigned int h_cmax = 0;
+    std::vector<int32_t> h_pch((size_t)n_tiles * MAX_CHUNKS);
     CK(cudaMemcpyAsync(&h_cmax, cmax.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_pch.data(), pch.p, h_pch.size() * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->chunk_entry_cap = ((int)h_cmax + 7) / 8 * 8;
+
+    // 5a. chunk-major entry blocks (the tile kernels load a chunk's block with
+    // its records): per tile a fixed stride = its largest block
+    int64_t blk_total = 0;
+    c->blk_cap = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int nch = (hm[t].own_count + hm[t].halo_count + c->tile_nodes - 1) / c->tile_nodes;
+      int mx = 0;
+      for (int ch = 0; ch < nch; ++ch) mx = std::max(mx, h_pch[(size_t)t * MAX_CHUNKS + ch]);
+      const int stride = blk_header(hm[t].node_count) + (mx + 7) / 8 * 8;
+      hm[t].blk_stride = stride;
+      hm[t].blk_base = blk_total;
+      blk_total += (int64_t)nch * stride;
+      c->blk_cap = std::max(c->blk_cap, stride);
+    }
+    CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
+    CK(dmalloc(&c->chunk_blocks, blk_total + 8, &B));
+    CK(cudaMemsetAsync(c->chunk_blocks, 0, (blk_total + 8) * 2, s));
+    k_chunk_blocks<<<n_tiles, c->tile_nodes, 0, s>>>(n_tiles, c->meta, c->node_desc,
+                                                      c->node_entries, c->tile_nodes,
+                                                      c->chunk_blocks);
+    CK(cudaGetLastError());
 
     // 5b. cross-tile exchange of the fused exact kernel ---------------------------
     Scratch stile, xcnt, xoff, xk, xk2, xv, xv2, xsum;
@@ -1271,16 +1339,19 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   {
     const int regs_cap = c->tile_nodes == 128 ? 4 : 2;
     auto fit = [&](int nb, int tb) {
-      const size_t sm = tile_exact_smem(dim, d, c->entry_cap, c->clo_cap, c->tile_nodes, nb, tb);
+      const size_t sm = tile_exact_smem(dim, d, c->blk_cap, c->clo_cap, c->tile_nodes, nb, tb);
       return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));
     };
-    // most CTAs per SM first, then the next tile's node values a tile ahead
-    // (nb = 2), then its tables (tb = 2); FM_TILE_CFG="nb,tb" forces a variant
+    // most CTAs per SM first, then the next tile's tables a tile ahead
+    // (tb = 2); node values a tile ahead (nb = 2) measured better in 2D (many
+    // small tiles, config 2/3) and worse in 3D (config 4: 0.874 vs 0.861 ms);
+    // FM_TILE_CFG="nb,tb" forces a variant
+    const int nb_pref = dim == 2 ? 2 : 1;
     int best = -1;
     for (int nb = 2; nb >= 1; --nb)
       for (int tb = 2; tb >= 1; --tb) {
         const int f = fit(nb, tb);
-        const int score = f * 4 + (nb == 2) * 2 + (tb == 2);
+        const int score = f * 8 + (tb == 2) * 2 + (nb == nb_pref);
         if (f > 0 && score > best) {
           best = score;
           c->node_bufs = nb;
@@ -1341,7 +1412,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
-                  c->partial,   c->node_clo};
+                  c->partial,   c->node_clo,  c->chunk_blocks};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;

@@ -55,9 +55,17 @@ struct TileMeta {
   int entry_begin, entry_count;  // range in node_entries (entry_begin % 8 == 0)
   int elem_begin;                // range start in flags (own + halo)
   int clo_begin, clo_count;      // node closure (clo_begin % 4 == 0)
-  int pad;
+  int blk_stride;                // chunk entry blocks: u16 units per block (multiple of 8)
+  int64_t blk_base;              // first block of the tile in chunk_blocks (u16 units)
+  int pad[2];
 };
-static_assert(sizeof(TileMeta) == 48, "TileMeta layout");
+static_assert(sizeof(TileMeta) == 64, "TileMeta layout");
+
+// Chunk entry block (u16 units): [node offsets: node_count + 1, padded to 8]
+// [the chunk's node entries (te << 2 | slot), node-major, te ascending per node]
+__host__ __device__ __forceinline__ int blk_header(int node_count) {
+  return (node_count + 1 + 7) / 8 * 8;
+}
 
 template <int DIM> struct Elem {
   int c[DIM + 1];  // global node ids (streaming kernels)
@@ -196,6 +204,7 @@ struct TileArgs {
   const int4 *node_desc;       // {entry_off | chunk counts, chunk counts, node id,
                                //  out | mask << 28} (see chunk_count)
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
+  const uint16_t *chunk_blocks;  // per tile and chunk: node offsets + entries (see blk_header)
   const int32_t *rank_of;      // node -> free rank or -1
   // cross-tile exchange of the fused exact kernel (elements computed once, by
   // their owner tile): items (owner te << 2 | slot) -> exchange slot, sorted by
@@ -211,6 +220,7 @@ struct TileArgs {
   int n_tiles;                 // node tiles
   int n_tiles_all;             // + orphan tiles (J only)
   int entry_cap;               // max entries of one tile, rounded up to 8
+  int blk_cap;                 // max chunk entry block, u16 units
   int clo_cap;                 // max closure size, rounded up to 4
 };
 
@@ -259,6 +269,8 @@ struct fm_ctx {
   double *xbuf = nullptr, *partial = nullptr;
   int32_t *node_outw = nullptr;  // per tile node: out offset | mask << 28
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
+  uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
+  int blk_cap = 0;                   // max block size, u16 units
   int64_t n_cross = 0;
   int32_t *fixed_nodes = nullptr;  // nodes without a free dof (b.v in the fused finalize)
   int64_t n_fixed_nodes = 0;
@@ -274,8 +286,9 @@ struct fm_ctx {
 
   fm::TileArgs tile_args() const {
     return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
-                        loc,     closure, flags,   node_desc,       node_entries, rank_of,  xkey,
+                        loc,     closure, flags,   node_desc,       node_entries, chunk_blocks,
+                        rank_of, xkey,
                         xpos,    xchunk,  xbuf,            partial,   node_clo,    n_tiles,
-                        n_tiles_all, entry_cap, clo_cap};
+                        n_tiles_all, entry_cap, blk_cap, clo_cap};
   }
 };

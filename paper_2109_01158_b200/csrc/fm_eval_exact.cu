@@ -63,18 +63,22 @@ __host__ __device__ constexpr size_t r16(size_t x) { return (x + 15) / 16 * 16; 
 template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
-  // records, then the rows' closure indices (u16 x 4)
-  __host__ __device__ static size_t stage() { return r16((size_t)CT * RB) + (size_t)(CT + 2) * 8; }
+  // stage: the chunk's records | their closure indices | its entry block
+  __host__ __device__ static size_t loc_off() { return r16((size_t)CT * RB); }
+  __host__ __device__ static size_t blk_off() { return loc_off() + (size_t)(CT + 2) * 8; }
+  __host__ __device__ static size_t stage(int blk_cap) {
+    return blk_off() + r16((size_t)blk_cap * 2);
+  }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
-  __host__ __device__ static size_t desc() { return (size_t)CT * 16; }
-  __host__ __device__ static size_t ents(int entry_cap) { return r16((size_t)entry_cap * 2); }
+  // per-tile tables: node descriptors | exchange-item chunk starts
+  __host__ __device__ static size_t tabs() { return (size_t)CT * 16 + XCH_STRIDE * 4; }
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
-  // nb node-value buffers; tb buffers of entries + chunk starts (2: the next
-  // tile's tables load during this tile)
-  __host__ __device__ static size_t total(int D, int entry_cap, int clo_cap, int nb, int tb) {
-    return 2 * stage() + nb * nodev(D, clo_cap) + cids(clo_cap) + desc() +
-           tb * (ents(entry_cap) + XCH_STRIDE * 4) + staging(D) + 32 * 8 + 8 * 8;
+  // nb node-value buffers, tb table buffers (2: the next tile's tables load a
+  // tile ahead)
+  __host__ __device__ static size_t total(int D, int blk_cap, int clo_cap, int nb, int tb) {
+    return 2 * stage(blk_cap) + nb * nodev(D, clo_cap) + cids(clo_cap) + tb * tabs() +
+           staging(D) + 32 * 8 + 8 * 8;
   }
 };
 
@@ -200,20 +204,19 @@ __global__ void __launch_bounds__(CT, MINB)
   using L = PipeLayout<DIM, CT>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int CAP = a.clo_cap;
-  // stage s at smem + s * stage(); node-value buffer k at nodev0 + k * nodev()
-  auto stg = [&](int s) { return smem + s * L::stage(); };
+  const size_t SG = L::stage(a.blk_cap);
+  // stage s at smem + s * SG; node-value buffer k at nodev0 + k * nodev()
+  auto stg = [&](int s) { return smem + s * SG; };
   auto nodev = [&](int k) {
-    return reinterpret_cast<double *>(smem + 2 * L::stage() + k * L::nodev(D, CAP));
+    return reinterpret_cast<double *>(smem + 2 * SG + k * L::nodev(D, CAP));
   };
-  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * L::stage() + NB * L::nodev(D, CAP));
-  int4 *desc = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(cids) + L::cids(CAP));
-  unsigned char *tabs0 = reinterpret_cast<unsigned char *>(desc) + L::desc();
-  const size_t tabsz = L::ents(a.entry_cap) + XCH_STRIDE * 4;
-  auto ents_of = [&](int k) { return reinterpret_cast<uint16_t *>(tabs0 + k * tabsz); };
+  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * SG + NB * L::nodev(D, CAP));
+  unsigned char *tabs0 = reinterpret_cast<unsigned char *>(cids) + L::cids(CAP);
+  auto desc_of = [&](int k) { return reinterpret_cast<int4 *>(tabs0 + k * L::tabs()); };
   auto xch_of = [&](int k) {  // the tile's exchange-item chunk starts
-    return reinterpret_cast<int *>(tabs0 + k * tabsz + L::ents(a.entry_cap));
+    return reinterpret_cast<int *>(tabs0 + k * L::tabs() + (size_t)CT * 16);
   };
-  double *stage_d = reinterpret_cast<double *>(tabs0 + TB * tabsz);
+  double *stage_d = reinterpret_cast<double *>(tabs0 + TB * L::tabs());
   double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stage_d) +
                                            L::staging(D));
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // record stages
@@ -241,16 +244,14 @@ __global__ void __launch_bounds__(CT, MINB)
       bulk_g2s(cids, a.closure + tm.clo_begin, bytes, cfull);
     }
   };
-  // descriptors, entries and exchange chunk starts of tile t -> table buffer k
+  // descriptors and exchange chunk starts of tile t -> table buffer k
   auto issue_tables = [&](int t, int k) {
     if (tid != 0 || t >= a.n_tiles_all) return;
     const TileMeta tm = a.meta[t];
     const uint32_t nb = (uint32_t)tm.node_count * 16;
-    const uint32_t eb = (uint32_t)r16((size_t)tm.entry_count * 2);
     const uint32_t xb_ = t < a.n_tiles ? XCH_STRIDE * 4 : 0;
-    mbar_arrive_expect_tx(tfull + k, nb + eb + xb_);
-    if (nb) bulk_g2s(desc, a.node_desc + tm.node_begin, nb, tfull + k);
-    if (eb) bulk_g2s(ents_of(k), a.entries + tm.entry_begin, eb, tfull + k);
+    mbar_arrive_expect_tx(tfull + k, nb + xb_);
+    if (nb) bulk_g2s(desc_of(k), a.node_desc + tm.node_begin, nb, tfull + k);
     if (xb_) bulk_g2s(xch_of(k), a.xchunk + (int64_t)t * XCH_STRIDE, xb_, tfull + k);
   };
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
@@ -266,20 +267,25 @@ __global__ void __launch_bounds__(CT, MINB)
     }
     cp_async_arrive_noinc(nfull + k);
   };
-  // own rows: records and their closure indices, one bulk copy each (the
-  // 8-byte index range is widened to 16-byte alignment: row r sits at
-  // position r + (r0 & 1) of the stage's index array)
+  // own rows: records, their closure indices and the chunk's entry block, one
+  // bulk copy each (the 8-byte index range is widened to 16-byte alignment:
+  // row r sits at position r + (r0 & 1) of the stage's index array)
   auto issue_records = [&](const Cursor<CT> &x, int s) {
     if (!x.valid(a) || tid != 0) return;
     const int cnt = min(CT, x.ne - x.c0);
     const int64_t r0 = (int64_t)x.tm.own_begin + x.c0;
     const int64_t l0 = r0 & ~1ll;
     const uint32_t nl = (uint32_t)((cnt + (r0 - l0) + 1) & ~1);
-    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB + nl * 8);
+    const uint32_t bb = (uint32_t)x.tm.blk_stride * 2;
+    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB + nl * 8 + bb);
     if (cnt) {
       bulk_g2s(stg(s), a.aos + r0 * RB, (uint32_t)cnt * RB, full + s);
-      bulk_g2s(stg(s) + r16((size_t)CT * RB), a.loc + l0, nl * 8, full + s);
+      bulk_g2s(stg(s) + L::loc_off(), a.loc + l0, nl * 8, full + s);
     }
+    if (bb)
+      bulk_g2s(stg(s) + L::blk_off(),
+               a.chunk_blocks + x.tm.blk_base + (int64_t)(x.c0 / CT) * x.tm.blk_stride, bb,
+               full + s);
   };
 
   double jsum = 0.0, bvsum = 0.0;  // vol*W of own elements; b.v of the tile nodes' dofs
@@ -340,11 +346,11 @@ __global__ void __launch_bounds__(CT, MINB)
       }
       mbar_wait(tfull + tb, TB == 2 ? (j >> 1) & 1 : j & 1);
       TRACE(7);
-      const uint16_t *ents = ents_of(tb);
+      const int4 *desc = desc_of(tb);
       const int *xch = xch_of(tb);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
-      int cur = 0, outw = 0;
+      int outw = 0;
       int4 nd = make_int4(0, 0, 0, 0);  // node descriptor (entry offset, per-chunk counts)
       double bj[D], acc[D];
 #pragma unroll
@@ -353,17 +359,13 @@ __global__ void __launch_bounds__(CT, MINB)
       if (my_node) {
         cl = __ldg(a.node_clo + tm.node_begin + tid);
         nd = desc[tid];
-        cur = nd.x & ENTRY_OFF_MASK;
         outw = nd.w;
         if (b) {
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
         }
       }
-      if (TB == 2) {
-        __syncthreads();  // every descriptor read: the next tile's tables load now
-        issue_tables(comp.t + gridDim.x, tb ^ 1);
-      }
+      if (TB == 2) issue_tables(comp.t + gridDim.x, tb ^ 1);  // buffer of tile j - 1: done
       const int ne_t = comp.ne;
       for (int c0 = 0; c0 < ne_t; c0 += CT, ++q) {
         const int s = q & 1;
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(CT, MINB)
         Elem<DIM> E;
         if (valid) {
           load_elem_smem<DIM>(stg(s), tid, E);
-          decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + r16((size_t)CT * RB) +
+          decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + L::loc_off() +
                                                        (tid + ((tm.own_begin + c0) & 1)) * 8),
                      E.loc);
           double vv[D][NV];
@@ -430,16 +432,16 @@ __global__ void __launch_bounds__(CT, MINB)
         __syncthreads();  // contributions staged; every record of stage s read
         TRACE(3);
         // stage s is free: records of chunk q + 2
-        issue_records(iss, s);
-        iss.advance(a);
         if (my_node && !(mdl.dbg & 2)) {
-          // this node's entries of the chunk: a known count, so the loads of
-          // two entries are issued together; the order (ascending tile element)
-          // is the fixed summation order
-          const int n = chunk_count(nd, c0 / CT);
+          // this node's entries of the chunk (its slice of the chunk's entry
+          // block): the loads of two entries are issued together; the order
+          // (ascending tile element) is the fixed summation order
+          const uint16_t *blk = reinterpret_cast<const uint16_t *>(stg(s) + L::blk_off());
+          const int e_beg = blk[tid], n = blk[tid + 1] - e_beg;
+          const uint16_t *ents = blk + blk_header(tm.node_count) + e_beg;
           int i = 0;
           for (; i + 1 < n; i += 2) {
-            const int e0 = ents[cur + i], e1 = ents[cur + i + 1];
+            const int e0 = ents[i], e1 = ents[i + 1];
             if ((e1 >> 2) >= ne_t) break;  // cross entries (finishing pass) from here on
             const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
             const double *s1 = stage_d + ((e1 >> 2) - c0) + (e1 & 3) * D * CT;
@@ -453,14 +455,13 @@ __global__ void __launch_bounds__(CT, MINB)
             for (int k = 0; k < D; ++k) acc[k] = (acc[k] + x0[k]) + x1[k];
           }
           if (i < n) {
-            const int e0 = ents[cur + i];
+            const int e0 = ents[i];
             const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
             if ((e0 >> 2) < ne_t) {
 #pragma unroll
               for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
             }
           }
-          cur += n;
         }
         for (int i = xb + tid; i < xe; i += CT) {
           const int key = i == xb + tid ? xkey0 : (int)__ldg(a.xkey + i);
@@ -473,8 +474,10 @@ __global__ void __launch_bounds__(CT, MINB)
         // it; two: the next chunk's barrier already orders this consumption
         // before the write two chunks ahead
         TRACE(4);
-        __syncthreads();
+        __syncthreads();  // stage s consumed: records of chunk q + 2
         TRACE(5);
+        issue_records(iss, s);
+        iss.advance(a);
       }
       if (WJ && my_node && b) {
 #pragma unroll
@@ -551,12 +554,12 @@ cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const 
   return cudaGetLastError();
 }
 
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int tb) {
+size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb) {
   if (ct == 128)
-    return dim == 3 ? PipeLayout<3, 128>::total(d, entry_cap, clo_cap, nb, tb)
-                    : PipeLayout<2, 128>::total(d, entry_cap, clo_cap, nb, tb);
-  return dim == 3 ? PipeLayout<3, 256>::total(d, entry_cap, clo_cap, nb, tb)
-                  : PipeLayout<2, 256>::total(d, entry_cap, clo_cap, nb, tb);
+    return dim == 3 ? PipeLayout<3, 128>::total(d, blk_cap, clo_cap, nb, tb)
+                    : PipeLayout<2, 128>::total(d, blk_cap, clo_cap, nb, tb);
+  return dim == 3 ? PipeLayout<3, 256>::total(d, blk_cap, clo_cap, nb, tb)
+                  : PipeLayout<2, 256>::total(d, blk_cap, clo_cap, nb, tb);
 }
 
 template <int DIM, int MODEL, int CT, int NB, int TB>
@@ -565,7 +568,7 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int MINB = CT == 128 ? 4 : 2;  // <= 128 registers per thread
-  const size_t smem = PipeLayout<DIM, CT>::total(D, a.entry_cap, a.clo_cap, NB, TB);
+  const size_t smem = PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB);
   auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, TB, MINB>
               : k_tile_exact<DIM, MODEL, false, CT, NB, TB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

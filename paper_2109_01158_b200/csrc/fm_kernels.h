@@ -18,7 +18,7 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
                                 const int32_t *xinv, const double *xbuf, const double *partial,
                                 double *g, cudaStream_t s);
-size_t tile_exact_smem(int dim, int d, int entry_cap, int clo_cap, int ct, int nb, int tb);
+size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
                            const double *v, const double *b, double eps, double *g,
