@@ -1492,7 +1492,8 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   ModelArgs ma = model_args(model);
   TimedLaunch tl(c, s);
   const int dm = model->kind == FM_MODEL_NEOHOOKEAN ? c->dim : 1;
-  if (tile_fd_smem(c->dim, dm, c->clo_cap, c->chunk_entry_cap, c->tile_nodes) > 227 * 1024) {
+  if (tile_fd_smem(c->dim, dm, c->clo_cap, c->chunk_entry_cap, c->tile_nodes, c->blk_cap) >
+      227 * 1024) {
     set_error("FD tile staging exceeds shared memory; use smaller tiles");
     return FM_INVALID_ARG;
   }

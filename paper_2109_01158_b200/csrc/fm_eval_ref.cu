@@ -128,9 +128,9 @@ struct FdLayout {
   __host__ __device__ static size_t recs() { return (size_t)CT * FRB; }
   __host__ __device__ static size_t fbuf(int D) { return r16((size_t)CT * D * DIM * 8); }
   __host__ __device__ static size_t stg(int D, int ech) { return (size_t)D * ech * 16; }
-  __host__ __device__ static size_t flat(int ech) { return r16((size_t)ech * 2); }
-  __host__ __device__ static size_t total(int D, int cap, int ech) {
-    return nodev(D, cap) + recs() + fbuf(D) + stg(D, ech) + flat(ech) + 32 * 4;
+  __host__ __device__ static size_t flat(int blk_cap) { return r16((size_t)blk_cap * 2); }
+  __host__ __device__ static size_t total(int D, int cap, int ech, int blk_cap) {
+    return nodev(D, cap) + recs() + fbuf(D) + stg(D, ech) + flat(blk_cap) + 32 * 4;
   }
 };
 
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(CT, 512 / CT)
   double2 *stg = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(Fb) + L::fbuf(D));
   uint16_t *flat = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stg) +
                                                 L::stg(D, ech));
-  int *wsum = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(flat) + L::flat(ech));
+  int *wsum = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(flat) + L::flat(a.blk_cap));
+  (void)wsum;
   const int tid = threadIdx.x;
 
   const TileMeta tm = a.meta[blockIdx.x];
@@ -198,7 +199,6 @@ __global__ void __launch_bounds__(CT, 512 / CT)
   const bool my_node = tid < tm.node_count;
   int4 nd = make_int4(0, 0, 0, 0);
   if (my_node) nd = a.node_desc[tm.node_begin + tid];
-  int cur = nd.x & ENTRY_OFF_MASK;
   double accm[D], accp[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) accm[j] = accp[j] = 0.0;
@@ -254,12 +254,19 @@ __global__ void __launch_bounds__(CT, 512 / CT)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + RB - 1));
     }
-    // ---- this chunk's entries, flattened in node order
-    const int cnt = my_node ? chunk_count(nd, ch) : 0;
-    int total;
-    const int base = block_excl_scan<CT>(cnt, wsum, total);  // (its barriers publish rows)
-    for (int k = 0; k < cnt; ++k) flat[base + k] = __ldg(a.entries + tm.entry_begin + cur + k);
-    __syncthreads();
+    // ---- this chunk's entries in node order: the chunk's entry block (node
+    // offsets + entries), copied as is
+    {
+      const uint4 *src = reinterpret_cast<const uint4 *>(a.chunk_blocks + tm.blk_base +
+                                                         (int64_t)ch * tm.blk_stride);
+      uint4 *dst = reinterpret_cast<uint4 *>(flat);
+      for (int i = tid; i < tm.blk_stride / 8; i += CT) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();  // (also publishes the rows)
+    const int H = blk_header(tm.node_count);
+    const int base = my_node ? flat[tid] : 0;
+    const int cnt = my_node ? flat[tid + 1] - base : 0;
+    const int total = flat[tm.node_count];
     // ---- items f (one entry: element row r, slot l), all D components and both
     // signs.  The row's data (dphi, unperturbed F, closure indices) are read
     // once per entry; j is a compile-time constant of each unrolled pass (no
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(CT, 512 / CT)
     // pair is unperturbed, and IEEE addition is commutative, so only p_l
     // depends on the sign.
     for (int f = tid; f < total; f += CT) {
-      const int en = flat[f];
+      const int en = flat[H + f];
       const int r = (en >> 2) - c0, l = en & 3;
       const unsigned char *rec = recs + r * FRB;
       const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
@@ -362,7 +369,6 @@ __global__ void __launch_bounds__(CT, 512 / CT)
           accp[j] += x.y;
         }
     }
-    cur += cnt;
     __syncthreads();
   }
   if (mykey != ~0ull) atomicMin(badkey, mykey);
@@ -380,10 +386,10 @@ __global__ void __launch_bounds__(CT, 512 / CT)
   }
 }
 
-size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct) {
+size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct, int blk_cap) {
   if (ct == 128)
-    return dim == 3 ? FdLayout<3, 128>::total(d, clo_cap, ech) : FdLayout<2, 128>::total(d, clo_cap, ech);
-  return dim == 3 ? FdLayout<3, 256>::total(d, clo_cap, ech) : FdLayout<2, 256>::total(d, clo_cap, ech);
+    return dim == 3 ? FdLayout<3, 128>::total(d, clo_cap, ech, blk_cap) : FdLayout<2, 128>::total(d, clo_cap, ech, blk_cap);
+  return dim == 3 ? FdLayout<3, 256>::total(d, clo_cap, ech, blk_cap) : FdLayout<2, 256>::total(d, clo_cap, ech, blk_cap);
 }
 
 // ----------------------------------------------------------------- descent
@@ -440,7 +446,7 @@ static cudaError_t fd_t(const TileArgs &a, int n_tiles, int ech, const double *v
                         double eps, double *g, unsigned long long *badkey, const ModelArgs &m,
                         cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  const size_t smem = FdLayout<DIM, CT>::total(D, a.clo_cap, ech);
+  const size_t smem = FdLayout<DIM, CT>::total(D, a.clo_cap, ech, a.blk_cap);
   auto k = k_tile_fd<DIM, MODEL, CT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<n_tiles, CT, smem, s>>>(a, v, b, eps, g, badkey, m, ech);
