@@ -1373,6 +1373,14 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
   }
 
+  // build-only tables: the kernels read the chunk entry blocks instead of the
+  // node-major entry lists, and no kernel reads the owned-slot flags
+  CK(cudaStreamSynchronize(s));
+  if (c->node_entries) CK(cudaFree(c->node_entries));
+  if (c->flags) CK(cudaFree(c->flags));
+  c->node_entries = nullptr;
+  c->flags = nullptr;
+
   // scratch ------------------------------------------------------------------
   c->n_energy_blocks = 148 * 8;
   c->n_dot_blocks = 148 * 2;
