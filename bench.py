@@ -49,6 +49,37 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+class MemSampler:
+    """Peak device memory in use (NVML, every 5 ms) while the problem and its
+    evaluation context are built."""
+
+    def __init__(self, index=0):
+        self.peak, self.stop_ev = 0, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            self.peak = max(self.peak, self.nv.nvmlDeviceGetMemoryInfo(self.h).used)
+            time.sleep(0.005)
+
+    def __exit__(self, *exc):
+        self.stop_ev.set()
+        if self.nv is not None:
+            self.t.join()
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -117,33 +148,72 @@ def cpu_baseline_sample(nx=96, ny=48, nz=48, repeats=2):
             "seconds_per_eval": best}
 
 
+METRIC = "J+gradJ throughput (fused J + exact gradient evals x elements / s)"
+
+
+def _ref_worker(q, bar, nx, ny, nz, ix0, ix1, warmup, steps):
+    """One host process of the reference arm: the femmin algorithm (oracle
+    port) on the x1-slab [ix0, ix1) of the beam, timed between barriers."""
+    from oracle import femmin_oracle as O
+    m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1)
+    P = O.build_patches(m)
+    for _ in range(warmup):
+        O.energy(v, m, model, b)
+        O.exact_gradient(v, m, P, model, b)
+    bar.wait()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.energy(v, m, model, b)
+        O.exact_gradient(v, m, P, model, b)
+    q.put((m.ne, t0, time.perf_counter()))
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on the host CPU (rank 0 only)."""
+    """--impl reference: the reference algorithm (femmin's numpy energy +
+    exact_gradient, restated in oracle/ and pinned bit-exactly against it) on
+    ALL host cores of this box: one single-threaded process per core, each on
+    its own one-cube x1-slab of the same cfg4 beam (a bounded sample of the
+    workload; rank 0 only).  Throughput = elements x steps of all processes /
+    (last stop - first start) on the host's monotonic clock."""
     if rank != 0:
         return
-    nx, ny, nz = 64, 32, 32
-    from oracle import femmin_oracle as O
-    m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109)
-    P = O.build_patches(m)
-    for _ in range(args.warmup):
-        O.energy(v, m, model, b)
-        O.exact_gradient(v, m, P, model, b)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.energy(v, m, model, b)
-        O.exact_gradient(v, m, P, model, b)
-    dt = (time.perf_counter() - t0) / args.steps
-    value = m.ne / dt / 1e6
+    import multiprocessing as mp
+    nx, ny, nz = 256, 128, 128
+    cores = len(os.sched_getaffinity(0))
+    # one process per core, bounded by host memory (about 0.5 GB per process)
+    try:
+        with open("/proc/meminfo") as fh:
+            avail_gb = int(next(x for x in fh if x.startswith("MemAvailable")).split()[1]) / 2**20
+    except Exception:
+        avail_gb = 16.0
+    nproc = max(1, min(cores, args.ref_procs or cores, nx, int(avail_gb / 2 / 0.5)))
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    ctx = mp.get_context("spawn")
+    q, bar = ctx.Queue(), ctx.Barrier(nproc)
+    procs = [ctx.Process(target=_ref_worker,
+                         args=(q, bar, nx, ny, nz, w, w + 1, args.warmup, args.steps))
+             for w in range(nproc)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in procs]
+    for p in procs:
+        p.join()
+    ne = sum(r[0] for r in res)
+    dt = (max(r[2] for r in res) - min(r[1] for r in res)) / args.steps
+    value = ne / dt / 1e6
+    sample = (f"{nproc} single-threaded processes, each one 1-cube x1-slab of the cfg4 beam "
+              f"({ne // nproc} tets each, {ne} total = {ne / (6 * nx * ny * nz):.3f} of cfg4), "
+              f"femmin algorithm (oracle port of energy + exact_gradient)")
     line = {
-        "impl": "reference", "metric": "J+gradJ throughput (fused J + exact gradient evals)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "Melem/s", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4-type 3D Neo-Hookean Kuhn beam sample {nx}x{ny}x{nz} "
-                               f"({m.ne} tets) on [0,2]x[0,1]^2", "parallelism": "host CPU"},
-        "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": 1, "kind": "port",
-                         "sample": f"beam {nx}x{ny}x{nz}, femmin algorithm (oracle port), "
-                                   f"numpy single-threaded ufuncs"},
+        "config": {"workload": f"cfg4 3D Neo-Hookean Kuhn beam {nx}x{ny}x{nz} on [0,2]x[0,1]^2, "
+                               f"sample of {ne} tets", "parallelism": f"host CPU x{nproc} processes"},
+        "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": nproc, "kind": "port",
+                         "sample": sample, "host_cores": cores},
         "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -163,6 +233,12 @@ def main():
     ap.add_argument("--tile-nodes", type=int, default=0)
     ap.add_argument("--box", type=str, default="")
     ap.add_argument("--stream-depth", type=int, default=2)
+    ap.add_argument("--ref-procs", type=int, default=0,
+                    help="--impl reference: host processes (default: all cores)")
+    ap.add_argument("--shard", type=str, default="",
+                    help="r/w: run rank r's x1-slab of a w-way partition on this one GPU")
+    ap.add_argument("--descent-iters", type=int, default=100,
+                    help="--extras: iterations of the config-5 descent loop")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -186,19 +262,33 @@ def main():
         box = [int(x) for x in args.box.split(",")] if args.box else [0, 0, 0]
         tiling = (args.tile_nodes, box + [0] * (3 - len(box)))
 
-    nx, ny, nz = 256, 128, 128
-    if args.config == "cfg4":
-        ix0, ix1 = slab_range(nx, rank, world)
+    BEAMS = {"cfg4": (256, 128, 128), "cfg5": (1024, 512, 512)}
+    msamp = MemSampler(local).__enter__()
+    if args.config in BEAMS:
+        nx, ny, nz = BEAMS[args.config]
+        prank, pworld = rank, world
+        if args.shard:
+            if world > 1:
+                raise SystemExit("--shard emulates one rank on one GPU; not under torchrun")
+            prank, pworld = (int(x) for x in args.shard.split("/"))
+        ix0, ix1 = slab_range(nx, prank, pworld)
         pr = problems.beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1, tiling=tiling)
-        workload = "cfg4: 3D compressible Neo-Hookean beam [0,2]x[0,1]^2, 256x128x128 hexes x 6 " \
-                   "Kuhn tets (25,165,824 tets, 4,276,737 nodes), f=(0,0,-2.5e7), v=x on x1=0"
+        workload = (f"{args.config}: 3D compressible Neo-Hookean beam [0,2]x[0,1]^2, "
+                    f"{nx}x{ny}x{nz} hexes x 6 Kuhn tets ({6 * nx * ny * nz:,} tets, "
+                    f"{(nx + 1) * (ny + 1) * (nz + 1):,} nodes), f=(0,0,-2.5e7), v=x on x1=0")
         ne_total = 6 * nx * ny * nz
+        if args.shard:
+            workload += (f"; ONE rank's x1-slab [{ix0},{ix1}) of the {pworld}-way partition "
+                         f"({pr.ne:,} tets) on this GPU, no exchange")
+            ne_total = pr.ne
     else:
         if world > 1:
-            raise SystemExit("only cfg4 is partitioned across GPUs")
+            raise SystemExit("only the beams (cfg4, cfg5) are partitioned across GPUs")
         pr = problems.CONFIGS[args.config](tiling=tiling)
         workload = args.config
         ne_total = pr.ne
+    msamp.__exit__()
+    torch.cuda.empty_cache()  # build temporaries back to the device
     dm, model, b, v = pr.dm, pr.model, pr.b, pr.v
     ex = SlabExchange.from_problem(pr, rank, world) if world > 1 else None
     g = torch.empty(dm.nfree_dofs, dtype=torch.float64, device="cuda")
@@ -239,6 +329,7 @@ def main():
     if world > 1:
         dist.barrier()
     launches = dm.launches() - l0
+    free_b, total_b = torch.cuda.mem_get_info()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
     kms = sum(a.elapsed_time(z) for a, z in kev) / args.steps
@@ -282,6 +373,49 @@ def main():
                            "tr_energy_calls": res.n_energy,
                            "tr_ms_per_grad_call": res.time / max(1, res.n_grad) * 1e3,
                            "tr_J_start_end": [float(dm.energy(v, model, b)[0]), res.J_u]})
+
+    if args.extras and args.descent_iters > 0 and args.config in ("cfg4", "cfg5"):
+        # config-5 first-order loop: v <- v - alpha grad J on the free dofs,
+        # alpha = 1e-3 h / max|g(v0)|, J recorded every iteration
+        it = args.descent_iters
+        dm.exact_gradient(v, model, b, g=g)
+        if ex is not None:
+            ex.reduce(g)
+        gmax = g.abs().max().reshape(1)
+        if world > 1:
+            dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+        alpha = 1e-3 * (2.0 / nx) / float(gmax)
+        vd = v.clone()
+        Jh = torch.empty((it, 3), dtype=torch.float64, device="cuda")
+        dm.descent(vd, model, b, alpha, 3, g=g, J_hist=Jh, exchange=ex)  # warm-up
+        vd.copy_(v)
+        dm.check()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        dm.descent(vd, model, b, alpha, it, g=g, J_hist=Jh, exchange=ex)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dms = d0.elapsed_time(d1) / it
+        if world > 1:
+            tt = torch.tensor([dms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dms = float(tt[0])
+        dm.check()
+        Jd = Jh[:, 0].cpu()
+        # bytes of one iteration: the fused evaluation + the update (v read and
+        # written, g read at the free dofs)
+        dbytes = algorithmic_bytes(dm.dim, dm.d, dm.ne, dm.nn, dm.nfree_dofs) + 24 * dm.nfree_dofs
+        extras.update({"descent_iters": it, "descent_alpha": alpha,
+                       "descent_ms_per_iter": dms,
+                       "descent_evals_per_s": 1e3 / dms,
+                       "descent_Melem_s": ne_total / dms / 1e3,
+                       "descent_hbm_frac": dbytes / (dms * 1e-3) / 1e9 / _peaks()[0],
+                       "descent_J_first_last": [float(Jd[0]), float(Jd[-1])],
+                       "descent_J_increases": int((Jd[1:] >= Jd[:-1]).sum()),
+                       "descent_J_first10": [float(x) for x in Jd[:10]]})
 
     # ---- end to end through the public device API, host buffers ----------
     v_host = v.cpu().pin_memory()
@@ -354,15 +488,18 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline_sample()
         line = {
-            "metric": "J+gradJ throughput (fused J + exact gradient evals x elements / s)",
+            "metric": METRIC,
             "value": value, "unit": "Melem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (GPU-generated mesh, seeded splitmix64 field v = x + U[-a,a])",
             "config": {"workload": workload, "elements": ne_total,
                        "evals_per_s": 1e3 / ms,
+                       "hbm_in_use_gb": (total_b - free_b) / 1e9,
+                       "hbm_build_peak_gb": msamp.peak / 1e9,
                        "parallelism": f"x1-slabs x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs (3.3 GB per eval) larger than the 126 MB L2; no flush",
+                       "l2": f"inputs ({alg / 1e9:.2f} GB per eval) larger than the 126 MB L2; "
+                             "no flush",
                        "tiles": {k: dm.stats[k] for k in (
                            "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
                            "ctas_per_sm", "node_bufs", "table_bufs", "entry_cap", "cross_entries",

@@ -184,6 +184,15 @@ int fm_grad_fd(fm_ctx *ctx, const fm_model *model, const double *v, const double
  * reference).  g indexed like dofs_minim. */
 int fm_descent_step(fm_ctx *ctx, double *v, const double *g, double alpha, void *stream);
 
+/* First-order descent loop of config 5 (BASELINE.json configs[4]; new, the
+ * reference has no such loop — its callers are the minimizers, solver.py):
+ * `iters` times { J_hist[3i..3i+2] = J(v) (fm_energy layout); g = grad J(v)
+ * (gradients.py:124-149); v_free <- v_free - alpha * g }.  J_hist may be NULL
+ * (gradient-only kernels); g (|dofs_minim|,) holds the last gradient.  Fully
+ * asynchronous on `stream`; inadmissible states latch (fm_ctx_check). */
+int fm_descent(fm_ctx *ctx, const fm_model *model, double *v, const double *b, double alpha,
+               int iters, double *g, double *J_hist, void *stream);
+
 /* Synchronises `stream`, returns the latched condition of the evaluations
  * since the last check and clears it: FM_OK or FM_INADMISSIBLE with
  * *index_host = offending dof (FD, gradients.py:77-81) or -1 (exact path). */

@@ -485,6 +485,20 @@ def exact_gradient(v, mesh: OMesh, P: OPatches, model, b=None):
     return g
 
 
+def descent_loop(v, mesh: OMesh, P: OPatches, model, b, alpha, iters):
+    """Config-5 first-order loop (BASELINE.json configs[4]): ``iters`` times
+    J_i = energy(v) (assembly.py:94-106), g = exact_gradient(v)
+    (gradients.py:124-149), v[dofs_minim] -= alpha * g.  Returns
+    (J history, final v, last g)."""
+    v = np.array(v, dtype=np.float64, copy=True)
+    Js, g = [], None
+    for _ in range(iters):
+        Js.append(energy(v, mesh, model, b)[0])
+        g = exact_gradient(v, mesh, P, model, b)
+        v[mesh.dofs_minim] = v[mesh.dofs_minim] - alpha * g
+    return np.array(Js), v, g
+
+
 def _perturbed_row_densities(v, mesh, P, model, eps, with_libm=False):
     """Core of gradients.py:84-121: the d*||T|| densities for each sign
     (-eps first), with G recomputed from perturbed nodal values."""

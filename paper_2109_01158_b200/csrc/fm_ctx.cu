@@ -1519,6 +1519,21 @@ int fm_descent_step(fm_ctx *c, double *v, const double *g, double alpha, void *s
   return FM_OK;
 }
 
+int fm_descent(fm_ctx *c, const fm_model *model, double *v, const double *b, double alpha,
+               int iters, double *g, double *J_hist, void *stream) {
+  FM_ARG(c && v && g, "null argument");
+  FM_ARG(iters >= 0, "negative iteration count");
+  // every iteration: (J,) grad J at v, then v_free -= alpha * g; the kernels
+  // of consecutive iterations are ordered on the stream, nothing syncs
+  for (int i = 0; i < iters; ++i) {
+    int st = fm_grad_exact(c, model, v, b, g, J_hist ? J_hist + 3 * (int64_t)i : nullptr, stream);
+    if (st) return st;
+    st = fm_descent_step(c, v, g, alpha, stream);
+    if (st) return st;
+  }
+  return FM_OK;
+}
+
 int fm_ctx_check(fm_ctx *c, void *stream, int64_t *index) {
   FM_ARG(c && index, "null argument");
   cudaStream_t s = as_stream(stream);

@@ -112,6 +112,32 @@ class DeviceMesh:
                                              stream_ptr()))
         return v
 
+    def descent(self, v, model, b=None, alpha=1e-3, iters=100, g=None, J_hist=None,
+                exchange=None):
+        """Config-5 first-order loop, in place on v: ``iters`` times
+        J_hist[i] = J(v), g = grad J(v), v_free -= alpha * g (Dirichlet dofs
+        untouched).  J_hist (iters, 3) device doubles or None.  With a
+        ``parallel.SlabExchange`` the interface partials of g and J are summed
+        across ranks before each update (identical g on both sides of a plane,
+        so the shared interface values stay identical)."""
+        if g is None:
+            g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        if J_hist is not None and (J_hist.numel() < 3 * iters or not J_hist.is_contiguous()):
+            raise ValueError("J_hist must hold iters x 3 contiguous doubles")
+        if exchange is None:
+            m = _model(model)
+            _lib.check(self._lib.fm_descent(self._h, C.byref(m), ptr(v), ptr(b), float(alpha),
+                                            int(iters), ptr(g), ptr(J_hist), stream_ptr()),
+                       "fm_descent")
+            return v
+        Jv = J_hist.view(-1, 3) if J_hist is not None else None
+        for i in range(iters):
+            Ji = Jv[i] if Jv is not None else None
+            self.exact_gradient(v, model, b, g=g, J=Ji)
+            exchange.reduce(g, Ji)
+            self.descent_step(v, g, alpha)
+        return v
+
     def check(self):
         """Synchronise and raise InadmissibleStateError for latched conditions."""
         idx = C.c_int64(-1)

@@ -219,7 +219,41 @@ def case_minimize():
     save("minimize_lshape1", **out)
 
 
+def case_descent(nx=8, ny=4, nz=4, seed=2109, iters=20):
+    """Config-5 first-order loop v <- v - alpha * grad J (masked Dirichlet
+    dofs) on a small config-4/5 beam, driven by the reference's energy and
+    exact_gradient; alpha = 1e-3 h / max|g0|."""
+    om = O.beam_mesh(nx, ny, nz, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    m = fmesh._make_mesh(3, -1, om.nodes2coord, om.elems2nodes)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    m = fmesh.mark_dirichlet(m, spec, d=3)
+    pt = femmin.build_patches(m)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    model = NeoHookean(ElasticParams(E=E, nu=nu), dim=3)
+    model.params = Lame(mu / 2, lam / 2)
+    load = LinearLoad.assemble(m, (0.0, 0.0, -2.5e7), d=3)
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    v[m.dofs_minim] += 1e-2 * (2.0 / nx) * (2.0 * O.uniform01(seed, m.dofs_minim) - 1.0)
+    v0 = v.copy()
+    alpha = 1e-3 * (2.0 / nx) / np.abs(exact_gradient(v, m, pt, model, load)).max()
+    Js = []
+    for _ in range(iters):
+        Js.append(energy(v, m, model, load)[0])
+        g = exact_gradient(v, m, pt, model, load)
+        v = v.copy()
+        v[m.dofs_minim] = v[m.dofs_minim] - alpha * g
+    save(f"descent_beam{nx}x{ny}x{nz}", v0=v0, v_final=v, J_hist=np.array(Js),
+         g_last=g, alpha=np.float64(alpha), iters=np.int64(iters), nx=np.int64(nx),
+         ny=np.int64(ny), nz=np.int64(nz), seed=np.int64(seed))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # only the named cases, e.g. "descent"
+        for name in sys.argv[1:]:
+            globals()["case_" + name]()
+        sys.exit(0)
+    case_descent()
     case_minimize()
     case_small_shapes()
     case_lshape1_tests()

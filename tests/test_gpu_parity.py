@@ -274,6 +274,27 @@ def test_mid_size_vs_oracle(kind, size):
                                 gd[ratio.argmax()], int((ratio > 1).sum()))
 
 
+def test_descent_loop_vs_reference(golden):
+    """Config-5 loop on the device (fm_descent) against the same loop driven
+    by the reference's energy / exact_gradient (golden descent_beam8x4x4):
+    J history within 1e-10 relative, final field within 1e-12 of its scale."""
+    gd = golden("descent_beam8x4x4")
+    pr = problems.beam(8, 4, 4, seed=2109)
+    assert np.array_equal(pr.v.cpu().numpy(), gd["v0"])
+    iters = int(gd["iters"])
+    v = pr.v.clone()
+    Jh = torch.empty((iters, 3), dtype=torch.float64, device="cuda")
+    pr.dm.descent(v, pr.model, pr.b, float(gd["alpha"]), iters, J_hist=Jh)
+    pr.dm.check()
+    Jd = Jh[:, 0].cpu().numpy()
+    assert (np.abs(Jd - gd["J_hist"]) / np.abs(gd["J_hist"])).max() < J_TOL
+    assert np.abs(v.cpu().numpy() - gd["v_final"]).max() < 1e-12 * np.abs(gd["v_final"]).max()
+    # the gradient-only loop (no J) reaches the same field bit for bit
+    v2 = pr.v.clone()
+    pr.dm.descent(v2, pr.model, pr.b, float(gd["alpha"]), iters)
+    assert torch.equal(v2, v)
+
+
 def test_determinism_bitwise():
     pr = problems.beam(16, 8, 8, seed=3)
     a = pr.dm.exact_gradient(pr.v, pr.model, pr.b).clone()

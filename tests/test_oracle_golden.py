@@ -174,6 +174,22 @@ def test_beam_problem_bit_exact(golden):
     np.testing.assert_array_equal(O.numeric_gradient(v, m, p, model, b, 1e-8), g["g_fd"])
 
 
+def test_descent_loop_bit_exact(golden):
+    """The config-5 first-order loop driven by the reference's energy and
+    exact_gradient (tests/golden/make_golden.py case_descent)."""
+    g = golden("descent_beam8x4x4")
+    m, model, b, v = O.problem_beam(8, 4, 4, seed=2109)
+    np.testing.assert_array_equal(v, g["v0"])
+    p = O.build_patches(m)
+    alpha = 1e-3 * (2.0 / 8) / np.abs(O.exact_gradient(v, m, p, model, b)).max()
+    assert alpha == g["alpha"]
+    Js, vf, gl = O.descent_loop(v, m, p, model, b, alpha, int(g["iters"]))
+    np.testing.assert_array_equal(Js, g["J_hist"])
+    np.testing.assert_array_equal(vf, g["v_final"])
+    np.testing.assert_array_equal(gl, g["g_last"])
+    assert (np.diff(Js) < 0).all()  # a descent loop: J decreases
+
+
 def test_direct_fd_within_roundoff_of_reference_fd(golden):
     """The direct-sum FD (the GPU's summation structure) differs from the
     reference cumsum FD only by roundoff; both sit near the exact gradient."""
