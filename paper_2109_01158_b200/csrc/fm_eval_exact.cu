@@ -317,6 +317,11 @@ __global__ void __launch_bounds__(CT, MINB)
 
     while (comp.valid(a)) {
       const TileMeta tm = comp.tm;
+      // every thread is done with the previous tile (its b.v reads of the node
+      // values, its descriptor) before any buffer of it is refilled: the
+      // node-value gather below overwrites the buffer that tile j - 1 (NB = 1)
+      // or j - 2 ... read at its end, and a tile without chunks has no barrier
+      if (j > 0) __syncthreads();
       TRACE(6);
       // ---- tile start: with TB = 1 the tables load now (previous tile done)
       const int tb = TB == 2 ? (int)(j & 1) : 0;

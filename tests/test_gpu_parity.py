@@ -304,6 +304,27 @@ def test_determinism_bitwise():
         assert torch.equal(pr.dm.energy(pr.v, pr.model, pr.b), Ja)
 
 
+def test_many_tiles_per_cta_fused_J():
+    """More tiles than resident CTAs (each CTA walks several tiles, so node
+    buffers are refilled between tiles): the fused J equals the energy
+    kernel's J and the oracle's, bit-stable over repeats (regression: a missing
+    barrier let the next tile's node-value gather overwrite values still read
+    for b.v)."""
+    pr = problems.beam(96, 48, 48, seed=11)
+    assert pr.dm.stats["n_tiles"] > 2 * 148 * pr.dm.stats["ctas_per_sm"]
+    om, omodel, b, v = O.problem_beam(96, 48, 48, seed=11)
+    Jo = O.energy(v, om, omodel, b)[0]
+    Je = pr.dm.energy(pr.v, pr.model, pr.b).clone()
+    J = torch.empty(3, dtype=torch.float64, device="cuda")
+    g0 = pr.dm.exact_gradient(pr.v, pr.model, pr.b, J=J).clone()
+    J0 = J.clone()
+    assert _rel(float(J0[0]), Jo) < J_TOL
+    assert (torch.abs(J0 - Je) <= 1e-12 * torch.abs(Je)).all(), (J0.tolist(), Je.tolist())
+    for _ in range(5):
+        g = pr.dm.exact_gradient(pr.v, pr.model, pr.b, J=J)
+        assert torch.equal(J, J0) and torch.equal(g, g0)
+
+
 @pytest.mark.parametrize("depth", [1, 2, 3])
 def test_field_stream_matches_serial(depth):
     """streaming.FieldStream: overlapped H2D / kernel / D2H of distinct host
