@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -204,10 +205,10 @@ __global__ void k_build_aos(int64_t ne, const int32_t *s2o, const int64_t *conn,
 
 // (tile, node) keys of every element a tile visits: node tiles from the unique
 // (tile, halo?, element) list, orphan tiles from their own storage range
-__global__ void k_closure_keys(int64_t M, const uint64_t *ukeys, int64_t n_orph, int64_t orph0,
-                               int n_tiles, int ot, const int32_t *s2o, const int64_t *conn,
-                               int nv, uint64_t *keys) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + n_orph;
+__global__ void k_closure_keys(int64_t i0, int64_t i1, int64_t M, const uint64_t *ukeys,
+                               int64_t orph0, int n_tiles, int ot, const int32_t *s2o,
+                               const int64_t *conn, int nv, uint64_t *keys) {
+  for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i1;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t t;
     int64_t e;
@@ -219,7 +220,7 @@ __global__ void k_closure_keys(int64_t M, const uint64_t *ukeys, int64_t n_orph,
       t = (uint64_t)(n_tiles + o / ot);
       e = s2o[orph0 + o];
     }
-    for (int l = 0; l < nv; ++l) keys[i * nv + l] = (t << 32) | (uint64_t)conn[e * nv + l];
+    for (int l = 0; l < nv; ++l) keys[(i - i0) * nv + l] = (t << 32) | (uint64_t)conn[e * nv + l];
   }
 }
 
@@ -636,6 +637,16 @@ template <class T> static cudaError_t dmalloc(T **p, size_t n, size_t *acc) {
   return cudaMalloc((void **)p, std::max<size_t>(n, 1) * sizeof(T));
 }
 
+// FM_DEBUG_MEM=1: device memory in use at the build stages (stderr)
+static void memlog(const char *stage, cudaStream_t s) {
+  static const bool on = getenv("FM_DEBUG_MEM") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  fprintf(stderr, "[fm mem] %-28s %8.2f GB in use\n", stage, (tot - fr) / 1e9);
+}
+
 static int bits_for(uint64_t x) {
   int b = 0;
   while (b < 64 && (x >> b)) ++b;
@@ -757,6 +768,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }                                                             \
   } while (0)
 
+  memlog("1. ranks and output offset", s);
   // 1. ranks and output offsets ---------------------------------------------
   CK(dmalloc(&c->rank_of, m->nn, &B));
   CK(dmalloc(&c->free_node, nfree, &B));
@@ -804,6 +816,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }
   }
 
+  memlog("2. node tiles (Morton", s);
   // 2. node tiles (Morton-ordered boxes) -------------------------------------
   std::vector<int32_t> h_tnp{0};      // tile node ptr
   std::vector<int32_t> h_lens;        // patch length per sorted node
@@ -909,6 +922,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
                                                        s_tnr.as<int32_t>(), s_tor.as<int32_t>());
   CK(cudaGetLastError());
 
+  memlog("3. element owners", s);
   // 3. element owners and storage order ---------------------------------------
   Scratch okey, okey2, oval2, owner_of, o2s, own_ptr;
   CK(okey.alloc(ne * 4, s));
@@ -935,9 +949,13 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
                                                                   own_ptr.as<int32_t>());
     CK(cudaGetLastError());
   }
+  okey.reset();  // owner keys and sort buffers are done
+  okey2.reset();
+  oval2.reset();
   std::vector<int32_t> h_own(n_tiles + 2);
   CK(cudaMemcpyAsync(h_own.data(), own_ptr.p, (n_tiles + 2) * 4, cudaMemcpyDeviceToHost, s));
 
+  memlog("4. tile element lists", s);
   // 4. tile element lists (own + halo) ----------------------------------------
   int64_t M = 0;
   Scratch ukeys, umask, tptr, tsplit, tpos;
@@ -972,6 +990,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     }, s));
     CK(cudaMemcpyAsync(&M, nsel.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    memlog("4. after patch-pair sort", s);
     k_tile_bounds<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(n_tiles, M, uk, tptr.as<int32_t>(),
                                                              tsplit.as<int32_t>());
     CK(cudaGetLastError());
@@ -1086,33 +1105,80 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(dmalloc(&c->halo_loc, halo_total + 4, &B));
   CK(cudaMemsetAsync(c->halo_loc, 0, (halo_total + 4) * 8, s));
 
+  memlog("4b. node closures", s);
   // 4b. node closures of every tile and the 16-bit closure indices ---------------
   {
     const int NTA = c->n_tiles_all;
-    const int64_t NK = (M + n_orph) * nv;
-    Scratch ck, ck2, cu, nsel, cstart;
-    CK(ck.alloc(NK * 8, s));
-    CK(ck2.alloc(NK * 8, s));
-    CK(cu.alloc(NK * 8, s));
+    const int64_t NI = M + n_orph;
+    // keys (tile << 32 | node) of the tile elements' nodes, sorted and
+    // de-duplicated in batches of whole tiles (tile-major keys: the batches'
+    // unique runs concatenate to the global result) so the sort buffers stay
+    // small at config-5 scale; at most FM_CLOSURE_BATCH (default 2^25) elements
+    int64_t cap = 1ll << 25;
+    if (const char *e = getenv("FM_CLOSURE_BATCH")) cap = std::max<int64_t>(1, atoll(e));
+    std::vector<int64_t> cuts{0};  // batch boundaries on tile boundaries
+    {
+      std::vector<int64_t> tb;  // tile starts in the element index space
+      for (int t = 1; t < n_tiles; ++t) tb.push_back(h_ptr[t]);
+      if (n_tiles > 0 && M < NI) tb.push_back(M);
+      for (int64_t o = OT; o < n_orph; o += OT) tb.push_back(M + o);
+      tb.push_back(NI);
+      int64_t last = 0;
+      for (size_t k = 0; k < tb.size(); ++k) {
+        const bool end = k + 1 == tb.size();
+        if (end || tb[k + 1] - cuts.back() > cap) {
+          if (tb[k] > cuts.back()) cuts.push_back(tb[k]);
+        }
+        last = tb[k];
+      }
+      if (cuts.back() != last) cuts.push_back(last);
+    }
+    int64_t bmax = 0;
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) bmax = std::max(bmax, cuts[k + 1] - cuts[k]);
+    const int64_t NKB = std::max<int64_t>(bmax * nv, 1);
+    Scratch ck, ck2, nsel, cstart, cu;
     CK(nsel.alloc(8, s));
     CK(cstart.alloc((NTA + 1) * 4, s));
-    k_closure_keys<<<grid_for(M + n_orph, 256), 256, 0, s>>>(
-        M, ukeys.as<uint64_t>(), n_orph, h_own[n_tiles], n_tiles, OT, c->storage_to_orig, m->conn,
-        nv, ck.as<uint64_t>());
-    CK(cudaGetLastError());
-    cub::DoubleBuffer<uint64_t> dk(ck.as<uint64_t>(), ck2.as<uint64_t>());
     const int end_bit = 32 + bits_for((uint64_t)NTA);
-    CK(cub_call([&](void *t, size_t &b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, dk, NK, 0, end_bit, s);
-    }, s));
-    uint64_t *cuk = cu.as<uint64_t>();
-    int64_t *ns = nsel.as<int64_t>();
-    CK(cub_call([&](void *t, size_t &b) {
-      return cub::DeviceSelect::Unique(t, b, dk.Current(), cuk, ns, NK, s);
-    }, s));
     int64_t C = 0;
-    CK(cudaMemcpyAsync(&C, nsel.p, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    {
+      CK(ck.alloc(NKB * 8, s));
+      CK(ck2.alloc(NKB * 8, s));
+      std::vector<std::unique_ptr<Scratch>> parts;
+      std::vector<int64_t> part_n;
+      for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+        const int64_t i0 = cuts[k], i1 = cuts[k + 1], nk = (i1 - i0) * nv;
+        k_closure_keys<<<grid_for(i1 - i0, 256), 256, 0, s>>>(
+            i0, i1, M, ukeys.as<uint64_t>(), h_own[n_tiles], n_tiles, OT, c->storage_to_orig,
+            m->conn, nv, ck.as<uint64_t>());
+        CK(cudaGetLastError());
+        cub::DoubleBuffer<uint64_t> dk(ck.as<uint64_t>(), ck2.as<uint64_t>());
+        CK(cub_call([&](void *t, size_t &b) {
+          return cub::DeviceRadixSort::SortKeys(t, b, dk, nk, 0, end_bit, s);
+        }, s));
+        uint64_t *dst = dk.Current() == ck.as<uint64_t>() ? ck2.as<uint64_t>() : ck.as<uint64_t>();
+        CK(cub_call([&](void *t, size_t &b) {
+          return cub::DeviceSelect::Unique(t, b, dk.Current(), dst, nsel.as<int64_t>(), nk, s);
+        }, s));
+        int64_t cb_n = 0;
+        CK(cudaMemcpyAsync(&cb_n, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        parts.emplace_back(new Scratch);
+        CK(parts.back()->alloc(std::max<int64_t>(cb_n, 1) * 8, s));
+        CK(cudaMemcpyAsync(parts.back()->p, dst, cb_n * 8, cudaMemcpyDeviceToDevice, s));
+        part_n.push_back(cb_n);
+        C += cb_n;
+      }
+      memlog("4b. after closure sorts", s);
+      CK(cu.alloc(std::max<int64_t>(C, 1) * 8, s));
+      int64_t off = 0;
+      for (size_t k = 0; k < parts.size(); ++k) {
+        CK(cudaMemcpyAsync(cu.as<uint64_t>() + off, parts[k]->p, part_n[k] * 8,
+                           cudaMemcpyDeviceToDevice, s));
+        off += part_n[k];
+      }
+    }
+    uint64_t *cuk = cu.as<uint64_t>();
     k_lower_bounds_u64<<<grid_for(NTA + 1, 256), 256, 0, s>>>(NTA, C, cuk, 32,
                                                               cstart.as<int32_t>());
     CK(cudaGetLastError());
@@ -1194,7 +1260,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
   }
+  o2s.reset();
+  umask.reset();
 
+  memlog("5. node descriptors", s);
   // 5. node descriptors and entries ---------------------------------------------
   if (nfree > 0) {
     Scratch eoff, eabs, ovf;
@@ -1218,6 +1287,9 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       set_error("internal error: patch entry not found in its tile or output offset overflow");
       return fail(FM_CUDA_ERROR);
     }
+    ukeys.reset();  // tile element lists: consumed by the descriptors / entries
+    tpos.reset();
+    owner_of.reset();
     Scratch cmax, pch;
     CK(cmax.alloc(4, s));
     CK(pch.alloc((size_t)n_tiles * MAX_CHUNKS * 4, s));
@@ -1381,6 +1453,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->node_entries = nullptr;
   c->flags = nullptr;
 
+  memlog("scratch", s);
   // scratch ------------------------------------------------------------------
   c->n_energy_blocks = 148 * 8;
   c->n_dot_blocks = 148 * 2;

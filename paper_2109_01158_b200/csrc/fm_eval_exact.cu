@@ -544,7 +544,18 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     const int mask = (unsigned)w >> OUT_MASK_SHIFT;
     if (!(mask & (1 << j))) continue;
     double sum = partial[i];
-    for (int p = lo; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
+    // four entries per step: their slot loads, then their value loads, are
+    // issued back to back (two dependent round trips per four entries instead
+    // of per entry); the sum stays sequential in entry order
+    int p = lo;
+    for (; p + 4 <= hi; p += 4) {
+      const int s0 = __ldg(xinv + p), s1 = __ldg(xinv + p + 1), s2 = __ldg(xinv + p + 2),
+                s3 = __ldg(xinv + p + 3);
+      const double x0 = __ldg(xbuf + (int64_t)s0 * D + j), x1 = __ldg(xbuf + (int64_t)s1 * D + j),
+                   x2 = __ldg(xbuf + (int64_t)s2 * D + j), x3 = __ldg(xbuf + (int64_t)s3 * D + j);
+      sum = (((sum + x0) + x1) + x2) + x3;
+    }
+    for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
     g[(w & ((1 << OUT_MASK_SHIFT) - 1)) + __popc(mask & ((1 << j) - 1))] = sum;
   }
 }

@@ -11,6 +11,8 @@ copy the result back.
 from __future__ import annotations
 
 import ctypes as C
+import os
+import sys
 import weakref
 
 import numpy as np
@@ -61,6 +63,13 @@ class DeviceMesh:
         if tiling is not None:
             nt, box = tiling
             til = _lib.FmTiling(int(nt), (C.c_int32 * 3)(*[int(b) for b in box]))
+        # the build's temporaries come from the CUDA stream-ordered pool: hand
+        # torch's cached (unused) blocks back first
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        if os.environ.get("FM_DEBUG_MEM"):
+            print(f"[fm mem] torch allocated before the context build "
+                  f"{torch.cuda.memory_allocated() / 1e9:.2f} GB", file=sys.stderr)
         h = C.c_void_p()
         _lib.check(self._lib.fm_ctx_create(C.byref(desc), C.byref(til) if til else None,
                                            stream_ptr(), C.byref(h)), "fm_ctx_create")
