@@ -126,7 +126,8 @@ int fm_field_nh(int64_t nn, int d, const double *coords, const int64_t *dofs_min
 
 /* ------------------------------------------------------------------------ */
 /* Evaluation context: the frozen Mesh + Patches uploaded once (mesh.py:31-53,
- * patches.py:22-34), re-laid out as 128-byte element records and node tiles. */
+ * patches.py:22-34), re-laid out as node tiles with 80-byte (3D) / 48-byte (2D)
+ * element records. */
 
 typedef struct fm_ctx fm_ctx;
 

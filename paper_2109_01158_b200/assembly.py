@@ -2,7 +2,7 @@
 
 Mirror of ``/root/reference/pkg/src/femmin/assembly.py``.  ``energy`` is one
 streaming pass of the fused element kernel (csrc/fm_eval_ref.cu ``k_energy``)
-over the 128-byte element records of the cached device context, plus a
+over the element records of the cached device context, plus a
 fixed-order ``b.v``; loads are assembled on the GPU from the mass-matrix rows.
 """
 

@@ -2,7 +2,7 @@
 
 ``DeviceMesh`` owns one ``fm_ctx`` (include/femmin_b200.h): the frozen Mesh +
 Patches of the reference (mesh.py:31-53, patches.py:22-34) uploaded once and
-re-laid out as 128-byte element records and node tiles.  Its methods take and
+re-laid out as node tiles with 80-byte (3D) / 48-byte (2D) element records.  Its methods take and
 return CUDA tensors without host copies; the numpy drop-in functions in
 ``assembly`` / ``gradients`` are thin wrappers that upload ``v``, call these and
 copy the result back.
