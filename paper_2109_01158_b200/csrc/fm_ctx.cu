@@ -1461,6 +1461,9 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(dmalloc(&c->jpart, c->n_part, &B));
   CK(dmalloc(&c->dotpart, std::max(c->n_part, c->n_dot_blocks), &B));
   CK(dmalloc(&c->status, 2, &B));
+  CK(dmalloc(&c->fpart, FINISH_MAX_BLOCKS, &B));
+  CK(dmalloc(&c->ticket, 1, &B));
+  CK(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), s));
   unsigned long long init[2] = {0ull, ~0ull};
   CK(cudaMemcpyAsync(c->status, init, 16, cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -1493,7 +1496,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
-                  c->partial,   c->node_clo,  c->chunk_blocks};
+                  c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1549,14 +1552,14 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
                               s));
     c->launches++;
   }
-  if (c->n_cross > 0) {
-    FM_CUDA(launch_finish_cross(c->d, c->nfree, c->node_xbase, c->node_outw, c->xpos, c->xbuf,
-                                c->partial, g, s));
-    c->launches++;
-  }
-  if (wj) {  // b.v of the tile nodes came with the tile kernel's partials
-    FM_CUDA(launch_finalize_tiles(c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0,
-                                  c->fixed_nodes, c->n_fixed_nodes, b, v, c->d, J_out, s));
+  if (c->n_cross > 0 || wj) {
+    // cross entries of the tile nodes, and with J its finalisation (b.v of the
+    // tile nodes came with the tile kernel's partials; the nodes without a
+    // free dof are added here)
+    JFinal jf{c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0, c->fixed_nodes,
+              c->n_fixed_nodes, b, v, c->fpart, c->ticket, wj ? J_out : nullptr};
+    FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->nfree : 0, c->node_xbase,
+                                c->node_outw, c->xpos, c->xbuf, c->partial, g, jf, s));
     c->launches++;
   }
   return FM_OK;

@@ -272,13 +272,15 @@ struct fm_ctx {
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units
   int64_t n_cross = 0;
-  int32_t *fixed_nodes = nullptr;  // nodes without a free dof (b.v in the fused finalize)
+  int32_t *fixed_nodes = nullptr;  // nodes without a free dof (their b.v: finishing pass)
   int64_t n_fixed_nodes = 0;
   // scratch
   double *jpart = nullptr;        // per CTA (fused) / per block (energy)
   double *dotpart = nullptr;      // b.v partials
   int n_dot_blocks = 0, n_energy_blocks = 0, n_part = 0;
   unsigned long long *status = nullptr;  // [0] exact inadmissible, [1] FD min key
+  double *fpart = nullptr;          // finishing pass: per-block b.v of fixed nodes
+  unsigned int *ticket = nullptr;    // finishing pass: last-block ticket (0 between calls)
   int64_t launches = 0;
   size_t bytes = 0;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;  // armed by fm_ctx_time_next

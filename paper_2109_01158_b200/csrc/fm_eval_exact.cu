@@ -26,7 +26,7 @@
 //                 item order) and added by k_finish_cross.
 // J: per-thread partials over a static tile assignment -> fixed block tree ->
 // one partial per CTA (vol * W, and b.v of the tile nodes from the closure
-// values), reduced in CTA order by k_finalize_tiles.
+// values), reduced in CTA order by the last block of k_finish_cross.
 #include "fm_density.cuh"
 #include "fm_kernels.h"
 #include "fm_pipe.cuh"
@@ -524,6 +524,11 @@ __global__ void __launch_bounds__(CT, MINB)
 // [xbase[k], xbase[k + 1]) (consecutive nodes back to back); the tile kernel
 // left the node's own-element sum (minus b) in partial.  g = partial + the
 // cross entries in ascending tile-element order.
+// With J (jf.out): every block also adds b.v of its share of the nodes without
+// a free dof (fixed block tree) into jf.fpart, and the last block to finish
+// (atomic ticket) sums the tile kernel's per-CTA partials and these in index
+// order: J = sum vol W - (b.v of tile nodes + b.v of fixed nodes).  The result
+// does not depend on which block is last; the ticket is reset for the next call.
 template <int D>
 __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int32_t *__restrict__ xbase,
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int32_t *__restrict__ xinv,
                                                       const double *__restrict__ xbuf,
                                                       const double *__restrict__ partial,
-                                                      double *__restrict__ g) {
+                                                      double *__restrict__ g, JFinal jf) {
   // one thread per (node, component): the D threads of a node read adjacent
   // doubles of each exchange slot
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntn * D;
@@ -545,8 +550,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     if (!(mask & (1 << j))) continue;
     double sum = partial[i];
     // four entries per step: their slot loads, then their value loads, are
-    // issued back to back (two dependent round trips per four entries instead
-    // of per entry); the sum stays sequential in entry order
+    // issued back to back; the sum stays sequential in entry order
     int p = lo;
     for (; p + 4 <= hi; p += 4) {
       const int s0 = __ldg(xinv + p), s1 = __ldg(xinv + p + 1), s2 = __ldg(xinv + p + 2),
@@ -558,15 +562,55 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
     g[(w & ((1 << OUT_MASK_SHIFT) - 1)) + __popc(mask & ((1 << j) - 1))] = sum;
   }
+  if (!jf.out) return;
+  __shared__ double red[32];
+  __shared__ bool last;
+  double f = 0.0;
+  if (jf.b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < jf.nfixed;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = (int64_t)__ldg(jf.fixed_nodes + i) * D;
+#pragma unroll
+      for (int j = 0; j < D; ++j) f += __ldg(jf.b + q + j) * __ldg(jf.v + q + j);
+    }
+  }
+  f = block_sum(f, red);
+  if (threadIdx.x == 0) {
+    jf.fpart[blockIdx.x] = f;
+    __threadfence();
+    last = atomicAdd(jf.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0.0, c = 0.0, ff = 0.0;
+  for (int i = threadIdx.x; i < jf.njp; i += blockDim.x) a += jf.jp[i];
+  if (jf.b) {
+    for (int i = threadIdx.x; i < jf.njp; i += blockDim.x) c += jf.bvp[i];
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) ff += __ldcg(jf.fpart + i);
+  }
+  const double A = block_sum(a, red);
+  const double C = block_sum(c, red);
+  const double F = block_sum(ff, red);
+  if (threadIdx.x == 0) {
+    jf.out[0] = A - (C + F);
+    jf.out[1] = A;
+    jf.out[2] = C + F;
+    *jf.ticket = 0u;
+  }
+}
+
+int finish_cross_grid(int d, int64_t ntn) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, FINISH_MAX_BLOCKS));
 }
 
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
                                 const int32_t *xinv, const double *xbuf, const double *partial,
-                                double *g, cudaStream_t s) {
-  const int grid = (int)std::min<int64_t>((ntn * d + 255) / 256, 148 * 32);
-  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
-  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
-  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g);
+                                double *g, const JFinal &jf, cudaStream_t s) {
+  const int grid = finish_cross_grid(d, ntn);
+  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
+  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
+  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
   return cudaGetLastError();
 }
 

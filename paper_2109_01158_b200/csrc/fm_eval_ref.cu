@@ -64,42 +64,6 @@ __global__ void __launch_bounds__(1024) k_finalize(const double *__restrict__ jp
   }
 }
 
-// Fused-path J: W partials per CTA, b.v partials per CTA (the tile nodes' dofs,
-// summed by the tile kernel) and the dofs of the nodes outside every tile
-// (all components fixed), summed here; fixed order, one block.
-__global__ void __launch_bounds__(1024) k_finalize_tiles(const double *__restrict__ jp,
-                                                         const double *__restrict__ bvp, int n,
-                                                         const int32_t *__restrict__ fixed_nodes,
-                                                         int64_t nfixed, const double *__restrict__ b,
-                                                         const double *__restrict__ v, int d,
-                                                         double *__restrict__ out) {
-  __shared__ double red[32];
-  double a = 0.0, c = 0.0, f = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) a += jp[i];
-  if (b) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c += bvp[i];
-    for (int64_t i = threadIdx.x; i < nfixed; i += blockDim.x) {
-      const int64_t q = (int64_t)fixed_nodes[i] * d;
-      for (int j = 0; j < d; ++j) f += b[q + j] * v[q + j];
-    }
-  }
-  const double A = block_sum(a, red);
-  const double C = block_sum(c, red);
-  const double Fx = block_sum(f, red);
-  if (threadIdx.x == 0) {
-    out[0] = A - (C + Fx);
-    out[1] = A;
-    out[2] = C + Fx;
-  }
-}
-
-cudaError_t launch_finalize_tiles(const double *jp, const double *bvp, int n,
-                                  const int32_t *fixed_nodes, int64_t nfixed, const double *b,
-                                  const double *v, int d, double *out, cudaStream_t s) {
-  k_finalize_tiles<<<1, 1024, 0, s>>>(jp, bvp, n, fixed_nodes, nfixed, b, v, d, out);
-  return cudaGetLastError();
-}
-
 // ----------------------------------------------------------------- FD
 // gradients.py:84-121.  One CTA per node tile; its element list (own + halo,
 // dealt order) in chunks of CT rows, three phases per chunk:

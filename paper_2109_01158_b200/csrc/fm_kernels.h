@@ -15,9 +15,22 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
                               int tb, bool wj, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s);
+// J finalisation carried by the finishing pass (see k_finish_cross)
+struct JFinal {
+  const double *jp, *bvp;      // tile kernel partials per CTA
+  int njp;
+  const int32_t *fixed_nodes;  // nodes without a free dof
+  int64_t nfixed;
+  const double *b, *v;
+  double *fpart;               // FINISH_MAX_BLOCKS
+  unsigned int *ticket;        // zero between calls
+  double *out;                 // null: no J
+};
+constexpr int FINISH_MAX_BLOCKS = 148 * 32;
+int finish_cross_grid(int d, int64_t ntn);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
                                 const int32_t *xinv, const double *xbuf, const double *partial,
-                                double *g, cudaStream_t s);
+                                double *g, const JFinal &jf, cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
@@ -33,9 +46,6 @@ cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, i
 cudaError_t launch_dot(const double *a, const double *b, int64_t n, int nblocks, double *part,
                        cudaStream_t s);
 
-cudaError_t launch_finalize_tiles(const double *jp, const double *bvp, int n,
-                                  const int32_t *fixed_nodes, int64_t nfixed, const double *b,
-                                  const double *v, int d, double *out, cudaStream_t s);
 cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, double *out,
                             cudaStream_t s);
 
