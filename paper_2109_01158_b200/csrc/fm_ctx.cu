@@ -1405,11 +1405,12 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaStreamSynchronize(s));
   }
 
-  // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads; shared memory
+  // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads (3D; 2D: 6 / 3,
+  // tile_exact_minb); shared memory
   // (228 KB per SM, 1 KB reserved per CTA) decides, preferring two node-value
   // buffers (one tile of lead) when that does not cost a CTA
   {
-    const int regs_cap = c->tile_nodes == 128 ? 4 : 2;
+    const int regs_cap = tile_exact_minb(dim, c->tile_nodes);
     auto fit = [&](int nb, int tb) {
       const size_t sm = tile_exact_smem(dim, d, c->blk_cap, c->clo_cap, c->tile_nodes, nb, tb);
       return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));

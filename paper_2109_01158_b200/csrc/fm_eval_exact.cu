@@ -627,7 +627,7 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double
                               const double *b, double *g, double *jpart, double *bvpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  constexpr int MINB = CT == 128 ? 4 : 2;  // <= 128 registers per thread
+  constexpr int MINB = tile_exact_minb(DIM, CT);
   const size_t smem = PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB);
   auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, TB, MINB>
               : k_tile_exact<DIM, MODEL, false, CT, NB, TB, MINB>;

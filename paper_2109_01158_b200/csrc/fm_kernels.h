@@ -15,6 +15,13 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
                               int tb, bool wj, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s);
+// CTAs per SM the fused tile kernel is compiled for (__launch_bounds__ min
+// blocks): 3D <= 128 registers per thread (2 x 256 threads); 2D elements need
+// fewer, <= 85 registers gives 3 x 256 threads, 24 warps to hide latency
+constexpr int tile_exact_minb(int dim, int ct) {
+  return dim == 2 ? (ct == 128 ? 6 : 3) : (ct == 128 ? 4 : 2);
+}
+
 // J finalisation carried by the finishing pass (see k_finish_cross)
 struct JFinal {
   const double *jp, *bvp;      // tile kernel partials per CTA
