@@ -1405,7 +1405,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaStreamSynchronize(s));
   }
 
-  // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads (3D; 2D: 6 / 3,
+  // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads (3D; 2D: 8 / 4,
   // tile_exact_minb); shared memory
   // (228 KB per SM, 1 KB reserved per CTA) decides, preferring two node-value
   // buffers (one tile of lead) when that does not cost a CTA

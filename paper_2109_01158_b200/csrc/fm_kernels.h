@@ -17,9 +17,10 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
                               const ModelArgs &m, cudaStream_t s);
 // CTAs per SM the fused tile kernel is compiled for (__launch_bounds__ min
 // blocks): 3D <= 128 registers per thread (2 x 256 threads); 2D elements need
-// fewer, <= 85 registers gives 3 x 256 threads, 24 warps to hide latency
+// fewer: <= 64 registers gives 4 x 256 threads, 32 warps to hide latency
+// (measured: 3 CTAs 0.865 ms, 4 CTAs 0.799 ms, 5 CTAs (spills) 0.862 ms at cfg2)
 constexpr int tile_exact_minb(int dim, int ct) {
-  return dim == 2 ? (ct == 128 ? 6 : 3) : (ct == 128 ? 4 : 2);
+  return dim == 2 ? (ct == 128 ? 8 : 4) : (ct == 128 ? 4 : 2);
 }
 
 // J finalisation carried by the finishing pass (see k_finish_cross)
