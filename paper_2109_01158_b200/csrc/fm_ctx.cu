@@ -373,6 +373,19 @@ __global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
   }
 }
 
+__global__ void k_nonzero_flags(int64_t n, const int32_t *x, int32_t *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = i < n && x[i] != 0;
+}
+
+__global__ void k_scatter_flagged(int64_t n, const int32_t *flag, const int32_t *pos,
+                                  int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = (int32_t)i;
+}
+
 // first item of every chunk of every tile
 __global__ void k_xchunk(int n_tiles, int ct, int64_t X, const uint64_t *keys, int32_t *xchunk) {
   const int n = n_tiles * XCH_STRIDE;
@@ -1387,6 +1400,26 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     k_mark_cross<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->node_xn, c->node_desc,
                                                        c->node_outw);
     CK(cudaGetLastError());
+    // the finishing pass visits only the tile nodes with cross entries
+    {
+      Scratch xf, xs, xt;
+      CK(xf.alloc((nfree + 1) * 4, s));
+      CK(xs.alloc((nfree + 1) * 4, s));
+      CK(xt.alloc(8, s));
+      k_nonzero_flags<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->node_xn, xf.as<int32_t>());
+      CK(cudaGetLastError());
+      int32_t *fl = xf.as<int32_t>(), *ps = xs.as<int32_t>();
+      CK(cub_call([&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, fl, ps, nfree + 1, s);
+      }, s));
+      int32_t hn = 0;
+      CK(cudaMemcpyAsync(&hn, ps + nfree, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      c->n_xnodes = hn;
+      CK(dmalloc(&c->xnodes, std::max(hn, 1), &B));
+      k_scatter_flagged<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, fl, ps, c->xnodes);
+      CK(cudaGetLastError());
+    }
     CK(dmalloc(&c->node_clo, nfree + 8, &B));
     k_node_clo<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(),
                                                      c->meta, c->node_desc, c->closure,
@@ -1497,7 +1530,8 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
-                  c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket};
+                  c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
+                  c->xnodes};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1559,8 +1593,9 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     // free dof are added here)
     JFinal jf{c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0, c->fixed_nodes,
               c->n_fixed_nodes, b, v, c->fpart, c->ticket, wj ? J_out : nullptr};
-    FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->nfree : 0, c->node_xbase,
-                                c->node_outw, c->xpos, c->xbuf, c->partial, g, jf, s));
+    FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->n_xnodes : 0, c->xnodes,
+                                c->node_xbase, c->node_outw, c->xpos, c->xbuf, c->partial, g,
+                                jf, s));
     c->launches++;
   }
   return FM_OK;

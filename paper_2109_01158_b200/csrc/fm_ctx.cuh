@@ -266,6 +266,8 @@ struct fm_ctx {
   uint16_t *xkey = nullptr;                        // cross-tile exchange (see TileArgs)
   int32_t *xpos = nullptr, *xchunk = nullptr;
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
+  int32_t *xnodes = nullptr;  // tile nodes with cross entries (finishing pass)
+  int64_t n_xnodes = 0;
   double *xbuf = nullptr, *partial = nullptr;
   int32_t *node_outw = nullptr;  // per tile node: out offset | mask << 28
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure

@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(CT, MINB)
 // does not depend on which block is last; the ticket is reset for the next call.
 template <int D>
 __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
+                                                      const int32_t *__restrict__ nodes,
                                                       const int32_t *__restrict__ xbase,
                                                       const int32_t *__restrict__ outw,
                                                       const int32_t *__restrict__ xinv,
@@ -541,14 +542,15 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
   // doubles of each exchange slot
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntn * D;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = i / D;
-    const int j = (int)(i - k * D);
+    const int64_t r = i / D;
+    const int j = (int)(i - r * D);
+    const int64_t k = __ldg(nodes + r);  // a tile node with cross entries
     const int lo = __ldg(xbase + k), hi = __ldg(xbase + k + 1);
     if (hi == lo) continue;
     const int w = __ldg(outw + k);
     const int mask = (unsigned)w >> OUT_MASK_SHIFT;
     if (!(mask & (1 << j))) continue;
-    double sum = partial[i];
+    double sum = partial[k * D + j];
     // four entries per step: their slot loads, then their value loads, are
     // issued back to back; the sum stays sequential in entry order
     int p = lo;
@@ -604,13 +606,17 @@ int finish_cross_grid(int d, int64_t ntn) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, FINISH_MAX_BLOCKS));
 }
 
-cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *xbase, const int32_t *outw,
-                                const int32_t *xinv, const double *xbuf, const double *partial,
-                                double *g, const JFinal &jf, cudaStream_t s) {
+cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,
+                                const int32_t *outw, const int32_t *xinv, const double *xbuf,
+                                const double *partial, double *g, const JFinal &jf,
+                                cudaStream_t s) {
   const int grid = finish_cross_grid(d, ntn);
-  if (d == 3) k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
-  else if (d == 2) k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
-  else k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xbase, outw, xinv, xbuf, partial, g, jf);
+  if (d == 3)
+    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
+  else if (d == 2)
+    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
+  else
+    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
   return cudaGetLastError();
 }
 
