@@ -129,8 +129,10 @@ __device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
 #define FM_FD_PREFETCH 1
 #endif
 
+// 3D: 2 x 256 threads per SM (<= 128 registers); 2D: 4 x 256 (<= 64; FD at
+// cfg2 3.59 ms with 2, 2.69 with 3, 2.34 with 4 CTAs per SM)
 template <int DIM, int MODEL, int CT>
-__global__ void __launch_bounds__(CT, 512 / CT)
+__global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
     k_tile_fd(TileArgs a, const double *__restrict__ v, const double *__restrict__ b, double eps,
               double *__restrict__ g, unsigned long long *badkey, ModelArgs mdl, int ech) {
   constexpr int NV = DIM + 1;
