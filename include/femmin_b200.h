@@ -216,6 +216,33 @@ int fm_dot(int64_t n, const double *a, const double *b, double *out, void *strea
 int fm_segment_sums(int64_t nseg, const double *vals, const int64_t *indx, double *out,
                     void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Hessian utilities (solver.py:344-398).                   */
+
+/* hessian_sparsity (solver.py:344-357): boolean pattern of the free-dof
+ * Hessian (node adjacency of the elements, d x d blocks, rows / columns =
+ * positions in dofs_minim) as CSR with ascending columns.  indptr
+ * (nfree_dofs + 1) may be NULL to query *nnz_host; indices (nnz) NULL skips
+ * the column pass. */
+int fm_hessian_pattern(int64_t nn, int64_t ne, int nv, int d, const int64_t *conn,
+                       int64_t nfree_dofs, const int64_t *dofs_minim, int64_t *indptr,
+                       int64_t *indices, int64_t *nnz_host, void *stream);
+/* greedy_coloring (solver.py:360-376) contract: distance-2 colouring of a
+ * symmetric pattern (columns sharing a row get distinct colours); parallel
+ * rounds instead of the sequential greedy sweep, so the colours may differ. */
+int fm_color_d2(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t *colors,
+                int32_t *ncolors_host, void *stream);
+/* colored_fd_hessian (solver.py:379-398) steps: xp[cols of colour] += step on
+ * the full field vp; H[rows, col] = (g_pert - g0)[rows] / step for the
+ * pattern columns of that colour; out = (H + H^T) * 0.5 on the pattern. */
+int fm_hess_perturb(int64_t nfree_dofs, const int64_t *dofs_minim, const int32_t *colors,
+                    int color, double step, double *vp, void *stream);
+int fm_hess_scatter(int64_t n, const int64_t *indptr, const int64_t *indices,
+                    const int32_t *colors, int color, const double *g_pert, const double *g0,
+                    double step, double *vals, void *stream);
+int fm_hess_symmetrize(int64_t n, const int64_t *indptr, const int64_t *indices,
+                       const double *vals, double *out, void *stream);
+
 /* Arms two cudaEvent_t to be recorded around the next dominant kernel launch
  * of this context (tile kernel of fm_grad_exact / fm_grad_fd, element kernel
  * of fm_energy) on its stream; used by bench.py for the roofline timing. */

@@ -79,6 +79,11 @@ SIGNATURES = {
     "fm_descent_step": (C.c_int, [vp, vp, vp, dbl, vp]),
     "fm_descent": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, dbl, C.c_int, vp, vp, vp]),
     "fm_ctx_check": (C.c_int, [vp, vp, P64]),
+    "fm_hessian_pattern": (C.c_int, [i64, i64, C.c_int, C.c_int, vp, i64, vp, vp, vp, P64, vp]),
+    "fm_color_d2": (C.c_int, [i64, vp, vp, vp, C.POINTER(i32), vp]),
+    "fm_hess_perturb": (C.c_int, [i64, vp, vp, C.c_int, dbl, vp, vp]),
+    "fm_hess_scatter": (C.c_int, [i64, vp, vp, vp, C.c_int, vp, vp, dbl, vp, vp]),
+    "fm_hess_symmetrize": (C.c_int, [i64, vp, vp, vp, vp, vp]),
     "fm_ctx_launches": (i64, [vp]),
     "fm_ctx_time_next": (C.c_int, [vp, vp, vp]),
 }

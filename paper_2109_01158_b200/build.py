@@ -29,6 +29,7 @@ UNITS = {
     "fm_ctx.cu": [],
     "fm_eval_exact.cu": [],
     "fm_eval_ref.cu": [],
+    "fm_hessian.cu": [],
 }
 
 

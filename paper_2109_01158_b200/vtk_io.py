@@ -1,0 +1,123 @@
+"""Legacy ASCII VTK output of meshes, fields and element densities
+(vtk_io.py:1-96 of the reference).
+
+``write_vtk`` / ``read_vtk`` keep the reference's signatures and write the
+same bytes (DataFile Version 2.0, UNSTRUCTURED_GRID, 2D points padded with
+z = 0, cell types 5 / 10, SCALARS ... double 1 with shortest round-trip
+``repr`` values).  The rows are formatted with list joins instead of one
+``fh.write`` per line.  ``write_solution_vtk`` is the device-side caller: it
+takes CUDA tensors from the engine (the trial / solution field and the
+per-element densities of ``fm_energy``) and writes the file the reference's
+CLI writes for the benchmark solutions (cli.py:155-163, 188-196).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_CELL_TYPE = {3: 5, 4: 10}  # triangle, tetrahedron (vtk_io.py:7)
+
+
+def _fmt(values) -> str:
+    return "\n".join(map(repr, np.asarray(values, dtype=float).ravel().tolist()))
+
+
+def write_vtk(path, points, cells, point_data=None, cell_data=None, title="femmin"):
+    """Write an unstructured grid; 2D points are padded with z = 0
+    (vtk_io.py:10-40)."""
+    points = np.asarray(points, dtype=float)
+    cells = np.asarray(cells, dtype=np.int64)
+    if points.shape[1] == 2:
+        points = np.column_stack([points, np.zeros(points.shape[0])])
+    nv = cells.shape[1]
+    if nv not in _CELL_TYPE:
+        raise KeyError(nv)
+    out = ["# vtk DataFile Version 2.0", f"{title}", "ASCII", "DATASET UNSTRUCTURED_GRID",
+           f"POINTS {points.shape[0]} double"]
+    out += [f"{x!r} {y!r} {z!r}" for x, y, z in points.tolist()]
+    out.append(f"CELLS {cells.shape[0]} {cells.shape[0] * (nv + 1)}")
+    pre = f"{nv} "
+    out += [pre + " ".join(map(str, row)) for row in cells.tolist()]
+    out.append(f"CELL_TYPES {cells.shape[0]}")
+    ct = str(_CELL_TYPE[nv])
+    out += [ct] * cells.shape[0]
+    for kind, count, data in (("POINT_DATA", points.shape[0], point_data),
+                              ("CELL_DATA", cells.shape[0], cell_data)):
+        if data:
+            out.append(f"{kind} {count}")
+            for name, values in data.items():
+                out += [f"SCALARS {name} double 1", "LOOKUP_TABLE default"]
+                if np.asarray(values).size:
+                    out.append(_fmt(values))
+    with open(path, "w") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
+def read_vtk(path):
+    """Reader for files produced by :func:`write_vtk` (vtk_io.py:51-96).
+
+    Returns (points, cells, point_data, cell_data)."""
+    with open(path) as fh:
+        lines = [ln.strip() for ln in fh]
+    i = 0
+
+    def advance_to(prefix):
+        nonlocal i
+        while not lines[i].startswith(prefix):
+            i += 1
+
+    advance_to("POINTS")
+    npts = int(lines[i].split()[1])
+    points = np.array([[float(t) for t in lines[i + 1 + k].split()] for k in range(npts)])
+    i += 1 + npts
+    advance_to("CELLS")
+    ncells = int(lines[i].split()[1])
+    cells = np.array([[int(t) for t in lines[i + 1 + k].split()[1:]] for k in range(ncells)],
+                     dtype=np.int64)
+    i += 1 + ncells
+    point_data: dict[str, np.ndarray] = {}
+    cell_data: dict[str, np.ndarray] = {}
+    target, count = None, 0
+    while i < len(lines):
+        ln = lines[i]
+        if ln.startswith("POINT_DATA"):
+            target, count = point_data, npts
+        elif ln.startswith("CELL_DATA"):
+            target, count = cell_data, ncells
+        elif ln.startswith("SCALARS") and target is not None:
+            name = ln.split()[1]
+            target[name] = np.array([float(lines[i + 2 + k]) for k in range(count)])
+            i += 1 + count
+        i += 1
+    return points, cells, point_data, cell_data
+
+
+def write_solution_vtk(path, coords, conn, v, d, model=None, dm=None, b=None,
+                       densities=None, point_fields=None, title="femmin"):
+    """The benchmark solution files of the reference CLI (cli.py:155-163,
+    188-196): points = the field reshaped (nn, d) when d = dim (deformed
+    configuration), else the mesh coordinates with the field as point data;
+    cell data "density" = the per-element energy densities.  ``v``,
+    ``coords``, ``conn`` may be CUDA tensors; with ``dm`` (a DeviceMesh) and
+    ``model`` the densities are evaluated on the GPU (fm_energy)."""
+    import torch
+
+    def host(x):
+        return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+    if densities is None and dm is not None and model is not None:
+        dens = torch.empty(dm.ne, dtype=torch.float64, device="cuda")
+        vd = v if isinstance(v, torch.Tensor) and v.is_cuda else torch.as_tensor(
+            np.asarray(v, dtype=np.float64)).cuda()
+        dm.energy(vd, model, b, densities=dens)
+        densities = dens
+    coords_h, conn_h, v_h = host(coords), host(conn), host(v).astype(float)
+    dim = coords_h.shape[1]
+    pdata = dict(point_fields or {})
+    if d == dim:
+        points = v_h.reshape(-1, d)
+    else:
+        points = coords_h
+        pdata = {"u": v_h, **pdata}
+    cdata = {"density": host(densities)} if densities is not None else None
+    write_vtk(path, points, conn_h, point_data=pdata or None, cell_data=cdata, title=title)

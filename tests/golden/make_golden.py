@@ -248,11 +248,81 @@ def case_descent(nx=8, ny=4, nz=4, seed=2109, iters=20):
          ny=np.int64(ny), nz=np.int64(nz), seed=np.int64(seed))
 
 
+def case_hessian():
+    """hessian_sparsity, greedy_coloring and colored_fd_hessian (solver.py:344-398)
+    of the reference on lshape_problem(1) (p = 2 at v = 0, plus the stiffness
+    matrix the reference test compares with) and on the 8x4x4 config-4 beam
+    (Neo-Hookean at the seeded field), gradients by the reference's
+    exact_gradient."""
+    from femmin.solver import colored_fd_hessian, greedy_coloring, hessian_sparsity
+    out = {}
+    m = bench.lshape_problem(1)
+    pt = femmin.build_patches(m)
+    model = PLaplacian(PLaplaceParams(p=2.0), dim=2)
+    load = LinearLoad.assemble(m, -10.0, d=1)
+    pat = hessian_sparsity(m, d=1)
+    v = np.zeros(m.nn)
+
+    def gx(x):
+        vv = v.copy()
+        vv[m.dofs_minim] = x
+        return exact_gradient(vv, m, pt, model, load)
+
+    H = colored_fd_hessian(gx, np.zeros(m.dofs_minim.size), pat, step=1e-6).toarray()
+    K = bench.assemble_stiffness_matrix(m)[m.dofs_minim][:, m.dofs_minim].toarray()
+    out.update(l_indptr=pat.indptr.astype(np.int64), l_indices=pat.indices.astype(np.int64),
+               l_colors=greedy_coloring(pat), l_H=H, l_K=K)
+    om = O.beam_mesh(8, 4, 4, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    bm = fmesh._make_mesh(3, -1, om.nodes2coord, om.elems2nodes)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    bm = fmesh.mark_dirichlet(bm, spec, d=3)
+    bp = femmin.build_patches(bm)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    nh = NeoHookean(ElasticParams(E=E, nu=nu), dim=3)
+    nh.params = Lame(mu / 2, lam / 2)
+    bl = LinearLoad.assemble(bm, (0.0, 0.0, -2.5e7), d=3)
+    bv = np.ascontiguousarray(bm.nodes2coord).ravel().copy()
+    bv[bm.dofs_minim] += 1e-2 * (2.0 / 8) * (2.0 * O.uniform01(2109, bm.dofs_minim) - 1.0)
+    bpat = hessian_sparsity(bm, d=3)
+
+    def bgx(x):
+        vv = bv.copy()
+        vv[bm.dofs_minim] = x
+        return exact_gradient(vv, bm, bp, nh, bl)
+
+    bH = colored_fd_hessian(bgx, bv[bm.dofs_minim].copy(), bpat, step=1e-6).tocsr()
+    bH.sort_indices()
+    out.update(b_indptr=bpat.indptr.astype(np.int64), b_indices=bpat.indices.astype(np.int64),
+               b_colors=greedy_coloring(bpat), b_H_indptr=bH.indptr.astype(np.int64),
+               b_H_indices=bH.indices.astype(np.int64), b_H_data=bH.data, b_v=bv)
+    save("hessian", **out)
+
+
+def case_vtk():
+    """The reference writer's bytes (vtk_io.py) for the reference test
+    fixtures lshape_problem(1) (2D, point + cell data) and bar level 1 (3D)."""
+    from femmin import vtk_io
+    m = bench.lshape_problem(1)
+    rng = np.random.default_rng(20240817)
+    u = rng.normal(size=m.nn)
+    dens = rng.normal(size=m.ne)
+    vtk_io.write_vtk(os.path.join(HERE, "vtk_lshape1.vtk"), m.nodes2coord, m.elems2nodes,
+                     point_data={"u": u}, cell_data={"density": dens})
+    np.savez_compressed(os.path.join(HERE, "vtk_lshape1_data.npz"), coords=m.nodes2coord,
+                        conn=m.elems2nodes, u=u, density=dens)
+    b1 = bench.bar_problem(1)
+    vtk_io.write_vtk(os.path.join(HERE, "vtk_bar1.vtk"), b1.nodes2coord, b1.elems2nodes)
+    print("vtk fixtures written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # only the named cases, e.g. "descent"
         for name in sys.argv[1:]:
             globals()["case_" + name]()
         sys.exit(0)
+    case_hessian()
+    case_vtk()
     case_descent()
     case_minimize()
     case_small_shapes()
