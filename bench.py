@@ -251,9 +251,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # one process per GPU; FM_DIST_BACKEND=gloo (with ranks sharing a device
+    # when there are fewer GPUs than ranks) is only a functional smoke test of
+    # the multi-rank path on a one-GPU box, never a measurement
+    backend = os.environ.get("FM_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2109_01158_b200 import problems
     from paper_2109_01158_b200.parallel import SlabExchange, slab_range
 

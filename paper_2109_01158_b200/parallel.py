@@ -59,6 +59,9 @@ class SlabExchange:
         self.send_l, self.recv_l = mk(), mk()
         self.send_r, self.recv_r = mk(), mk()
         self.jall = torch.empty((world, 3), dtype=torch.float64, device=dev)
+        # NCCL moves device buffers; a gloo group (CPU tests, or the one-GPU
+        # functional smoke test of the multi-rank bench) needs host copies
+        self.host = dev.type == "cuda" and dist.get_backend(group) != "nccl"
 
     @classmethod
     def from_problem(cls, pr, rank, world, group=None):
@@ -68,25 +71,35 @@ class SlabExchange:
 
     def reduce(self, g: torch.Tensor, J: torch.Tensor | None = None):
         """In place: g += neighbours' interface partials; J <- global J."""
-        ops = []
+        ops, recvs = [], []
+        h = (lambda t: t.cpu()) if self.host else (lambda t: t)  # noqa: E731
         if self.left is not None:
             torch.index_select(g, 0, self.left, out=self.send_l)
-            ops += [dist.P2POp(dist.isend, self.send_l, self.rank - 1, self.group),
-                    dist.P2POp(dist.irecv, self.recv_l, self.rank - 1, self.group)]
+            rl = h(self.recv_l)
+            ops += [dist.P2POp(dist.isend, h(self.send_l), self.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, rl, self.rank - 1, self.group)]
+            recvs.append((self.left, self.recv_l, rl))
         if self.right is not None:
             torch.index_select(g, 0, self.right, out=self.send_r)
-            ops += [dist.P2POp(dist.isend, self.send_r, self.rank + 1, self.group),
-                    dist.P2POp(dist.irecv, self.recv_r, self.rank + 1, self.group)]
+            rr = h(self.recv_r)
+            ops += [dist.P2POp(dist.isend, h(self.send_r), self.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, rr, self.rank + 1, self.group)]
+            recvs.append((self.right, self.recv_r, rr))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        if self.left is not None:
-            g.index_add_(0, self.left, self.recv_l)
-        if self.right is not None:
-            g.index_add_(0, self.right, self.recv_r)
+        for pos, buf, got in recvs:
+            if got is not buf:
+                buf.copy_(got)
+            g.index_add_(0, pos, buf)
         if J is not None:
-            dist.all_gather_into_tensor(self.jall, J.reshape(1, 3).contiguous(),
-                                        group=self.group)
+            if self.host:
+                ja = self.jall.cpu()
+                dist.all_gather_into_tensor(ja, J.reshape(1, 3).cpu(), group=self.group)
+                self.jall.copy_(ja)
+            else:
+                dist.all_gather_into_tensor(self.jall, J.reshape(1, 3).contiguous(),
+                                            group=self.group)
             acc = self.jall[0].clone()
             for r in range(1, self.world):
                 acc += self.jall[r]
