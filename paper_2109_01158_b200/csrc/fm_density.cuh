@@ -103,6 +103,42 @@ __device__ __forceinline__ double density(const double (&F)[MODEL == FM_MODEL_NE
   }
 }
 
+// log(det) of a perturbed state from its unperturbed row's det0, 1/det0 and
+// ld0 = log(det0): ld0 + log1p(x), x = (det - det0) / det0 (the subtraction is
+// exact for det within a factor 2 of det0), log1p by its Taylor polynomial to
+// x^7 when |x| < 1e-3 (relative truncation < 1.5e-19); otherwise log(det).
+// The error stays within a few ulps of log(det), the libm term the FD
+// tolerance already allows for.
+__device__ __forceinline__ double log_near(double det, double det0, double rdet0, double ld0) {
+  const double x = (det - det0) * rdet0;
+  if (!(fabs(x) < 1e-3)) return log(det);  // also det0 <= 0 (NaN ld0, huge x)
+  double p = fma(x, 1.0 / 7.0, -1.0 / 6.0);
+  p = fma(p, x, 1.0 / 5.0);
+  p = fma(p, x, -0.25);
+  p = fma(p, x, 1.0 / 3.0);
+  p = fma(p, x, -0.5);
+  p = fma(p, x, 1.0);
+  return ld0 + p * x;
+}
+
+// Neo-Hookean W of a perturbed FD state (density() with log_near).
+template <int DIM>
+__device__ __forceinline__ double density_nh_near(const double (&F)[DIM][DIM], const ModelArgs &m,
+                                                  double det0, double rdet0, double ld0) {
+  double det = det_F<DIM>(F);
+  double I1 = rmul(F[0][0], F[0][0]);
+#pragma unroll
+  for (int j = 0; j < DIM; ++j)
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+      if (j + k > 0) I1 = radd(I1, rmul(F[j][k], F[j][k]));
+  if (!(det > 0.0)) return INFINITY;
+  double ld = log_near(det, det0, rdet0, ld0);
+  double dm1 = rsub(det, 1.0);
+  return radd(rmul(m.C1, rsub(rsub(I1, (double)DIM), rmul(2.0, ld))),
+              rmul(m.D1, rmul(dm1, dm1)));
+}
+
 // dW/dF; sets bad when det <= 0 (Neo-Hookean).
 template <int DIM, int MODEL>
 __device__ __forceinline__ void ddensity(const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],

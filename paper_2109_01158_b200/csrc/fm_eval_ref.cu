@@ -93,8 +93,13 @@ struct FdLayout {
   __host__ __device__ static size_t fbuf(int D) { return r16((size_t)CT * D * DIM * 8); }
   __host__ __device__ static size_t stg(int D, int ech) { return (size_t)D * ech * 16; }
   __host__ __device__ static size_t flat(int blk_cap) { return r16((size_t)blk_cap * 2); }
+  // 3D Neo-Hookean: per row det0, 1/det0, log(det0) of the unperturbed F
+  // (2D: register-bound at 4 CTAs per SM, the reuse spills; measured slower)
+  __host__ __device__ static size_t lrow(int D) {
+    return D == DIM && DIM == 3 ? (size_t)CT * 3 * 8 : 0;
+  }
   __host__ __device__ static size_t total(int D, int cap, int ech, int blk_cap) {
-    return nodev(D, cap) + recs() + fbuf(D) + stg(D, ech) + flat(blk_cap) + 32 * 4;
+    return nodev(D, cap) + recs() + fbuf(D) + lrow(D) + stg(D, ech) + flat(blk_cap) + 32 * 4;
   }
 };
 
@@ -148,7 +153,8 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
   double *nodev = reinterpret_cast<double *>(smem);
   unsigned char *recs = smem + L::nodev(D, CAP);
   double *Fb = reinterpret_cast<double *>(recs + L::recs());
-  double2 *stg = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(Fb) + L::fbuf(D));
+  double *lrow = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(Fb) + L::fbuf(D));
+  double2 *stg = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(lrow) + L::lrow(D));
   uint16_t *flat = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stg) +
                                                 L::stg(D, ech));
   int *wsum = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(flat) + L::flat(a.blk_cap));
@@ -212,6 +218,14 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
       for (int j = 0; j < D; ++j)
 #pragma unroll
         for (int m = 0; m < DIM; ++m) Fb[tid * NF + j * DIM + m] = F[j][m];
+      if constexpr (MODEL == FM_MODEL_NEOHOOKEAN && DIM == 3) {
+        // the row's log(det F) once: the 2 D perturbed states of each of its
+        // entries differ from it by O(eps) (log_near)
+        const double det0 = det_F<DIM>(F);
+        lrow[tid] = det0;
+        lrow[CT + tid] = 1.0 / det0;
+        lrow[2 * CT + tid] = det0 > 0.0 ? log(det0) : NAN;
+      }
     }
     // next chunk: its storage ids now, its own records towards L2
     s_next = row_src(e + CT);
@@ -306,7 +320,11 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
               Fp[j][m] = l == 1 ? radd(radd(q1[m], q2[m]), pl) : radd(radd(pl, q1[m]), q2[m]);
             }
           }
-          const double W = density<DIM, MODEL>(Fp, mdl);
+          double W;
+          if constexpr (MODEL == FM_MODEL_NEOHOOKEAN && DIM == 3)
+            W = density_nh_near<DIM>(Fp, mdl, lrow[r], lrow[CT + r], lrow[2 * CT + r]);
+          else
+            W = density<DIM, MODEL>(Fp, mdl);
           if (!isfinite(W)) {
             const int node = __ldg(a.closure + tm.clo_begin + cl);
             const int te = r + c0;
