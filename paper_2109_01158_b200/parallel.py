@@ -7,8 +7,8 @@ Because J, the consistent load b and the element contributions to grad J are
 all sums over elements, each rank's slab-local results are exact partial sums:
 
 * J       = sum over ranks of the local J (elastic part and b.v both split by
-            elements) -> all-gather of 3 doubles, summed in rank order, so every
-            rank holds the same bits;
+            elements) -> all-gather of 3 doubles, summed by one fixed reduction
+            on every rank, so every rank holds the same bits;
 * grad J  = local value at interior nodes; at an interface node the sum of the
             two neighbours' partials, exchanged as one plane buffer
             (ny+1)(nz+1)*3 doubles per side over NCCL send/recv and added as
@@ -54,10 +54,14 @@ class SlabExchange:
                      if rank > 0 else None)
         self.right = (plane_dof_positions(plane_nodes(nxl, nxl, ny, nz, dev), d, dofs_minim)
                       if rank < world - 1 else None)
+        # both planes packed / added back with one launch each: positions
+        # [left | right], send and receive buffers with the same layout
+        planes = [p for p in (self.left, self.right) if p is not None]
+        self.pos = torch.cat(planes) if planes else None
         n = (ny + 1) * (nz + 1) * d
-        mk = lambda: torch.empty(n, dtype=torch.float64, device=dev)  # noqa: E731
-        self.send_l, self.recv_l = mk(), mk()
-        self.send_r, self.recv_r = mk(), mk()
+        self.n = n
+        self.send = torch.empty(len(planes) * n, dtype=torch.float64, device=dev)
+        self.recv = torch.empty_like(self.send)
         self.jall = torch.empty((world, 3), dtype=torch.float64, device=dev)
         # NCCL moves device buffers; a gloo group (CPU tests, or the one-GPU
         # functional smoke test of the multi-rank bench) needs host copies
@@ -70,28 +74,26 @@ class SlabExchange:
                    mt["dofs_minim"], rank, world, group)
 
     def reduce(self, g: torch.Tensor, J: torch.Tensor | None = None):
-        """In place: g += neighbours' interface partials; J <- global J."""
-        ops, recvs = [], []
-        h = (lambda t: t.cpu()) if self.host else (lambda t: t)  # noqa: E731
-        if self.left is not None:
-            torch.index_select(g, 0, self.left, out=self.send_l)
-            rl = h(self.recv_l)
-            ops += [dist.P2POp(dist.isend, h(self.send_l), self.rank - 1, self.group),
-                    dist.P2POp(dist.irecv, rl, self.rank - 1, self.group)]
-            recvs.append((self.left, self.recv_l, rl))
-        if self.right is not None:
-            torch.index_select(g, 0, self.right, out=self.send_r)
-            rr = h(self.recv_r)
-            ops += [dist.P2POp(dist.isend, h(self.send_r), self.rank + 1, self.group),
-                    dist.P2POp(dist.irecv, rr, self.rank + 1, self.group)]
-            recvs.append((self.right, self.recv_r, rr))
-        if ops:
+        """In place: g += neighbours' interface partials; J <- global J
+        (the all-gathered per-rank partials summed by one fixed reduction, the
+        same on every rank)."""
+        if self.pos is not None:
+            torch.index_select(g, 0, self.pos, out=self.send)
+            send = self.send.cpu() if self.host else self.send
+            recv = self.recv.cpu() if self.host else self.recv
+            ops, k = [], 0
+            for peer, plane in ((self.rank - 1, self.left), (self.rank + 1, self.right)):
+                if plane is None:
+                    continue
+                sl = slice(k * self.n, (k + 1) * self.n)
+                ops += [dist.P2POp(dist.isend, send[sl], peer, self.group),
+                        dist.P2POp(dist.irecv, recv[sl], peer, self.group)]
+                k += 1
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        for pos, buf, got in recvs:
-            if got is not buf:
-                buf.copy_(got)
-            g.index_add_(0, pos, buf)
+            if recv is not self.recv:
+                self.recv.copy_(recv)
+            g.index_add_(0, self.pos, self.recv)
         if J is not None:
             if self.host:
                 ja = self.jall.cpu()
@@ -100,8 +102,5 @@ class SlabExchange:
             else:
                 dist.all_gather_into_tensor(self.jall, J.reshape(1, 3).contiguous(),
                                             group=self.group)
-            acc = self.jall[0].clone()
-            for r in range(1, self.world):
-                acc += self.jall[r]
-            J.copy_(acc)
+            torch.sum(self.jall, 0, out=J)
         return g, J
