@@ -145,10 +145,12 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
       fac = np_scalar_pow(n2, m.e_dw);
     else
       fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
+    // W = |g|^p / p = |g|^(p-2) |g|^2 / p from the gradient's factor: no second
+    // pow (a few ulps from pow(n2, p/2) / p; J is compared at 1e-10)
+    if (want_w) W = fac * n2 / m.p;
     fac *= vol;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) P[0][k] = fac * F[0][k];
-    if (want_w) W = np_scalar_pow(n2, m.e_w) / m.p;
   }
 }
 
