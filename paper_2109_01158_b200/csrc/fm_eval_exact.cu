@@ -109,10 +109,10 @@ __device__ __forceinline__ void cof_F_fma(const double (&F)[DIM][DIM], double (&
 // configs) by the atanh series 2 s (1 + z/3 + ... + z^7/15), s = (det-1)/(det+1),
 // z = s^2 <= 0.0035 (truncation < 1e-18 relative; det - 1 is exact), Estrin
 // evaluated; libm log elsewhere.  A few ulps, against J's 1e-10 tolerance.
-__device__ __forceinline__ double log_fused(double det) {
+__device__ __forceinline__ double log_fused(double det, double inv_dp1) {
   const double x = det - 1.0;
   if (!(fabs(x) < 0.125)) return log(det);
-  const double s = x / (det + 1.0);
+  const double s = x * inv_dp1;  // x / (det + 1)
   const double z = s * s, z2 = z * z, z4 = z2 * z2;
   const double a = fma(z, 1.0 / 3.0, 1.0), b = fma(z, 1.0 / 7.0, 1.0 / 5.0);
   const double c = fma(z, 1.0 / 11.0, 1.0 / 9.0), d = fma(z, 1.0 / 15.0, 1.0 / 13.0);
@@ -134,7 +134,10 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
 #pragma unroll
     for (int k = 0; k < DIM; ++k) det = fma(F[0][k], C[0][k], det);
     bad = !(det > 0.0);
-    const double rdet = 1.0 / det;
+    // 1/det and (for J) 1/(det+1) from one division
+    const double dp1 = det + 1.0;
+    const double R = 1.0 / (det * dp1);
+    const double rdet = dp1 * R;
     const double a = 2.0 * m.C1 * vol;
     const double bc = vol * (2.0 * m.D1 * (det - 1.0) - 2.0 * m.C1 * rdet);
 #pragma unroll
@@ -149,7 +152,8 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
         for (int k = 0; k < DIM; ++k) I1 = fma(F[j][k], F[j][k], I1);
       const double dm1 = det - 1.0;
       W = bad ? INFINITY
-              : m.C1 * ((I1 - (double)DIM) - 2.0 * log_fused(det)) + m.D1 * (dm1 * dm1);
+              : m.C1 * ((I1 - (double)DIM) - 2.0 * log_fused(det, det * R)) +
+                    m.D1 * (dm1 * dm1);
     }
   } else {
     bad = false;
