@@ -108,10 +108,11 @@ __device__ __forceinline__ void cof_F_fma(const double (&F)[DIM][DIM], double (&
 // log(det) for the fused J: near 1 (|det - 1| < 1/8, the elastic states of the
 // configs) by the atanh series 2 s (1 + z/3 + ... + z^7/15), s = (det-1)/(det+1),
 // z = s^2 <= 0.0035 (truncation < 1e-18 relative; det - 1 is exact), Estrin
-// evaluated; libm log elsewhere.  A few ulps, against J's 1e-10 tolerance.
-__device__ __forceinline__ double log_fused(double det, double inv_dp1) {
+// evaluated, branch-free so that it interleaves with the contributions; states
+// farther from 1 are corrected with libm's log after the contributions are
+// staged (W += 2 C1 (series - log det)).  A few ulps, against J's 1e-10.
+__device__ __forceinline__ double log_series(double det, double inv_dp1) {
   const double x = det - 1.0;
-  if (!(fabs(x) < 0.125)) return log(det);
   const double s = x * inv_dp1;  // x / (det + 1)
   const double z = s * s, z2 = z * z, z4 = z2 * z2;
   const double a = fma(z, 1.0 / 3.0, 1.0), b = fma(z, 1.0 / 7.0, 1.0 / 5.0);
@@ -126,7 +127,8 @@ template <int DIM, int MODEL>
 __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
                                           double vol, const ModelArgs &m, bool want_w,
                                           double (&P)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
-                                          double &W, bool &bad) {
+                                          double &W, bool &bad, bool &far, double &det_out,
+                                          double &ls_out) {
   if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
     double C[DIM][DIM];
     cof_F_fma<DIM>(F, C);
@@ -151,9 +153,12 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
 #pragma unroll
         for (int k = 0; k < DIM; ++k) I1 = fma(F[j][k], F[j][k], I1);
       const double dm1 = det - 1.0;
-      W = bad ? INFINITY
-              : m.C1 * ((I1 - (double)DIM) - 2.0 * log_fused(det, det * R)) +
-                    m.D1 * (dm1 * dm1);
+      const double ls = log_series(det, det * R);
+      W = bad ? INFINITY : m.C1 * ((I1 - (double)DIM) - 2.0 * ls) + m.D1 * (dm1 * dm1);
+      // far from 1: the caller adds 2 C1 (ls - log det) later
+      far = !bad && !(fabs(dm1) < 0.125);
+      det_out = det;
+      ls_out = ls;
     }
   } else {
     bad = false;
@@ -168,6 +173,8 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
     // W = |g|^p / p = |g|^(p-2) |g|^2 / p from the gradient's factor: no second
     // pow (a few ulps from pow(n2, p/2) / p; J is compared at 1e-10)
     if (want_w) W = fac * n2 / m.p;
+    far = false;
+    det_out = ls_out = 0.0;
     fac *= vol;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) P[0][k] = fac * F[0][k];
@@ -413,6 +420,8 @@ __global__ void __launch_bounds__(CT, MINB)
         const int e = c0 + tid;
         const bool valid = e < ne_t && !(mdl.dbg & 8);  // 8: data-movement-only probe
         double P[D][DIM];
+        double Wel = 0.0, det_el = 1.0, ls_el = 0.0;  // this element's W (J) and its log fix-up
+        bool far = false;
         Elem<DIM> E;
         if (valid) {
           load_elem_smem<DIM>(stg(s), tid, E);
@@ -433,11 +442,9 @@ __global__ void __launch_bounds__(CT, MINB)
 #pragma unroll
               for (int m = 0; m < DIM; ++m) P[k][m] = F[k][m];
           } else if (has_nodes) {
-            double W = 0.0;
             bool bad;
-            element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, W, bad);
+            element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, Wel, bad, far, det_el, ls_el);
             bad_any |= bad;
-            if (WJ && own) jsum += E.vol * W;
           } else if (WJ) {
             jsum += E.vol * density<DIM, MODEL>(F, mdl);
           }
@@ -454,6 +461,10 @@ __global__ void __launch_bounds__(CT, MINB)
               for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
               stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
             }
+          if (WJ) {
+            if (far) Wel += 2.0 * mdl.C1 * (ls_el - log(det_el));
+            jsum += E.vol * Wel;
+          }
         }
         TRACE(2);
         __syncthreads();  // contributions staged; every record of stage s read
