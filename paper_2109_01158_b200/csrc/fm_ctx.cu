@@ -805,6 +805,8 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     CK(cudaMemcpyAsync(&nfd, c->free_out + nfree, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->nfree_dofs = nfd;
+    CK(dmalloc(&c->dof_pos, std::max(nfd, 1), &B));
+    CK(launch_dof_pos(nfree, d, c->free_node, c->free_out, c->free_mask, c->dof_pos, s));
     // nodes outside every tile (all components fixed): their b.v goes to the
     // fused path's finalize
     Scratch fl, nsel;
@@ -1531,7 +1533,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
-                  c->xnodes};
+                  c->xnodes,    c->dof_pos};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1625,8 +1627,7 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
 
 int fm_descent_step(fm_ctx *c, double *v, const double *g, double alpha, void *stream) {
   FM_ARG(c && v && g, "null argument");
-  FM_CUDA(launch_descent(c->nfree, c->d, c->free_node, c->free_out, c->free_mask, g, alpha, v,
-                         as_stream(stream)));
+  FM_CUDA(launch_descent(c->nfree_dofs, c->dof_pos, g, alpha, v, as_stream(stream)));
   c->launches++;
   return FM_OK;
 }

@@ -263,6 +263,7 @@ struct fm_ctx {
   int32_t *free_node = nullptr, *free_out = nullptr, *rank_of = nullptr;
   int32_t *storage_to_orig = nullptr;
   uint8_t *free_mask = nullptr;
+  int32_t *dof_pos = nullptr;  // free dof q -> its index in v (descent update)
   uint16_t *xkey = nullptr;                        // cross-tile exchange (see TileArgs)
   int32_t *xpos = nullptr, *xchunk = nullptr;
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries

@@ -377,18 +377,26 @@ size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct, int blk_cap) {
 }
 
 // ----------------------------------------------------------------- descent
-__global__ void k_descent(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
-                          const uint8_t *free_mask, const double *g, double alpha, double *v) {
+// free dof q (the order of g and dofs_minim) -> its position in v
+__global__ void k_dof_pos(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
+                          const uint8_t *free_mask, int32_t *dof_pos) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nfree;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t node = free_node[r];
     const int mask = free_mask[r];
     int o = free_out[r];
     for (int j = 0; j < d; ++j)
-      if (mask & (1 << j)) {
-        v[node * d + j] = rsub(v[node * d + j], rmul(alpha, g[o]));
-        ++o;
-      }
+      if (mask & (1 << j)) dof_pos[o++] = (int32_t)(node * d + j);
+  }
+}
+
+// v[dof_pos[q]] -= alpha g[q]: one thread per free dof, g read coalesced
+__global__ void k_descent(int64_t nfd, const int32_t *__restrict__ dof_pos,
+                          const double *__restrict__ g, double alpha, double *__restrict__ v) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nfd;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = __ldg(dof_pos + q);
+    v[i] = rsub(v[i], rmul(alpha, __ldg(g + q)));
   }
 }
 
@@ -457,11 +465,15 @@ cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, i
   return fd_ct<3, FM_MODEL_NEOHOOKEAN>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
 }
 
-cudaError_t launch_descent(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
-                           const uint8_t *free_mask, const double *g, double alpha, double *v,
-                           cudaStream_t s) {
-  k_descent<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, d, free_node, free_out, free_mask, g,
-                                                 alpha, v);
+cudaError_t launch_dof_pos(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
+                           const uint8_t *free_mask, int32_t *dof_pos, cudaStream_t s) {
+  k_dof_pos<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, d, free_node, free_out, free_mask, dof_pos);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_descent(int64_t nfd, const int32_t *dof_pos, const double *g, double alpha,
+                           double *v, cudaStream_t s) {
+  k_descent<<<grid_for(nfd, 256), 256, 0, s>>>(nfd, dof_pos, g, alpha, v);
   return cudaGetLastError();
 }
 

@@ -58,8 +58,9 @@ cudaError_t launch_dot(const double *a, const double *b, int64_t n, int nblocks,
 cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, double *out,
                             cudaStream_t s);
 
-cudaError_t launch_descent(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
-                           const uint8_t *free_mask, const double *g, double alpha, double *v,
-                           cudaStream_t s);
+cudaError_t launch_dof_pos(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
+                           const uint8_t *free_mask, int32_t *dof_pos, cudaStream_t s);
+cudaError_t launch_descent(int64_t nfd, const int32_t *dof_pos, const double *g, double alpha,
+                           double *v, cudaStream_t s);
 
 }  // namespace fm
