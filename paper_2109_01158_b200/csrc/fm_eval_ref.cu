@@ -86,7 +86,10 @@ __global__ void __launch_bounds__(1024) k_finalize(const double *__restrict__ jp
 template <int DIM, int CT>
 struct FdLayout {
   // expanded shared-memory rows: vol | dphi[DIM][DIM + 1] | loc word
-  static constexpr int FRB = 8 * (2 + DIM * (DIM + 1));
+  // (2D: +1 pad double, an odd number of 8-byte words per row, so the
+  // row-per-lane stores of the rows phase hit distinct bank pairs: cfg3 FD
+  // 0.52 -> 0.45 ms; in 3D the pad was slower, 6.89 -> 7.08 ms)
+  static constexpr int FRB = 8 * (2 + DIM * (DIM + 1) + (DIM == 2 ? 1 : 0));
   __host__ __device__ static size_t r16(size_t x) { return (x + 15) / 16 * 16; }
   __host__ __device__ static size_t nodev(int D, int cap) { return r16((size_t)D * cap * 8); }
   __host__ __device__ static size_t recs() { return (size_t)CT * FRB; }
