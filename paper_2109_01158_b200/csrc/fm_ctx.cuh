@@ -181,8 +181,12 @@ struct ModelArgs {
                      // gathers; results are wrong on purpose), 0 = off
 };
 
+// x ** e with numpy's fast scalar cases (-1, 0, 0.5, 1, 2) and, beyond numpy,
+// 1.5 as x sqrt(x) (the p = 3 energy; <= 2 ulps of pow(x, 1.5), within the
+// libm term of every tolerance); other exponents through pow
 __device__ __forceinline__ double np_scalar_pow(double x, double e) {
   if (e == 0.5) return sqrt(x);
+  if (e == 1.5) return x * sqrt(x);
   if (e == 1.0) return x;
   if (e == 2.0) return x * x;
   if (e == -1.0) return 1.0 / x;

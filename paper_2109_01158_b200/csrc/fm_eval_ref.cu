@@ -326,13 +326,6 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
           double W;
           if constexpr (MODEL == FM_MODEL_NEOHOOKEAN && DIM == 3) {
             W = density_nh_near<DIM>(Fp, mdl, lrow[r], lrow[CT + r], lrow[2 * CT + r]);
-          } else if constexpr (MODEL == FM_MODEL_PLAPLACE) {
-            // |g|^p / p; p = 3 as n2 sqrt(n2) (<= 2 ulps of libm's pow(n2, 1.5),
-            // within the FD tolerance's libm term), other p as numpy
-            double n2 = rmul(Fp[0][0], Fp[0][0]);
-#pragma unroll
-            for (int k = 1; k < DIM; ++k) n2 = radd(n2, rmul(Fp[0][k], Fp[0][k]));
-            W = (mdl.e_w == 1.5 ? n2 * sqrt(n2) : np_scalar_pow(n2, mdl.e_w)) / mdl.p;
           } else {
             W = density<DIM, MODEL>(Fp, mdl);
           }
