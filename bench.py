@@ -348,27 +348,54 @@ def main():
     dm.check()
 
     extras = {}
-    if args.extras and world == 1:
+    if args.extras:
         # secondary kernels on the same problem: energy-only pass and FD gradient
+        # (with N ranks: each rank's slab, the slab partials reduced across ranks
+        # like the exact gradient's; times are the max over ranks)
         def timed(fn, n):
             fn()
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             for _ in range(n):
                 fn()
             a1.record(stream)
             torch.cuda.synchronize()
-            return a0.elapsed_time(a1) / n
-        e_ms = timed(lambda: dm.energy(v, model, b, out=J), 20)
-        fd_ms = timed(lambda: dm.numeric_gradient(v, model, b, 1e-8, g=torch.empty_like(g)), 3)
-        go_ms = timed(lambda: dm.exact_gradient(v, model, b, g=g), 20)
+            t = a0.elapsed_time(a1) / n
+            if world > 1:
+                tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt[0])
+            return t
+        gfd = torch.empty_like(g)
+
+        def energy_step():
+            dm.energy(v, model, b, out=J)
+            if ex is not None:
+                ex.reduce(None, J)
+
+        def fd_step():
+            dm.numeric_gradient(v, model, b, 1e-8, g=gfd)
+            if ex is not None:
+                ex.reduce(gfd)
+
+        def grad_step():
+            dm.exact_gradient(v, model, b, g=g)
+            if ex is not None:
+                ex.reduce(g)
+
+        e_ms = timed(energy_step, 20)
+        fd_ms = timed(fd_step, 3)
+        go_ms = timed(grad_step, 20)
         extras = {"energy_only_ms": e_ms, "energy_only_Melem_s": ne_total / e_ms / 1e3,
                   "fd_grad_ms": fd_ms, "fd_grad_Melem_s": ne_total / fd_ms / 1e3,
                   "grad_only_ms": go_ms,
-                  "fd_W_evals_per_s": 2 * dm.d * dm.stats["node_entries_total"] / (fd_ms * 1e-3)}
+                  "fd_W_evals_per_s": 2 * dm.d * dm.stats["node_entries_total"] * world
+                  / (fd_ms * 1e-3)}
         dm.check()
-        if "dofs_minim" in pr.meta:
+        if "dofs_minim" in pr.meta and world == 1:
             # a few trust-region iterations of the device-resident minimizer
             # from the benchmark field: wall time per
             # gradient call (each CG step is one Hessian-vector product = 2)

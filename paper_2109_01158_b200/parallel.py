@@ -73,11 +73,11 @@ class SlabExchange:
         return cls(mt["nx"], mt["ny"], mt["nz"], mt["ix0"], mt["ix1"], pr.dm.d,
                    mt["dofs_minim"], rank, world, group)
 
-    def reduce(self, g: torch.Tensor, J: torch.Tensor | None = None):
+    def reduce(self, g: torch.Tensor | None, J: torch.Tensor | None = None):
         """In place: g += neighbours' interface partials; J <- global J
         (the all-gathered per-rank partials summed by one fixed reduction, the
-        same on every rank)."""
-        if self.pos is not None:
+        same on every rank).  Either may be None."""
+        if g is not None and self.pos is not None:
             torch.index_select(g, 0, self.pos, out=self.send)
             send = self.send.cpu() if self.host else self.send
             recv = self.recv.cpu() if self.host else self.recv
