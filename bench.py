@@ -404,6 +404,11 @@ def main():
                             SolveOptions(max_iters=1, max_cg=2))
             res = minimize_device(dm, model, b, v, pr.meta["dofs_minim"],
                                   SolveOptions(max_iters=3, max_cg=20))
+            rx = minimize_device(dm, model, b, v, pr.meta["dofs_minim"],
+                                 SolveOptions(max_iters=3, max_cg=20, hvp="exact"))
+            hp_ms = timed(lambda: dm.hvp(v, v, model, out=g), 20)  # kernel timing only
+            extras.update({"tr_exact_hvp_3iters_s": rx.time, "tr_exact_hvp_calls": rx.n_hvp,
+                           "tr_exact_hvp_J_end": rx.J_u, "hvp_exact_ms": hp_ms})
             extras.update({"tr_3iters_s": res.time, "tr_grad_calls": res.n_grad,
                            "tr_energy_calls": res.n_energy,
                            "tr_ms_per_grad_call": res.time / max(1, res.n_grad) * 1e3,

@@ -177,6 +177,14 @@ int fm_energy(fm_ctx *ctx, const fm_model *model, const double *v, const double 
 int fm_grad_exact(fm_ctx *ctx, const fm_model *model, const double *v, const double *b,
                   double *g_out, double *J_out, void *stream);
 
+/* Exact Hessian-vector product (new; SURVEY §8f row 4 "exact HVP via d2W"):
+ * hp_out (|dofs_minim|,) = d(grad J)(v)[p] = sum_k vol_k d2W/dF2(F_k) : grad p
+ * contracted with the basis gradients, on the free dofs; p is a full field
+ * (d*nn) that must be zero on the Dirichlet dofs.  det F <= 0 latches like
+ * fm_grad_exact.  One fused launch (+ the finishing pass), the same tiles. */
+int fm_hvp_exact(fm_ctx *ctx, const fm_model *model, const double *v, const double *p,
+                 double *hp_out, void *stream);
+
 /* numeric_gradient (gradients.py:84-121): nodal-patch central differences. */
 int fm_grad_fd(fm_ctx *ctx, const fm_model *model, const double *v, const double *b,
                double eps, double *g_out, void *stream);

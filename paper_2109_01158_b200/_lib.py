@@ -76,6 +76,7 @@ SIGNATURES = {
     "fm_energy": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, vp, vp, vp]),
     "fm_grad_exact": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, vp, vp, vp]),
     "fm_grad_fd": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, dbl, vp, vp]),
+    "fm_hvp_exact": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, vp, vp]),
     "fm_descent_step": (C.c_int, [vp, vp, vp, dbl, vp]),
     "fm_descent": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, dbl, C.c_int, vp, vp, vp]),
     "fm_ctx_check": (C.c_int, [vp, vp, P64]),

@@ -1585,8 +1585,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
     FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
-                              c->table_bufs, wj, v, b, g, c->jpart, c->dotpart, c->status, ma,
-                              s));
+                              c->table_bufs, wj ? 1 : 0, v, b, g, c->jpart, c->dotpart,
+                              c->status, ma, s));
     c->launches++;
   }
   if (c->n_cross > 0 || wj) {
@@ -1598,6 +1598,38 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->n_xnodes : 0, c->xnodes,
                                 c->node_xbase, c->node_outw, c->xpos, c->xbuf, c->partial, g,
                                 jf, s));
+    c->launches++;
+  }
+  return FM_OK;
+}
+
+int fm_hvp_exact(fm_ctx *c, const fm_model *model, const double *v, const double *p, double *hp,
+                 void *stream) {
+  int st = check_model(c, model);
+  if (st) return st;
+  FM_ARG(v && p && hp, "null field, direction or output");
+  cudaStream_t s = as_stream(stream);
+  ModelArgs ma = model_args(model);
+  TileArgs ta = c->tile_args();
+  ta.n_tiles_all = c->n_tiles;  // no J: orphan tiles not needed
+  if (tile_exact_smem(c->dim, c->d, c->blk_cap, c->clo_cap, c->tile_nodes, c->node_bufs,
+                      c->table_bufs, 2 * c->d) > 227 * 1024) {
+    set_error("Hessian-vector tile staging exceeds shared memory; use smaller tiles");
+    return FM_INVALID_ARG;
+  }
+  const int grid = std::min(c->n_sm * c->ctas_per_sm, std::max(1, ta.n_tiles_all));
+  if (ta.n_tiles_all > 0) {
+    TimedLaunch tl(c, s);
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
+                              c->table_bufs, 2, v, p, hp, c->jpart, c->dotpart, c->status, ma,
+                              s));
+    c->launches++;
+  }
+  if (c->n_cross > 0) {
+    JFinal jf{c->jpart, c->dotpart, 0, c->fixed_nodes, 0, nullptr, v, c->fpart, c->ticket,
+              nullptr};
+    FM_CUDA(launch_finish_cross(c->d, c->n_xnodes, c->xnodes, c->node_xbase, c->node_outw,
+                                c->xpos, c->xbuf, c->partial, hp, jf, s));
     c->launches++;
   }
   return FM_OK;

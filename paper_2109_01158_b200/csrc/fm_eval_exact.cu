@@ -76,8 +76,11 @@ struct PipeLayout {
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
   // nb node-value buffers, tb table buffers (2: the next tile's tables load a
   // tile ahead)
-  __host__ __device__ static size_t total(int D, int blk_cap, int clo_cap, int nb, int tb) {
-    return 2 * stage(blk_cap) + nb * nodev(D, clo_cap) + cids(clo_cap) + tb * tabs() +
+  // (dn: node-value components per node, D; 2 D for the Hessian-vector
+  // product, which gathers the direction's node values too)
+  __host__ __device__ static size_t total(int D, int blk_cap, int clo_cap, int nb, int tb,
+                                          int dn = 0) {
+    return 2 * stage(blk_cap) + nb * nodev(dn ? dn : D, clo_cap) + cids(clo_cap) + tb * tabs() +
            staging(D) + 32 * 8 + 8 * 8;
   }
 };
@@ -181,6 +184,72 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
   }
 }
 
+// Hessian-vector product per element: dP' = vol * d2W/dF2 : dF, the
+// derivative of element_P's P' along dF = grad p (models.py:103-138
+// differentiated once more).  NH: P' = a F + b C (a = 2 C1 vol, b = vol (2 D1
+// (det-1) - 2 C1/det), C = cof F) -> dP' = a dF + db C + b dC with
+// ddet = C : dF, db = vol (2 D1 + 2 C1/det^2) ddet, dC the cofactors'
+// derivative (bilinear minors).  p-Laplace: P' = vol f g, f = |g|^(p-2) ->
+// dP' = vol f (dg + (p-2) (g.dg)/|g|^2 g); at g = 0: vol f dg (f = [p == 2]).
+template <int DIM, int MODEL>
+__device__ __forceinline__ void element_dP(
+    const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
+    const double (&dF)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM], double vol,
+    const ModelArgs &m, double (&dP)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM], bool &bad) {
+  if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
+    double C[DIM][DIM], dC[DIM][DIM];
+    cof_F_fma<DIM>(F, C);
+    if constexpr (DIM == 2) {
+      cof_F_fma<DIM>(dF, dC);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int j1 = j == 0 ? 1 : 0, j2 = j == 2 ? 1 : 2;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int k1 = k == 0 ? 1 : 0, k2 = k == 2 ? 1 : 2;
+          const double t = fma(dF[j1][k1], F[j2][k2], F[j1][k1] * dF[j2][k2]) -
+                           fma(dF[j1][k2], F[j2][k1], F[j1][k2] * dF[j2][k1]);
+          dC[j][k] = ((j + k) & 1) ? -t : t;
+        }
+      }
+    }
+    double det = 0.0, ddet = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) det = fma(F[0][k], C[0][k], det);
+#pragma unroll
+    for (int j = 0; j < DIM; ++j)
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) ddet = fma(C[j][k], dF[j][k], ddet);
+    bad = !(det > 0.0);
+    const double rdet = 1.0 / det;
+    const double a = 2.0 * m.C1 * vol;
+    const double bc = vol * (2.0 * m.D1 * (det - 1.0) - 2.0 * m.C1 * rdet);
+    const double dbc = vol * (2.0 * m.D1 + 2.0 * m.C1 * rdet * rdet) * ddet;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j)
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) dP[j][k] = fma(a, dF[j][k], fma(dbc, C[j][k], bc * dC[j][k]));
+  } else {
+    bad = false;
+    double n2 = 0.0, gd = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      n2 = fma(F[0][k], F[0][k], n2);
+      gd = fma(F[0][k], dF[0][k], gd);
+    }
+    double fac;
+    if (m.p >= 2.0)
+      fac = np_scalar_pow(n2, m.e_dw);
+    else
+      fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
+    const double c2 = n2 > 0.0 ? (m.p - 2.0) * gd / n2 : 0.0;
+    fac *= vol;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) dP[0][k] = fac * fma(c2, F[0][k], dF[0][k]);
+  }
+}
+
 // F = grad v as chained FMAs (one DMUL + NV-1 DFMA per entry)
 template <int DIM, int D>
 __device__ __forceinline__ void grad_F_fma(const double (&vv)[D][DIM + 1],
@@ -221,13 +290,16 @@ struct Cursor {
   }
 };
 
-template <int DIM, int MODEL, bool WJ, int CT, int NB, int TB, int MINB>
+// HV: Hessian-vector product instead of the gradient; b then holds the
+// direction field p (full, zero on the Dirichlet dofs), there is no load term.
+template <int DIM, int MODEL, bool WJ, bool HV, int CT, int NB, int TB, int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, double *__restrict__ bvpart,
                  unsigned long long *status, ModelArgs mdl) {
   constexpr int NV = DIM + 1;
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
+  constexpr int DG = HV ? 2 * D : D;  // node-value components gathered per node
   constexpr int RB = RecBytes<DIM>::value;
   constexpr int NCH = RB / 16;
   using L = PipeLayout<DIM, CT>;
@@ -237,9 +309,9 @@ __global__ void __launch_bounds__(CT, MINB)
   // stage s at smem + s * SG; node-value buffer k at nodev0 + k * nodev()
   auto stg = [&](int s) { return smem + s * SG; };
   auto nodev = [&](int k) {
-    return reinterpret_cast<double *>(smem + 2 * SG + k * L::nodev(D, CAP));
+    return reinterpret_cast<double *>(smem + 2 * SG + k * L::nodev(DG, CAP));
   };
-  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * SG + NB * L::nodev(D, CAP));
+  int32_t *cids = reinterpret_cast<int32_t *>(smem + 2 * SG + NB * L::nodev(DG, CAP));
   unsigned char *tabs0 = reinterpret_cast<unsigned char *>(cids) + L::cids(CAP);
   auto desc_of = [&](int k) { return reinterpret_cast<int4 *>(tabs0 + k * L::tabs()); };
   auto xch_of = [&](int k) {  // the tile's exchange-item chunk starts
@@ -286,12 +358,12 @@ __global__ void __launch_bounds__(CT, MINB)
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
     double *dst = nodev(k);
     for (int i = tid; i < clo_count && !(mdl.dbg & 32); i += CT) {  // 32: probe without gathers
-      const double *src = v + (int64_t)cids[i] * D;
+      const int64_t off = (int64_t)cids[i] * D;
 #pragma unroll
-      for (int kk = 0; kk < D; ++kk)
+      for (int kk = 0; kk < DG; ++kk)  // HV: components D.. are the direction's
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                          smem_u32(dst + kk * CAP + i)),
-                     "l"(src + kk)
+                     "l"(kk < D ? v + off + kk : b + off + (kk - D))
                      : "memory");
     }
     cp_async_arrive_noinc(nfull + k);
@@ -394,7 +466,7 @@ __global__ void __launch_bounds__(CT, MINB)
         cl = __ldg(a.node_clo + tm.node_begin + tid);
         nd = desc[tid];
         outw = nd.w;
-        if (b) {
+        if (b && !HV) {
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
         }
@@ -441,6 +513,17 @@ __global__ void __launch_bounds__(CT, MINB)
             for (int k = 0; k < D; ++k)
 #pragma unroll
               for (int m = 0; m < DIM; ++m) P[k][m] = F[k][m];
+          } else if (HV && has_nodes) {
+            double pp[D][NV];
+#pragma unroll
+            for (int l = 0; l < NV; ++l)
+#pragma unroll
+              for (int k = 0; k < D; ++k) pp[k][l] = nv[(D + k) * CAP + E.loc[l]];
+            double dF[D][DIM];
+            grad_F_fma<DIM, D>(pp, E.g, dF);
+            bool bad;
+            element_dP<DIM, MODEL>(F, dF, E.vol, mdl, P, bad);
+            bad_any |= bad;
           } else if (has_nodes) {
             bool bad;
             element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, Wel, bad, far, det_el, ls_el);
@@ -653,64 +736,67 @@ cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const 
   return cudaGetLastError();
 }
 
-size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb) {
+size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
+                       int dn) {
   if (ct == 128)
-    return dim == 3 ? PipeLayout<3, 128>::total(d, blk_cap, clo_cap, nb, tb)
-                    : PipeLayout<2, 128>::total(d, blk_cap, clo_cap, nb, tb);
-  return dim == 3 ? PipeLayout<3, 256>::total(d, blk_cap, clo_cap, nb, tb)
-                  : PipeLayout<2, 256>::total(d, blk_cap, clo_cap, nb, tb);
+    return dim == 3 ? PipeLayout<3, 128>::total(d, blk_cap, clo_cap, nb, tb, dn)
+                    : PipeLayout<2, 128>::total(d, blk_cap, clo_cap, nb, tb, dn);
+  return dim == 3 ? PipeLayout<3, 256>::total(d, blk_cap, clo_cap, nb, tb, dn)
+                  : PipeLayout<2, 256>::total(d, blk_cap, clo_cap, nb, tb, dn);
 }
 
 template <int DIM, int MODEL, int CT, int NB, int TB>
-static cudaError_t launch_cfg(const TileArgs &a, int grid, bool wj, const double *v,
+static cudaError_t launch_cfg(const TileArgs &a, int grid, int mode, const double *v,
                               const double *b, double *g, double *jpart, double *bvpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int MINB = tile_exact_minb(DIM, CT);
-  const size_t smem = PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB);
-  auto k = wj ? k_tile_exact<DIM, MODEL, true, CT, NB, TB, MINB>
-              : k_tile_exact<DIM, MODEL, false, CT, NB, TB, MINB>;
+  const size_t smem =
+      PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB, mode == 2 ? 2 * D : D);
+  auto k = mode == 2   ? k_tile_exact<DIM, MODEL, false, true, CT, NB, TB, MINB>
+           : mode == 1 ? k_tile_exact<DIM, MODEL, true, false, CT, NB, TB, MINB>
+                       : k_tile_exact<DIM, MODEL, false, false, CT, NB, TB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, bvpart, status, m);
   return cudaGetLastError();
 }
 
 template <int DIM, int MODEL, int CT>
-static cudaError_t launch_ct(const TileArgs &a, int grid, int nb, int ns, bool wj,
+static cudaError_t launch_ct(const TileArgs &a, int grid, int nb, int ns, int mode,
                              const double *v, const double *b, double *g, double *jpart,
                              double *bvpart, unsigned long long *status, const ModelArgs &m,
                              cudaStream_t s) {
   if (nb == 2 && ns == 2)
-    return launch_cfg<DIM, MODEL, CT, 2, 2>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
-  if (nb == 2) return launch_cfg<DIM, MODEL, CT, 2, 1>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
-  if (ns == 2) return launch_cfg<DIM, MODEL, CT, 1, 2>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
-  return launch_cfg<DIM, MODEL, CT, 1, 1>(a, grid, wj, v, b, g, jpart, bvpart, status, m, s);
+    return launch_cfg<DIM, MODEL, CT, 2, 2>(a, grid, mode, v, b, g, jpart, bvpart, status, m, s);
+  if (nb == 2) return launch_cfg<DIM, MODEL, CT, 2, 1>(a, grid, mode, v, b, g, jpart, bvpart, status, m, s);
+  if (ns == 2) return launch_cfg<DIM, MODEL, CT, 1, 2>(a, grid, mode, v, b, g, jpart, bvpart, status, m, s);
+  return launch_cfg<DIM, MODEL, CT, 1, 1>(a, grid, mode, v, b, g, jpart, bvpart, status, m, s);
 }
 
 template <int DIM, int MODEL>
-static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, int ns, bool wj,
+static cudaError_t launch_exact_t(const TileArgs &a, int grid, int ct, int nb, int ns, int mode,
                                   const double *v, const double *b, double *g, double *jpart,
                                   double *bvpart, unsigned long long *status, const ModelArgs &m,
                                   cudaStream_t s) {
   if (ct == 128)
-    return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
-  return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, wj, v, b, g, jpart, bvpart, status, m, s);
+    return launch_ct<DIM, MODEL, 128>(a, grid, nb, ns, mode, v, b, g, jpart, bvpart, status, m, s);
+  return launch_ct<DIM, MODEL, 256>(a, grid, nb, ns, mode, v, b, g, jpart, bvpart, status, m, s);
 }
 
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
-                              int ns, bool wj, const double *v, const double *b, double *g,
+                              int ns, int mode, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s) {
   if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+    return launch_exact_t<2, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, mode, v, b, g, jpart, bvpart,
                                                 status, m, s);
   if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+    return launch_exact_t<3, FM_MODEL_PLAPLACE>(a, grid, ct, nb, ns, mode, v, b, g, jpart, bvpart,
                                                 status, m, s);
   if (dim == 2)
-    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart,
+    return launch_exact_t<2, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, mode, v, b, g, jpart,
                                                   bvpart, status, m, s);
-  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, wj, v, b, g, jpart, bvpart,
+  return launch_exact_t<3, FM_MODEL_NEOHOOKEAN>(a, grid, ct, nb, ns, mode, v, b, g, jpart, bvpart,
                                                 status, m, s);
 }
 

@@ -11,8 +11,9 @@ namespace fm {
 // persistent pipelined fused J + exact gradient; grid = ctas_per_sm * #SMs, CONSUMERS threads
 // ct = threads per CTA = chunk size = max tile nodes (128 or 256); nb = node-value buffers
 // tb = table buffers (2: the next tile's descriptors / entries load a tile ahead)
+// mode 0: gradient, 1: gradient + J, 2: Hessian-vector product (b = direction)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
-                              int tb, bool wj, const double *v, const double *b, double *g,
+                              int ns, int mode, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
                               const ModelArgs &m, cudaStream_t s);
 // CTAs per SM the fused tile kernel is compiled for (__launch_bounds__ min
@@ -40,7 +41,8 @@ cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const 
                                 const int32_t *outw,
                                 const int32_t *xinv, const double *xbuf, const double *partial,
                                 double *g, const JFinal &jf, cudaStream_t s);
-size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb);
+size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
+                       int dn = 0);
 
 cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
                            const double *v, const double *b, double eps, double *g,

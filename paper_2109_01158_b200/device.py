@@ -106,6 +106,16 @@ class DeviceMesh:
                                            stream_ptr()), "fm_grad_exact")
         return g
 
+    def hvp(self, v, p, model, out=None):
+        """Exact Hessian-vector product on the free dofs: d(grad J)(v)[p]
+        (fm_hvp_exact).  p: full field (d*nn,), zero on the Dirichlet dofs."""
+        if out is None:
+            out = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        m = _model(model)
+        _lib.check(self._lib.fm_hvp_exact(self._h, C.byref(m), ptr(v), ptr(p), ptr(out),
+                                          stream_ptr()), "fm_hvp_exact")
+        return out
+
     def numeric_gradient(self, v, model, b=None, eps=DEFAULT_EPS, g=None):
         """gradients.py:84-121 into g (nfree_dofs,)."""
         if g is None:

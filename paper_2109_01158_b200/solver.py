@@ -55,12 +55,18 @@ class SolveOptions:
     hvp_step: float | None = None  # None: sqrt(eps_mach) (1 + |x|) / |dir|
     lbfgs_memory: int = 10
     verbose: bool = False
+    # new (not in the reference): "exact" makes minimize_device's trust-region
+    # CG use the engine's exact Hessian-vector product (fm_hvp_exact, one
+    # launch) instead of central differences of two gradients
+    hvp: str = "fd"
 
     def __post_init__(self):
         if min(self.tol_g, self.tol_step, self.tol_f) <= 0:
             raise ValueError("tolerances must be positive")
         if self.solver not in ("tr", "lbfgs"):
             raise ValueError(f"unknown solver {self.solver!r}")
+        if self.hvp not in ("fd", "exact"):
+            raise ValueError(f"unknown Hessian-vector product {self.hvp!r}")
 
 
 @dataclass
@@ -128,7 +134,7 @@ def _steihaug(g, hvp, radius, rtol, maxiter):
     return z, False
 
 
-def _trust_region(fx, gx, x, f, opts):
+def _trust_region(fx, gx, x, f, opts, hx=None):
     g = gx(x)
     gn0 = _nrm_inf(g)
     gtol = opts.tol_g * max(1.0, gn0)
@@ -146,6 +152,8 @@ def _trust_region(fx, gx, x, f, opts):
         xnorm = _nrm(x)
 
         def hvp(p):
+            if hx is not None:  # exact product at x (admissible: f(x) is finite)
+                return hx(x, p)
             pn = _nrm(p)
             if pn == 0.0:
                 return torch.zeros_like(p)
@@ -241,12 +249,13 @@ def _lbfgs(fx, gx, x, f, opts):
     return x, f, it, _nrm_inf(g), converged, status
 
 
-def _run(fx, gx, x0, opts):
+def _run(fx, gx, x0, opts, hx=None):
     f0 = fx(x0)
     if not math.isfinite(f0):
         raise InvalidStartError("initial field has non-finite energy")
-    loop = _lbfgs if opts.solver == "lbfgs" else _trust_region
-    return loop(fx, gx, x0, f0, opts)
+    if opts.solver == "lbfgs":
+        return _lbfgs(fx, gx, x0, f0, opts)
+    return _trust_region(fx, gx, x0, f0, opts, hx)
 
 
 def minimize(J, g, v0, dofs_minim, opts: SolveOptions | None = None) -> MinimizeResult:
@@ -306,12 +315,22 @@ def minimize_device(dm, model, b, v0: torch.Tensor, dofs_minim: torch.Tensor,
         dm.check()
         return gr
 
+    hx = None
+    if opts.hvp == "exact":
+        pfull = torch.zeros_like(template)  # direction, zero on the Dirichlet dofs
+
+        def hx(x, p):
+            count["h"] = count.get("h", 0) + 1
+            return dm.hvp(embed(x), pfull.index_copy_(0, dofs, p), model)
+
     t0 = time.perf_counter()
-    x, f, it, gn, conv, status = _run(fx, gx, template.index_select(0, dofs), opts)
+    x, f, it, gn, conv, status = _run(fx, gx, template.index_select(0, dofs), opts, hx)
     torch.cuda.synchronize()
-    return MinimizeResult(u=template.index_copy(0, dofs, x), J_u=f, iters=it, grad_norm=gn,
-                          time=time.perf_counter() - t0, converged=conv, status=status,
-                          n_energy=count["f"], n_grad=count["g"])
+    res = MinimizeResult(u=template.index_copy(0, dofs, x), J_u=f, iters=it, grad_norm=gn,
+                         time=time.perf_counter() - t0, converged=conv, status=status,
+                         n_energy=count["f"], n_grad=count["g"])
+    res.n_hvp = count.get("h", 0)
+    return res
 
 
 def continuation_solve(J, g, v0, dofs_minim, dofs_dirichlet, dirichlet_values,

@@ -112,3 +112,70 @@ def test_solution_vtk_from_device(tmp_path):
     np.testing.assert_array_equal(cells, om.elems2nodes)
     W = O.energy(v, om, omodel, b)[1]
     np.testing.assert_allclose(cdata["density"], W, rtol=1e-13)
+
+
+def _embed(n_full, dofs, x):
+    p = torch.zeros(n_full, dtype=torch.float64, device="cuda")
+    p[torch.as_tensor(dofs, device="cuda")] = x
+    return p
+
+
+def test_exact_hvp_p2_is_stiffness(golden):
+    """fm_hvp_exact for p = 2 is the P1 stiffness matrix (the reference's
+    bench.assemble_stiffness_matrix, restricted to the free dofs)."""
+    h = golden("hessian")
+    m, g = _lshape1(golden)
+    P = fb.Patches(lengths=g["p_lengths"], elems=g["p_elems"], volumes=None, elems2nodes=None,
+                   dphi=None, logical=None, prefix=g["p_prefix"], slot=g["p_slot"])
+    model = fb.PLaplacian(fb.PLaplaceParams(p=2.0), dim=2)
+    dm = fb.context_for(m, P, d=1)
+    rng = np.random.default_rng(3)
+    v = torch.as_tensor(rng.normal(size=m.nn)).cuda()
+    x = rng.normal(size=m.dofs_minim.size)
+    hp = dm.hvp(v, _embed(m.nn, m.dofs_minim, torch.as_tensor(x).cuda()), model)
+    dm.check()
+    ref = h["l_K"] @ x
+    assert np.abs(hp.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("kind", ["beam", "lshape_p3", "lshape_p18", "rect"])
+def test_exact_hvp_vs_gradient_differences(kind):
+    """H p against central differences of the exact gradient (h = 1e-6 |v|/|p|:
+    truncation + roundoff ~1e-8 of |Hp|) and symmetry q.Hp = p.Hq."""
+    if kind == "beam":
+        pr = problems.beam(16, 8, 8, seed=4)
+    elif kind == "rect":
+        pr = problems.rect(64, 32, seed=4)
+    else:
+        pr = problems.lshape(5, 3.0 if kind == "lshape_p3" else 1.8, seed=4, keep=True)
+    dm, model = pr.dm, pr.model
+    dofs = (pr.meta["dofs_minim"] if "dofs_minim" in pr.meta else None)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    nf = dm.nfree_dofs
+    xp = torch.rand(nf, generator=gen, device="cuda", dtype=torch.float64) - 0.5
+    xq = torch.rand(nf, generator=gen, device="cuda", dtype=torch.float64) - 0.5
+    p, q = _embed(pr.v.numel(), dofs, xp), _embed(pr.v.numel(), dofs, xq)
+    hp = dm.hvp(pr.v, p, model)
+    hq = dm.hvp(pr.v, q, model)
+    dm.check()
+    h = 1e-6 * float(pr.v.abs().max()) / float(p.abs().max())
+    fd = (dm.exact_gradient(pr.v + h * p, model, pr.b) -
+          dm.exact_gradient(pr.v - h * p, model, pr.b)) / (2 * h)
+    scale = float(hp.abs().max())
+    assert float((hp - fd).abs().max()) <= 2e-6 * scale, float((hp - fd).abs().max()) / scale
+    a, b_ = float(torch.dot(xq, hp)), float(torch.dot(xp, hq))
+    assert abs(a - b_) <= 1e-12 * max(abs(a), abs(b_), 1e-300)
+
+
+def test_exact_hvp_matches_reference_fd_hessian(golden):
+    """8x4x4 beam at the seeded field: H p against the reference's coloured FD
+    Hessian times p (its own FD noise level, 1e-6 of the scale)."""
+    h = golden("hessian")
+    pr = problems.beam(8, 4, 4, seed=2109, keep=True)
+    Href = hessian._to_scipy(torch.from_numpy(h["b_H_indptr"]), torch.from_numpy(h["b_H_indices"]),
+                             600, h["b_H_data"])
+    x = np.random.default_rng(9).normal(size=600)
+    hp = pr.dm.hvp(pr.v, _embed(pr.v.numel(), pr.meta["dofs_minim"], torch.as_tensor(x).cuda()),
+                   pr.model)
+    ref = Href @ x
+    assert np.abs(hp.cpu().numpy() - ref).max() <= 1e-6 * np.abs(ref).max()
