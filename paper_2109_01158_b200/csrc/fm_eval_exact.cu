@@ -85,6 +85,19 @@ struct PipeLayout {
   }
 };
 
+// x^e for the fused kernels (x > 0): numpy's fast exponents, else
+// exp2(e log2 x) — no extended-precision log as in pow(); |e log2 x| stays
+// small for these fields, so the result is within a few ulps (1e-10 bars)
+__device__ __forceinline__ double pow_fused(double x, double e) {
+  if (e == 0.5) return sqrt(x);
+  if (e == 1.5) return x * sqrt(x);
+  if (e == 1.0) return x;
+  if (e == 2.0) return x * x;
+  if (e == -1.0) return 1.0 / x;
+  if (e == 0.0) return 1.0;
+  return exp2(e * log2(x));
+}
+
 // cofactors with one rounding per minor (fused; this kernel is not bound to
 // the reference's operation order)
 template <int DIM>
@@ -170,9 +183,9 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
     for (int k = 0; k < DIM; ++k) n2 = fma(F[0][k], F[0][k], n2);
     double fac;
     if (m.p >= 2.0)
-      fac = np_scalar_pow(n2, m.e_dw);
+      fac = pow_fused(n2, m.e_dw);  // 0^e = 0 for e > 0 (exp2(-inf))
     else
-      fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
+      fac = n2 > 0.0 ? pow_fused(n2, m.e_dw) : 0.0;
     // W = |g|^p / p = |g|^(p-2) |g|^2 / p from the gradient's factor: no second
     // pow (a few ulps from pow(n2, p/2) / p; J is compared at 1e-10)
     if (want_w) W = fac * n2 / m.p;
@@ -240,9 +253,9 @@ __device__ __forceinline__ void element_dP(
     }
     double fac;
     if (m.p >= 2.0)
-      fac = np_scalar_pow(n2, m.e_dw);
+      fac = pow_fused(n2, m.e_dw);
     else
-      fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
+      fac = n2 > 0.0 ? pow_fused(n2, m.e_dw) : 0.0;
     const double c2 = n2 > 0.0 ? (m.p - 2.0) * gd / n2 : 0.0;
     fac *= vol;
 #pragma unroll
