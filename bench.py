@@ -1,20 +1,24 @@
 """Benchmark: fused J + exact grad J on the config-4 Neo-Hookean beam.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg4] [--no-cpu-baseline]
+                    [--config cfg1|cfg2|cfg2_p1.8|cfg3|cfg4|cfg5] [--shard r/W]
+                    [--extras [--descent-iters I]] [--no-cpu-baseline]
 
 N = 1: BASELINE.json configs[3] (3D compressible Neo-Hookean, 256x128x128 Kuhn
 beam, 25,165,824 tets) — the config the north-star target (>= 60 % of the HBM
 roofline on the 3D NH exact-gradient path) is quoted on.  One step = one fused
 J + grad J evaluation of the whole mesh (energy, chain-rule gradient on all
 12.78M free dofs, consistent load), device-resident.  N > 1 (torchrun): the
-beam is split into x1-slabs, one per rank, J is all-reduced over NCCL and the
+beam is split into x1-slabs, one per rank, J is all-gathered over NCCL and the
 interface-plane gradient partials are exchanged with the slab neighbours
-(strong scaling: the total mesh is fixed).
+(strong scaling: the total mesh is fixed); ``--config cfg5`` runs the
+1.61 G-tet beam the same way, ``--shard r/W`` one rank's slab on this GPU.
+``--extras`` adds the energy-only, FD, gradient-only, exact-HVP, trust-region
+and config-5 descent-loop timings.
 
 Rank 0 prints ONE JSON line.  ``--impl reference`` times the reference
-algorithm's CPU implementation (the oracle port of femmin, oracle/) on this
-host on a bounded sample of the same workload.
+algorithm's CPU implementation (the oracle port of femmin, oracle/) on all
+host cores on a bounded sample of the same workload.
 """
 
 from __future__ import annotations
