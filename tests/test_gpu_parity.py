@@ -398,3 +398,35 @@ def test_tilings_vs_oracle(kind, tiling):
     ratio = np.abs(gn - gd) / (FD_FACTOR * scale + 1e-300)
     assert ratio.max() <= 1.0, (ratio.max(), int(ratio.argmax()), gn[ratio.argmax()],
                                 gd[ratio.argmax()], int((ratio > 1).sum()))
+
+
+@pytest.mark.parametrize("p", [3.0, 1.8])
+def test_plaplace_3d_vs_oracle(p):
+    """3D p-Laplace (scalar field on tetrahedra; no benchmark config uses it,
+    the drop-in supports it): J, exact and FD gradients and the exact HVP's
+    symmetry against the oracle on a 10x5x5 Kuhn beam, Dirichlet at x1 = 0."""
+    om = O.beam_mesh(10, 5, 5, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    om = O.mark_dirichlet(om, O.fixed_mask(om, [(O.left_face, None)], 1), 1)
+    omodel = O.Model("plap", O.PParams(p), 3)
+    b = O.load_vector(om, -10.0, 1)
+    v = O.field_plap(om, 17)
+    op = O.build_patches(om)
+    m = fb.Mesh(dim=3, level=-1, nodes2coord=om.nodes2coord, elems2nodes=om.elems2nodes,
+                volumes=om.volumes, dphi=list(om.dphi), d=1,
+                nodes_dirichlet=om.nodes_dirichlet, nodes_minim=om.nodes_minim,
+                dofs_dirichlet=om.dofs_dirichlet, dofs_minim=om.dofs_minim,
+                dofs_minim_local=om.dofs_minim_local)
+    pt = fb.build_patches(m)
+    model = fb.PLaplacian(fb.PLaplaceParams(p=p), dim=3)
+    load = fb.LinearLoad(b=b)
+    J, W = fb.energy(v, m, model, load)
+    Jo, Wo = O.energy(v, om, omodel, b)
+    assert _rel(J, Jo) < J_TOL
+    np.testing.assert_allclose(W, Wo, rtol=1e-13, atol=1e-15 * np.abs(Wo).max())
+    go = O.exact_gradient(v, om, op, omodel, b)
+    assert _grel(fb.exact_gradient(v, m, pt, model, load), go) < G_TOL
+    Jf, gf = fb.energy_and_gradient(v, m, pt, model, load)
+    assert _rel(Jf, Jo) < J_TOL and _grel(gf, go) < G_TOL
+    gn = fb.numeric_gradient(v, m, pt, model, load, eps=1e-6)
+    gd, scale = O.numeric_gradient_direct(v, om, op, omodel, b, 1e-6)
+    assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
