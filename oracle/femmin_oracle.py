@@ -499,6 +499,41 @@ def descent_loop(v, mesh: OMesh, P: OPatches, model, b, alpha, iters):
     return np.array(Js), v, g
 
 
+def sampled_exact_gradient(v, conn, volumes, dphi, prefix, elems, slot, nodes_minim, d, model,
+                           b, dofs_minim, sample):
+    """gradients.py:124-149 for a SAMPLE of free dofs only (the
+    size-independent check of full-size runs the CPU oracle cannot evaluate
+    whole): for free dof q = dofs_minim[sample[i]] (node n, component j), the
+    patch rows of n (CSR prefix / elems / slot, patches.py:37-71), F of those
+    elements (einsum order), dW (models.py) and
+    g = sum_rows vol * sum_m dW[j][m] * dphi[m][row, slot] - b[q], summed in
+    patch order (the reference's cumsum differs only by roundoff).
+    conn (ne, nv), dphi (dim, ne, nv), prefix inclusive (|M|,)."""
+    q = np.asarray(dofs_minim)[np.asarray(sample)]
+    node, comp = q // d, q % d
+    rank = np.searchsorted(nodes_minim, node)
+    lo = np.where(rank > 0, prefix[np.maximum(rank - 1, 0)], 0)
+    hi = prefix[rank]
+    cnt = hi - lo
+    rows = np.concatenate([np.arange(a, z) for a, z in zip(lo, hi)])
+    owner = np.repeat(np.arange(q.size), cnt)
+    el = elems[rows]
+    sl = slot[rows]
+    dim = len(dphi)
+    F = grad_field([dm[el] for dm in dphi], element_values(v, d, conn[el]))
+    dW = model.ddensity(F)
+    dF = [dm[el, sl] for dm in dphi]
+    jj = comp[owner]
+    contrib = np.zeros(rows.size)
+    for j in range(d):
+        sel = jj == j
+        if sel.any():
+            contrib[sel] = (volumes[el] * sum(dW[j][m] * dF[m] for m in range(dim)))[sel]
+    g = np.zeros(q.size)
+    np.add.at(g, owner, contrib)
+    return g - (b[q] if b is not None else 0.0)
+
+
 def _perturbed_row_densities(v, mesh, P, model, eps, with_libm=False):
     """Core of gradients.py:84-121: the d*||T|| densities for each sign
     (-eps first), with G recomputed from perturbed nodal values."""

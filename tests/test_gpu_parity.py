@@ -430,3 +430,31 @@ def test_plaplace_3d_vs_oracle(p):
     gn = fb.numeric_gradient(v, m, pt, model, load, eps=1e-6)
     gd, scale = O.numeric_gradient_direct(v, om, op, omodel, b, 1e-6)
     assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
+
+
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg2"])
+def test_full_size_sampled_dofs(cfg):
+    """Full-size configs (too large for the CPU oracle whole): the fused
+    gradient at 20,000 random free dofs against the oracle's per-dof
+    restatement of gradients.py:124-149 over the same patches,
+    and the fused J against the energy kernel."""
+    pr = problems.CONFIGS[cfg](keep=True)
+    dm, model, b, v = pr.dm, pr.model, pr.b, pr.v
+    J = torch.empty(3, dtype=torch.float64, device="cuda")
+    g = dm.exact_gradient(v, model, b, J=J).cpu().numpy()
+    Je = dm.energy(v, model, b).clone()
+    dm.check()
+    assert float(torch.abs(J[0] - Je[0])) <= 1e-12 * abs(float(Je[0]))
+    mt = pr.meta
+    rng = np.random.default_rng(21)
+    sample = rng.choice(mt["dofs_minim"].numel(), size=20000, replace=False)
+    dim = mt["coords"].shape[1]
+    omodel = (O.Model("nh", O.LameParams(model.params.C1, model.params.D1), dim) if dm.d > 1
+              else O.Model("plap", O.PParams(model.params.p), dim))
+    gs = O.sampled_exact_gradient(
+        v.cpu().numpy(), mt["conn"].cpu().numpy(), mt["volumes"].cpu().numpy(),
+        list(mt["dphi"].cpu().numpy()), mt["p_prefix"].cpu().numpy(),
+        mt["p_elems"].cpu().numpy(), mt["p_slot"].cpu().numpy(),
+        mt["nodes_minim"].cpu().numpy(), dm.d, omodel, b.cpu().numpy(),
+        mt["dofs_minim"].cpu().numpy(), sample)
+    assert np.abs(g[sample] - gs).max() <= G_TOL * np.abs(g).max()

@@ -229,3 +229,16 @@ def test_splitmix_reference_values():
     u = O.uniform01(2109, np.arange(4))
     assert u.dtype == np.float64 and ((0 <= u) & (u < 1)).all()
     assert O.splitmix64(np.array([0], dtype=np.uint64))[0] == np.uint64(0xE220A8397B1DCDAF)
+
+
+def test_sampled_exact_gradient_matches_full(golden):
+    """The per-dof restatement used for the full-size GPU checks agrees with the
+    reference's exact gradient (golden) up to the cumsum roundoff."""
+    g = golden("beam8x4x4_nh")
+    m, model, b, v = O.problem_beam(8, 4, 4, seed=2109)
+    p = O.build_patches(m)
+    sample = np.arange(0, m.dofs_minim.size, 3)
+    gs = O.sampled_exact_gradient(v, m.elems2nodes, m.volumes, m.dphi, p.prefix, p.elems, p.slot,
+                                  m.nodes_minim, 3, model, b, m.dofs_minim, sample)
+    ref = g["g_exact"][sample]
+    assert np.abs(gs - ref).max() <= 1e-12 * np.abs(g["g_exact"]).max()
