@@ -72,3 +72,21 @@ print(f"{cfg} {shard}: ne={pr.ne:,} J={float(J[0]):.12e} |J-J_energy|/|J|="
       f"{abs(float(J[0] - Je[0])) / abs(float(Je[0])):.1e}  sampled dofs {n}: "
       f"max|g - g_oracle| / max|g| = {err:.2e}  ({time.time() - t0:.0f} s)")
 assert err < 1e-10
+
+# nodal-patch FD at the sampled nodes: the direct-sum oracle on the sub-mesh of
+# their patches (global node ids, only the sampled nodes free), bound
+# 64 u sum_patch vol (|W+-| + L+-) / (2 eps) as in tests/test_gpu_parity.py
+eps = 1e-8 if dm.d > 1 else 1e-6
+gfd = dm.numeric_gradient(v, model, b, eps).cpu().numpy()
+dm.check()
+d = dm.d
+sub_dofs = (nodes_h[:, None] * d + np.arange(d)[None]).ravel()
+sub = O.OMesh(dim, -1, None, conn, vol, dphi, d, np.zeros(0, np.int64), nodes_h,
+              np.zeros(0, np.int64), sub_dofs, np.arange(sub_dofs.size))
+P = O.OPatches(lens, lelems, lslot, lprefix)
+gd, scale = O.numeric_gradient_direct(vh, sub, P, omodel, bh, eps)
+pos = np.searchsorted(mt["dofs_minim"].cpu().numpy(), sub_dofs)
+ratio = np.abs(gfd[pos] - gd) / (64.0 * scale + 1e-300)
+print(f"    FD at the {nodes_h.size} sampled nodes ({sub_dofs.size} dofs): max |g - g_direct| / bound "
+      f"= {ratio.max():.2e}  ({time.time() - t0:.0f} s)")
+assert ratio.max() <= 1.0
