@@ -458,3 +458,27 @@ def test_full_size_sampled_dofs(cfg):
         mt["nodes_minim"].cpu().numpy(), dm.d, omodel, b.cpu().numpy(),
         mt["dofs_minim"].cpu().numpy(), sample)
     assert np.abs(g[sample] - gs).max() <= G_TOL * np.abs(g).max()
+    # nodal-patch FD at 2,000 sampled free nodes: direct-sum oracle on the
+    # sub-mesh of their patches (global node ids; only those nodes free)
+    eps = 1e-8 if dm.d > 1 else 1e-6
+    gfd = dm.numeric_gradient(v, model, b, eps).cpu().numpy()
+    dm.check()
+    nm = mt["nodes_minim"]
+    nodes = torch.unique(mt["dofs_minim"][torch.as_tensor(sample[:2000], device="cuda")] // dm.d)
+    rank = torch.searchsorted(nm, nodes)
+    pre = mt["p_prefix"]
+    lo = torch.where(rank > 0, pre[(rank - 1).clamp(min=0)], torch.zeros_like(rank))
+    hi = pre[rank]
+    rows = torch.cat([torch.arange(a, z, device="cuda") for a, z in zip(lo.tolist(), hi.tolist())])
+    uel, inv = torch.unique(mt["p_elems"][rows], return_inverse=True)
+    d = dm.d
+    nodes_h = nodes.cpu().numpy()
+    sub_dofs = (nodes_h[:, None] * d + np.arange(d)[None]).ravel()
+    sub = O.OMesh(dim, -1, None, mt["conn"][uel].cpu().numpy(), mt["volumes"][uel].cpu().numpy(),
+                  list(mt["dphi"][:, uel].cpu().numpy()), d, np.zeros(0, np.int64), nodes_h,
+                  np.zeros(0, np.int64), sub_dofs, np.arange(sub_dofs.size))
+    P = O.OPatches((hi - lo).cpu().numpy(), inv.cpu().numpy(), mt["p_slot"][rows].cpu().numpy(),
+                   np.cumsum((hi - lo).cpu().numpy()))
+    gd, scale = O.numeric_gradient_direct(v.cpu().numpy(), sub, P, omodel, b.cpu().numpy(), eps)
+    pos = np.searchsorted(mt["dofs_minim"].cpu().numpy(), sub_dofs)
+    assert (np.abs(gfd[pos] - gd) <= FD_FACTOR * scale + 1e-300).all()
