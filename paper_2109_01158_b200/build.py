@@ -13,6 +13,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -45,37 +46,55 @@ def _headers():
     return hs + [os.path.join(INCLUDE, "femmin_b200.h")]
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
-    os.makedirs(objdir, exist_ok=True)
+def _compile(unit, extra, objdir, force):
+    src = os.path.join(CSRC, unit)
+    obj = os.path.join(objdir, unit.replace(".cu", ".o"))
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
-    objs, relink = [], force or not os.path.exists(LIB)
-    log = []
-    for unit, extra in UNITS.items():
-        src = os.path.join(CSRC, unit)
-        obj = os.path.join(objdir, unit.replace(".cu", ".o"))
-        objs.append(obj)
-        if (not force and os.path.exists(obj)
-                and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime)):
-            continue
-        cmd = [_nvcc(), *ARCH, *BASE, *extra, "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {unit}:\n{r.stdout}\n{r.stderr}")
-        relink = True
-    if relink or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [_nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    if (not force and os.path.exists(obj)
+            and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime)):
+        return obj, None
+    cmd = [_nvcc(), *ARCH, *BASE, *extra, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {unit}:\n{r.stdout}\n{r.stderr}")
+    return obj, r.stdout + r.stderr
+
+
+def _build(lib: str, objdir: str, defines: list[str], force: bool, verbose: bool) -> str:
+    """Compile every unit (in parallel, only what changed) and link ``lib``."""
+    os.makedirs(objdir, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
+        res = list(ex.map(lambda kv: _compile(kv[0], kv[1] + defines, objdir, force),
+                          UNITS.items()))
+    objs = [o for o, _ in res]
+    log = [l for _, l in res if l is not None]
+    if (force or log or not os.path.exists(lib)
+            or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     if log:
-        with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
+        with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
             fh.write("\n".join(log))
         if verbose:
             print("\n".join(log))
-    return LIB
+    return lib
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    """The product library lib/libfemmin_b200.so."""
+    os.makedirs(LIBDIR, exist_ok=True)
+    return _build(LIB, os.path.join(LIBDIR, "obj"), [], force, verbose)
+
+
+def build_variant(name: str, defines: list[str], force: bool = False) -> str:
+    """A profiling build of the same sources (lib/libfemmin_<name>.so, e.g.
+    -DFM_TRACE=1 or -DFM_ABLATE=1), selected at run time with FM_LIB_OVERRIDE;
+    the product library never carries these switches."""
+    os.makedirs(LIBDIR, exist_ok=True)
+    return _build(os.path.join(LIBDIR, f"libfemmin_{name}.so"),
+                  os.path.join(LIBDIR, f"obj_{name}"), defines, force, False)
 
 
 if __name__ == "__main__":

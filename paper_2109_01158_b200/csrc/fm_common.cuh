@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "femmin_b200.h"
 
 namespace fm {
@@ -31,9 +33,35 @@ void set_error(const std::string &msg);
     }                                                                        \
   } while (0)
 
+// NVTX range around a C-ABI entry point (header-only NVTX v3: a no-op unless
+// a profiler is attached), so nsys / ncu timelines show the femmin calls
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define FM_NVTX(name) ::fm::NvtxRange _fm_nvtx_range(name)
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 64) {
+// SM count of the current device (queried once per device; 148 on B200)
+inline int sm_count() {
+  static thread_local int cached_dev = -1, cached_n = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached_dev = dev;
+    cached_n = n > 0 ? n : 1;
+  }
+  return cached_n;
+}
+
+// grid-stride launches: at most 64 blocks per SM
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 0) {
+  if (cap <= 0) cap = (int64_t)sm_count() * 64;
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
   if (g > cap) g = cap;

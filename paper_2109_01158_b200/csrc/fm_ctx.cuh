@@ -176,10 +176,18 @@ struct ModelArgs {
   // p-Laplace exponents classified like numpy's fast scalar power
   // (ndarray ** scalar: 0.5 -> sqrt, 1 -> copy, 2 -> square, -1 -> reciprocal)
   double e_w, e_dw;  // p/2 and (p-2)/2
-  int dbg;           // profiling ablations of the tile kernel (FM_TILE_ABLATE, tools/ablate.py:
-                     // 1 no constitutive, 2 no consume, 8 no compute, 32 no closure
-                     // gathers; results are wrong on purpose), 0 = off
+  int dbg;           // profiling ablations of the tile kernel, read through FM_DBG (FM_TILE_ABLATE,
+                     // tools/ablate.py: 1 no constitutive, 2 no consume, 8 no compute, 32 no
+                     // closure gathers; results are wrong on purpose), 0 = off
 };
+
+// The ablation switches exist only in profiling builds (-DFM_ABLATE=1, a
+// separate library built by tools/ablate.py); in the product library FM_DBG
+// is the constant 0 and the compiler drops every ablation branch.
+#ifndef FM_ABLATE
+#define FM_ABLATE 0
+#endif
+#define FM_DBG(m) (FM_ABLATE ? (m).dbg : 0)
 
 // x ** e with numpy's fast scalar cases (-1, 0, 0.5, 1, 2) and, beyond numpy,
 // 1.5 as x sqrt(x) (the p = 3 energy; <= 2 ulps of pow(x, 1.5), within the
@@ -255,7 +263,7 @@ struct fm_ctx {
   int64_t n_tile_elems = 0, n_node_entries = 0;
   int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, clo_cap = 0;
   int chunk_entry_cap = 0;  // max node entries of one chunk of one tile (FD staging)
-  int n_sm = 148, ctas_per_sm = 2, node_bufs = 2, table_bufs = 2;
+  int n_sm = 0, ctas_per_sm = 2, node_bufs = 2, table_bufs = 2;
   uint8_t *aos = nullptr;
   int4 *conn4 = nullptr;
   fm::TileMeta *meta = nullptr;

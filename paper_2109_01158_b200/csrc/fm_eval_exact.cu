@@ -263,7 +263,9 @@ __device__ __forceinline__ void element_dP(
   }
 }
 
-// F = grad v as chained FMAs (one DMUL + NV-1 DFMA per entry)
+// F = grad v as chained FMAs (one DMUL + NV-1 DFMA per entry; the edge-
+// difference form sum_{l>=1} (v_l - v_0) dphi_l, one DADD fewer per entry and
+// no dphi column 0, measured 2 % slower at cfg4)
 template <int DIM, int D>
 __device__ __forceinline__ void grad_F_fma(const double (&vv)[D][DIM + 1],
                                            const double (&g)[DIM][DIM + 1], double (&F)[D][DIM]) {
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(CT, MINB)
   };
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
     double *dst = nodev(k);
-    for (int i = tid; i < clo_count && !(mdl.dbg & 32); i += CT) {  // 32: probe without gathers
+    for (int i = tid; i < clo_count && !(FM_DBG(mdl) & 32); i += CT) {  // 32: probe without gathers
       const int64_t off = (int64_t)cids[i] * D;
 #pragma unroll
       for (int kk = 0; kk < DG; ++kk)  // HV: components D.. are the direction's
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(CT, MINB)
         mbar_wait(full + s, (q >> 1) & 1);
         TRACE(1);
         const int e = c0 + tid;
-        const bool valid = e < ne_t && !(mdl.dbg & 8);  // 8: data-movement-only probe
+        const bool valid = e < ne_t && !(FM_DBG(mdl) & 8);  // 8: data-movement-only probe
         double P[D][DIM];
         double Wel = 0.0, det_el = 1.0, ls_el = 0.0;  // this element's W (J) and its log fix-up
         bool far = false;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(CT, MINB)
           double F[D][DIM];
           grad_F_fma<DIM, D>(vv, E.g, F);
           const bool own = true;
-          if (mdl.dbg & 1) {  // ablation: no constitutive work
+          if (FM_DBG(mdl) & 1) {  // ablation: no constitutive work
 #pragma unroll
             for (int k = 0; k < D; ++k)
 #pragma unroll
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(CT, MINB)
         __syncthreads();  // contributions staged; every record of stage s read
         TRACE(3);
         // stage s is free: records of chunk q + 2
-        if (my_node && !(mdl.dbg & 2)) {
+        if (my_node && !(FM_DBG(mdl) & 2)) {
           // this node's entries of the chunk (its slice of the chunk's entry
           // block): the loads of two entries are issued together; the order
           // (ascending tile element) is the fixed summation order
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
 }
 
 int finish_cross_grid(int d, int64_t ntn) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, FINISH_MAX_BLOCKS));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, finish_max_blocks()));
 }
 
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,

@@ -588,6 +588,7 @@ static ModelArgs rows_model(const fm_model *m) {
 
 extern "C" int fm_density_rows(const fm_model *m, int64_t n, const double *F, double *W,
                                double *P, int64_t *nbad_host, void *stream) {
+  FM_NVTX("fm_density_rows");
   FM_ARG(m && F, "null argument");
   FM_ARG(m->dim == 2 || m->dim == 3, "dim must be 2 or 3");
   FM_ARG(m->kind == FM_MODEL_PLAPLACE || m->kind == FM_MODEL_NEOHOOKEAN, "unknown model kind");
@@ -616,6 +617,7 @@ extern "C" int fm_density_rows(const fm_model *m, int64_t n, const double *F, do
 
 extern "C" int fm_det_rows(int dim, int64_t n, const double *F, double *det, double *cof,
                            void *stream) {
+  FM_NVTX("fm_det_rows");
   FM_ARG(dim == 2 || dim == 3, "dim must be 2 or 3");
   cudaStream_t s = as_stream(stream);
   if (dim == 2)
@@ -628,6 +630,7 @@ extern "C" int fm_det_rows(int dim, int64_t n, const double *F, double *det, dou
 
 extern "C" int fm_eval_F(int dim, int d, int64_t rows, const double *vals, const double *dphi,
                          double *F, void *stream) {
+  FM_NVTX("fm_eval_F");
   FM_ARG(dim == 2 || dim == 3, "dim must be 2 or 3");
   cudaStream_t s = as_stream(stream);
   if (dim == 2)
@@ -640,6 +643,7 @@ extern "C" int fm_eval_F(int dim, int d, int64_t rows, const double *vals, const
 
 extern "C" int fm_segment_sums(int64_t nseg, const double *vals, const int64_t *indx,
                                double *out, void *stream) {
+  FM_NVTX("fm_segment_sums");
   cudaStream_t s = as_stream(stream);
   k_segment_sums<<<grid_for(nseg, 256), 256, 0, s>>>(nseg, vals, indx, out);
   FM_CHECK_LAUNCH();
@@ -648,9 +652,10 @@ extern "C" int fm_segment_sums(int64_t nseg, const double *vals, const int64_t *
 
 // linear_term (assembly.py:89-91): out[0] = a.b with the fixed-order partials.
 extern "C" int fm_dot(int64_t n, const double *a, const double *b, double *out, void *stream) {
+  FM_NVTX("fm_dot");
   FM_ARG(a && b && out, "null argument");
   cudaStream_t s = as_stream(stream);
-  const int nb = 148 * 2;
+  const int nb = sm_count() * 2;
   Scratch part;
   FM_CUDA(part.alloc(nb * sizeof(double), s));
   FM_CUDA(launch_dot(a, b, n, nb, part.as<double>(), s));

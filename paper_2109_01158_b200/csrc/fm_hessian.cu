@@ -185,6 +185,7 @@ extern "C" {
 int fm_hessian_pattern(int64_t nn, int64_t ne, int nv, int d, const int64_t *conn,
                        int64_t nfree_dofs, const int64_t *dofs_minim, int64_t *indptr,
                        int64_t *indices, int64_t *nnz_host, void *stream) {
+  FM_NVTX("fm_hessian_pattern");
   FM_ARG(nn >= 0 && ne >= 0 && nv >= 1 && d >= 1 && nnz_host, "invalid pattern arguments");
   FM_ARG(nn < (1ll << 31), "node ids must fit 32 bits");
   cudaStream_t s = as_stream(stream);
@@ -246,6 +247,7 @@ int fm_hessian_pattern(int64_t nn, int64_t ne, int nv, int d, const int64_t *con
 
 int fm_color_d2(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t *colors,
                 int32_t *ncolors_host, void *stream) {
+  FM_NVTX("fm_color_d2");
   FM_ARG(n >= 0 && ncolors_host, "invalid colouring arguments");
   cudaStream_t s = as_stream(stream);
   Scratch other, left;
@@ -285,6 +287,7 @@ int fm_color_d2(int64_t n, const int64_t *indptr, const int64_t *indices, int32_
 
 int fm_hess_perturb(int64_t nfree_dofs, const int64_t *dofs_minim, const int32_t *colors,
                     int color, double step, double *vp, void *stream) {
+  FM_NVTX("fm_hess_perturb");
   cudaStream_t s = as_stream(stream);
   k_hess_perturb<<<grid_for(nfree_dofs, 256), 256, 0, s>>>(nfree_dofs, dofs_minim, colors, color,
                                                            step, vp);
@@ -295,6 +298,7 @@ int fm_hess_perturb(int64_t nfree_dofs, const int64_t *dofs_minim, const int32_t
 int fm_hess_scatter(int64_t n, const int64_t *indptr, const int64_t *indices,
                     const int32_t *colors, int color, const double *g_pert, const double *g0,
                     double step, double *vals, void *stream) {
+  FM_NVTX("fm_hess_scatter");
   cudaStream_t s = as_stream(stream);
   k_hess_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, indptr, indices, colors, color, g_pert, g0,
                                                   step, vals);
@@ -304,6 +308,7 @@ int fm_hess_scatter(int64_t n, const int64_t *indptr, const int64_t *indices,
 
 int fm_hess_symmetrize(int64_t n, const int64_t *indptr, const int64_t *indices,
                        const double *vals, double *out, void *stream) {
+  FM_NVTX("fm_hess_symmetrize");
   cudaStream_t s = as_stream(stream);
   k_hess_sym<<<grid_for(n, 256), 256, 0, s>>>(n, indptr, indices, vals, out);
   FM_CHECK_LAUNCH();

@@ -31,11 +31,12 @@ struct JFinal {
   const int32_t *fixed_nodes;  // nodes without a free dof
   int64_t nfixed;
   const double *b, *v;
-  double *fpart;               // FINISH_MAX_BLOCKS
+  double *fpart;               // finish_max_blocks()
   unsigned int *ticket;        // zero between calls
   double *out;                 // null: no J
 };
-constexpr int FINISH_MAX_BLOCKS = 148 * 32;
+// finishing-pass grid cap (32 blocks per SM); sizes the per-block b.v partials
+inline int finish_max_blocks() { return sm_count() * 32; }
 int finish_cross_grid(int d, int64_t ntn);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,
                                 const int32_t *outw,

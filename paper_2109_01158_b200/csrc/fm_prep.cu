@@ -400,6 +400,7 @@ int fm_lshape_sizes(int level, int64_t *nn, int64_t *ne) {
 }
 
 int fm_gen_lshape(int level, double *coords, int64_t *conn, void *stream) {
+  FM_NVTX("fm_gen_lshape");
   int64_t nn, ne;
   int st = fm_lshape_sizes(level, &nn, &ne);
   if (st) return st;
@@ -414,6 +415,7 @@ int fm_gen_lshape(int level, double *coords, int64_t *conn, void *stream) {
 
 int fm_gen_rect(int nx, int ny, double x0, double x1, double y0, double y1, double *coords,
                 int64_t *conn, void *stream) {
+  FM_NVTX("fm_gen_rect");
   FM_ARG(nx > 0 && ny > 0, "grid sizes must be positive");
   int64_t n = std::max<int64_t>((int64_t)(nx + 1) * (ny + 1), (int64_t)nx * ny);
   k_rect<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(nx, ny, x0, x1, (x1 - x0) / nx, y0,
@@ -424,6 +426,7 @@ int fm_gen_rect(int nx, int ny, double x0, double x1, double y0, double y1, doub
 
 int fm_gen_beam(int nx, int ny, int nz, const double *b, int ix0, int ix1, double *coords,
                 int64_t *conn, void *stream) {
+  FM_NVTX("fm_gen_beam");
   FM_ARG(nx > 0 && ny > 0 && nz > 0, "grid sizes must be positive");
   FM_ARG(b[1] > b[0] && b[3] > b[2] && b[5] > b[4], "bar dimensions must be positive");
   FM_ARG(0 <= ix0 && ix0 < ix1 && ix1 <= nx, "slab range must satisfy 0 <= ix0 < ix1 <= nx");
@@ -441,6 +444,7 @@ int fm_gen_beam(int nx, int ny, int nz, const double *b, int ix0, int ix1, doubl
 
 int fm_p1_gradients(int dim, int64_t nn, int64_t ne, const double *coords, const int64_t *conn,
                     double *volumes, double *dphi, int64_t *bad_elem_host, void *stream) {
+  FM_NVTX("fm_p1_gradients");
   FM_ARG(dim == 2 || dim == 3, "dim must be 2 or 3");
   (void)nn;
   cudaStream_t s = as_stream(stream);
@@ -473,6 +477,7 @@ int fm_p1_gradients(int dim, int64_t nn, int64_t ne, const double *coords, const
 int fm_dirichlet_predicate(int kind, int dim, int d, int64_t nn, const double *coords, int axis,
                            double c, double tol, const int32_t *comps, int ncomps,
                            uint8_t *fixed, int64_t *matched_host, void *stream) {
+  FM_NVTX("fm_dirichlet_predicate");
   FM_ARG(kind >= 0 && kind <= 2, "unknown predicate kind");
   FM_ARG(axis >= 0 && axis < dim, "axis out of range");
   FM_ARG(d >= 1 && d <= 3, "d must be 1..3");
@@ -502,6 +507,7 @@ int fm_dirichlet_predicate(int kind, int dim, int d, int64_t nn, const double *c
 int fm_mark_dirichlet(int64_t nn, int d, const uint8_t *fixed, int64_t *nodes_dirichlet,
                       int64_t *nodes_minim, int64_t *dofs_dirichlet, int64_t *dofs_minim,
                       int64_t *dofs_minim_local, int64_t *counts_host, void *stream) {
+  FM_NVTX("fm_mark_dirichlet");
   FM_ARG(d >= 1 && d <= 3, "d must be 1..3");
   cudaStream_t s = as_stream(stream);
   Scratch fl, cnt;
@@ -534,6 +540,7 @@ int fm_build_patches(int64_t nn, int64_t ne, int nv, const int64_t *conn,
                      const int64_t *nodes_minim, int64_t nfree, int64_t *lengths,
                      int64_t *prefix, int64_t *elems, int64_t *slot, int64_t *total_host,
                      int64_t *bad_node_host, void *stream) {
+  FM_NVTX("fm_build_patches");
   FM_ARG(nv >= 2 && nv <= 4, "nv must be 2..4");
   FM_ARG(ne < (1ll << 32) && nfree < (1ll << 31), "mesh too large for 32-bit patch keys");
   cudaStream_t s = as_stream(stream);
@@ -652,17 +659,20 @@ static int load_impl(int dim, int d, int64_t nn, int64_t ne, const int64_t *conn
 
 int fm_load_constant(int dim, int d, int64_t nn, int64_t ne, const int64_t *conn,
                      const double *volumes, const double *f, double *b, void *stream) {
+  FM_NVTX("fm_load_constant");
   return load_impl(dim, d, nn, ne, conn, volumes, f, nullptr, b, stream);
 }
 
 int fm_load_nodal(int dim, int d, int64_t nn, int64_t ne, const int64_t *conn,
                   const double *volumes, const double *f, double *b, void *stream) {
+  FM_NVTX("fm_load_nodal");
   FM_ARG(f != nullptr, "null nodal load");
   return load_impl(dim, d, nn, ne, conn, volumes, nullptr, f, b, stream);
 }
 
 int fm_field_uniform(int64_t ndof, const int64_t *dofs, int64_t nfd, const int64_t *gid,
                      uint64_t seed, double *v, void *stream) {
+  FM_NVTX("fm_field_uniform");
   cudaStream_t s = as_stream(stream);
   FM_CUDA(cudaMemsetAsync(v, 0, ndof * 8, s));
   if (nfd)
@@ -673,6 +683,7 @@ int fm_field_uniform(int64_t ndof, const int64_t *dofs, int64_t nfd, const int64
 
 int fm_field_nh(int64_t nn, int d, const double *coords, const int64_t *dofs, int64_t nfd,
                 const int64_t *gid, uint64_t seed, double amp, double *v, void *stream) {
+  FM_NVTX("fm_field_nh");
   cudaStream_t s = as_stream(stream);
   FM_CUDA(cudaMemcpyAsync(v, coords, nn * d * 8, cudaMemcpyDeviceToDevice, s));
   if (nfd)

@@ -2,6 +2,9 @@
 ablated runs compute wrong results on purpose, so no checks are made).
 
     python tools/ablate.py 0 1 2 4 ...
+
+The switches exist only in a separate profiling build (lib/libfemmin_ablate.so,
+-DFM_ABLATE=1), selected through FM_LIB_OVERRIDE; the product library has none.
 """
 import os
 import subprocess
@@ -28,8 +31,12 @@ torch.cuda.synchronize()
 print(sum(a.elapsed_time(z) for a, z in ev) / len(ev))
 ''' % ROOT
 
+sys.path.insert(0, ROOT)
+from paper_2109_01158_b200 import build as B  # noqa: E402
+
+LIB = B.build_variant("ablate", ["-DFM_ABLATE=1"])
 for setting in sys.argv[1:]:
-    env = dict(os.environ, FM_TILE_ABLATE=setting)
+    env = dict(os.environ, FM_TILE_ABLATE=setting, FM_LIB_OVERRIDE=LIB)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     out = r.stdout.strip().splitlines()
     print(f"ablate {setting}: kernel {out[-1] if out else 'FAILED ' + r.stderr[-300:]} ms")

@@ -28,17 +28,8 @@ CTAS, WARPS, CHUNKS, STAMPS = 4, 8, 160, 8
 
 
 def build_trace():
-    objdir = os.path.join(B.LIBDIR, "obj_trace")
-    os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for unit, extra in B.UNITS.items():
-        obj = os.path.join(objdir, unit.replace(".cu", ".o"))
-        flags = list(extra) + (["-DFM_TRACE=1"] if unit == "fm_eval_exact.cu" else [])
-        cmd = [B._nvcc(), *B.ARCH, *B.BASE, *flags, "-c", os.path.join(B.CSRC, unit), "-o", obj]
-        subprocess.run(cmd, check=True, capture_output=True)
-        objs.append(obj)
-    subprocess.run([B._nvcc(), *B.ARCH, "-shared", "-o", TRACE_LIB, *objs, "-lcudart"], check=True)
-    return TRACE_LIB
+    # every unit gets the define; only fm_eval_exact.cu uses it
+    return B.build_variant("trace", ["-DFM_TRACE=1"])
 
 
 def main():
