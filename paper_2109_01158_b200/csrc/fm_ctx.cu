@@ -346,11 +346,13 @@ __global__ void k_node_clo(int64_t ntn, const int32_t *tile_node_rank, const int
   }
 }
 
-__global__ void k_mark_cross(int64_t ntn, const int32_t *xn, int4 *desc, int32_t *outw) {
+__global__ void k_mark_cross(int64_t ntn, const int32_t *xn, int4 *desc, int32_t *outw,
+                             uint8_t *fmask) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntn;
        k += (int64_t)gridDim.x * blockDim.x) {
     outw[k] = desc[k].w;
-    if (xn[k]) desc[k].w = (int)((unsigned)desc[k].w | CROSS_FLAG);
+    fmask[k] = (uint8_t)desc_mask(desc[k]);
+    if (xn[k]) desc[k].x = (int)((unsigned)desc[k].x | CROSS_FLAG);
   }
 }
 
@@ -620,7 +622,8 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
       }
       const bool found = lo < hi0 && ukeys[lo] == key;
       const int64_t te = found ? tpos[lo] : 0;
-      if (te >= MAX_TILE_ELEMS || !found) atomicAdd(overflow, 1ull);
+      if (!found) atomicOr(overflow, 1ull);               // internal: entry not in its tile
+      if (te >= MAX_TILE_ELEMS) atomicOr(overflow, 2ull);  // capacity: tile too large
       uint16_t v = (uint16_t)((te << 2) | slot[q]);
       int p = n++;  // insertion sort by te (entries of one node are few)
       while (p > 0 && out[p - 1] > v) {
@@ -629,22 +632,22 @@ __global__ void k_node_desc(int64_t ntn, const int32_t *tile_node_rank, const in
       }
       out[p] = v;
     }
-    const int fo = free_out[r];
-    if (fo >= (1 << OUT_MASK_SHIFT)) atomicAdd(overflow, 1ull);
+    const int fo = free_out[r];  // < 2^31 (checked on the host)
     // entries per chunk of ct tile elements (5 bits x MAX_CHUNKS) packed with the
     // tile-local entry offset (13 bits): x = off | c0..c2 << 13, y = c3..c8
     unsigned long long cc = 0;
     for (int p = 0; p < n; ++p) {
       const int ch = (out[p] >> 2) / ct;
       if (ch >= MAX_CHUNKS || ((cc >> (5 * ch)) & 31ull) == 31ull) {
-        atomicAdd(overflow, 1ull);
+        atomicOr(overflow, 2ull);  // capacity: > 9 chunks or > 31 entries in one chunk
         continue;
       }
       cc += 1ull << (5 * ch);
     }
-    if (entry_off[k] >= (1 << 13)) atomicAdd(overflow, 1ull);
-    desc[k] = make_int4(entry_off[k] | (int)((cc & 0x7fffull) << 13), (int)(cc >> 15),
-                        free_node[r], fo | ((int)free_mask[r] << OUT_MASK_SHIFT));
+    if (entry_off[k] >= (1 << 13)) atomicOr(overflow, 2ull);
+    desc[k] = make_int4(entry_off[k] | (int)((cc & 0x7fffull) << 13) |
+                            (int)((unsigned)free_mask[r] << DESC_MASK_SHIFT),
+                        (int)(cc >> 15), free_node[r], fo);
   }
 }
 
@@ -740,14 +743,21 @@ int fm_ctx_time_next(fm_ctx *c, void *ev_start, void *ev_stop) {
   return FM_OK;
 }
 
-int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, fm_ctx **out) {
-  FM_NVTX("fm_ctx_create");
+// One build attempt with the given tiling.  A per-tile capacity limit
+// (closure > 2^16 nodes, > 16384 tile elements, > 9 chunks, > 31 entries of
+// one node in a chunk, tables beyond shared memory) sets *cap and returns
+// FM_INVALID_ARG; fm_ctx_create then retries with smaller tile boxes.
+static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, fm_ctx **out,
+                     bool *cap) {
+  *cap = false;
   FM_ARG(m && out, "null argument");
   FM_ARG(m->dim == 2 || m->dim == 3, "dim must be 2 or 3");
   FM_ARG(m->d >= 1 && m->d <= m->dim, "d must be 1..dim");
   FM_ARG(m->ne > 0 && m->nn > 0, "empty mesh");
   FM_ARG(m->ne < (1ll << 31) && m->nn < (1ll << 31) && m->p_total < (1ll << 31),
          "per-GPU mesh must fit 32-bit indices (shard larger meshes)");
+  FM_ARG(m->nfree >= 0 && m->nfree * (int64_t)m->d < (1ll << 31),
+         "per-GPU free dofs must be < 2^31 (shard larger meshes)");
   cudaStream_t s = as_stream(stream);
   const int dim = m->dim, nv = dim + 1, d = m->d;
   fm_ctx *c = new fm_ctx();
@@ -755,6 +765,11 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   auto fail = [&](int code) {
     fm_ctx_destroy(c);
     return code;
+  };
+  auto capacity = [&](const char *msg) {
+    set_error(std::string(msg) + " (tile capacity)");
+    *cap = true;
+    return fail(FM_INVALID_ARG);
   };
   c->dim = dim;
   c->d = d;
@@ -764,13 +779,6 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   c->nfree = m->nfree;
   c->p_total = m->p_total;
   // tile = CTA width: 256 nodes (3D 8x8x4 boxes, 2D 16x16) or 128 (3D 8x4x4)
-  // FM_TILING="nodes,bx,by,bz" overrides the default tiling (tuning aid)
-  fm_tiling env_til{};
-  if (!tiling)
-    if (const char *e = getenv("FM_TILING"))
-      if (sscanf(e, "%d,%d,%d,%d", &env_til.tile_nodes, &env_til.box[0], &env_til.box[1],
-                 &env_til.box[2]) == 4)
-        tiling = &env_til;
   int NT = (tiling && tiling->tile_nodes) ? tiling->tile_nodes : 256;
   NT = NT <= 128 ? 128 : 256;
   int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? (NT == 128 ? 4 : 8) : 16, dim == 3 ? 4 : 1};
@@ -883,7 +891,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       double nb = std::floor((from_ord(hmx[a]) - x0[a] + 0.5 * h) / edge[a]) + 1;
       if (!(nb < 2e6)) {
         set_error("tiling box grid too large (> 2^21 boxes per axis)");
-        return fail(FM_INVALID_ARG);
+        return fail(FM_INVALID_ARG);  // smaller boxes would not help
       }
     }
     Scratch keys, keys2, vals2, lens;
@@ -1110,8 +1118,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     max_halo = std::max(max_halo, tm.halo_count);
   }
   if (c->max_tile_elems > MAX_TILE_ELEMS) {
-    set_error("a node tile touches more than 16384 elements; use smaller tiles");
-    return fail(FM_INVALID_ARG);
+    return capacity("a node tile touches more than 16384 elements");
   }
   const int OT = 4 * CONSUMERS;  // orphan elements per J-only tile
   for (int64_t o = 0; o < n_orph; o += OT) {
@@ -1225,8 +1232,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     h_cb[NTA] = (int)ctot;
     c->clo_cap = (c->clo_cap + 3) / 4 * 4;
     if (c->clo_cap > 65536) {
-      set_error("a tile's node closure exceeds 65536 nodes; use smaller tiles");
-      return fail(FM_INVALID_ARG);
+      return capacity("a tile's node closure exceeds 65536 nodes");
     }
     CK(dmalloc(&c->closure, ctot + 4, &B));
     CK(cudaMemsetAsync(c->closure, 0, (ctot + 4) * 4, s));
@@ -1265,8 +1271,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   CK(dmalloc(&c->flags, M + 16, &B));
   CK(dmalloc(&c->node_desc, std::max<int64_t>(nfree, 1), &B));
   if (c->max_tile_elems > MAX_CHUNKS * c->tile_nodes) {
-    set_error("a node tile has more than 9 chunks of elements; use smaller tile boxes");
-    return fail(FM_INVALID_ARG);
+    return capacity("a node tile has more than 9 chunks of elements");
   }
   CK(dmalloc(&c->node_entries, entry_total + 8, &B));
   c->n_node_entries = entry_total;
@@ -1310,10 +1315,12 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     unsigned long long h_ovf = 0;
     CK(cudaMemcpyAsync(&h_ovf, ovf.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (h_ovf) {
-      set_error("internal error: patch entry not found in its tile or output offset overflow");
+    if (h_ovf & 1) {
+      set_error("internal error: patch entry not found in its tile");
       return fail(FM_CUDA_ERROR);
     }
+    if (h_ovf) return capacity("a tile node has more than 31 patch elements in one chunk of "
+                               "its tile, or a tile more than 8192 node entries");
     ukeys.reset();  // tile element lists: consumed by the descriptors / entries
     tpos.reset();
     owner_of.reset();
@@ -1410,9 +1417,10 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
     // nodes with cross entries: flagged in their descriptor (the tile kernel
     // then leaves a dense partial sum instead of g), outputs for the finish
     CK(dmalloc(&c->node_outw, nfree, &B));
+    CK(dmalloc(&c->node_fmask, nfree, &B));
     CK(dmalloc(&c->partial, (size_t)nfree * d, &B));
     k_mark_cross<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, c->node_xn, c->node_desc,
-                                                       c->node_outw);
+                                                       c->node_outw, c->node_fmask);
     CK(cudaGetLastError());
     // the finishing pass visits only the tile nodes with cross entries
     {
@@ -1488,8 +1496,7 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
       }
     }
     if (best < 0) {
-      set_error("tile tables exceed shared memory; use smaller tiles");
-      return fail(FM_INVALID_ARG);
+      return capacity("tile tables exceed shared memory");
     }
   }
 
@@ -1537,6 +1544,42 @@ int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, 
   return FM_OK;
 }
 
+int fm_ctx_create(const fm_mesh_desc *m, const fm_tiling *tiling, void *stream, fm_ctx **out) {
+  FM_NVTX("fm_ctx_create");
+  // FM_TILING="nodes,bx,by,bz" overrides the default tiling (tuning aid)
+  fm_tiling til{};
+  if (tiling) {
+    til = *tiling;
+  } else if (const char *e = getenv("FM_TILING")) {
+    if (sscanf(e, "%d,%d,%d,%d", &til.tile_nodes, &til.box[0], &til.box[1], &til.box[2]) != 4)
+      til = fm_tiling{};
+  }
+  FM_ARG(m && out, "null argument");
+  const int dim = m->dim;
+  int box[3] = {dim == 3 ? 8 : 16, dim == 3 ? 8 : 16, dim == 3 ? 4 : 1};
+  if (til.tile_nodes > 0 && til.tile_nodes <= 128 && dim == 3) box[1] = 4;
+  for (int a = 0; a < 3; ++a)
+    if (til.box[a] > 0) box[a] = til.box[a];
+  // capacity failures retry with the largest box edge halved (a mesh much
+  // denser or more graded than the structured configs); other errors return
+  std::string first_err;
+  for (int attempt = 0;; ++attempt) {
+    for (int a = 0; a < 3; ++a) til.box[a] = box[a];
+    bool cap = false;
+    const int st = ctx_build(m, &til, stream, out, &cap);
+    if (st == FM_OK || !cap) return st;
+    if (attempt == 0) first_err = fm_last_error();
+    int big = 0;
+    for (int a = 1; a < dim; ++a)
+      if (box[a] > box[big]) big = a;
+    if (box[big] <= 1) {
+      set_error(first_err + "; no tiling down to single-width boxes fits");
+      return FM_INVALID_ARG;
+    }
+    box[big] /= 2;
+  }
+}
+
 int fm_ctx_destroy(fm_ctx *c) {
   FM_NVTX("fm_ctx_destroy");
   if (!c) return FM_OK;
@@ -1544,7 +1587,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->closure,   c->flags,     c->node_desc, c->node_entries, c->free_node,
                   c->free_out,  c->rank_of,   c->storage_to_orig, c->free_mask, c->jpart,
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
-                  c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw,
+                  c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw, c->node_fmask,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
                   c->xnodes,    c->dof_pos};
   for (void *p : ptrs)
@@ -1611,7 +1654,7 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     JFinal jf{c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0, c->fixed_nodes,
               c->n_fixed_nodes, b, v, c->fpart, c->ticket, wj ? J_out : nullptr};
     FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->n_xnodes : 0, c->xnodes,
-                                c->node_xbase, c->node_outw, c->xpos, c->xbuf, c->partial, g,
+                                c->node_xbase, c->node_outw, c->node_fmask, c->xpos, c->xbuf, c->partial, g,
                                 jf, s));
     c->launches++;
   }
@@ -1645,7 +1688,7 @@ int fm_hvp_exact(fm_ctx *c, const fm_model *model, const double *v, const double
     JFinal jf{c->jpart, c->dotpart, 0, c->fixed_nodes, 0, nullptr, v, c->fpart, c->ticket,
               nullptr};
     FM_CUDA(launch_finish_cross(c->d, c->n_xnodes, c->xnodes, c->node_xbase, c->node_outw,
-                                c->xpos, c->xbuf, c->partial, hp, jf, s));
+                                c->node_fmask, c->xpos, c->xbuf, c->partial, hp, jf, s));
     c->launches++;
   }
   return FM_OK;

@@ -31,8 +31,12 @@ namespace fm {
 
 constexpr int MAX_TILE_ELEMS = 16384;  // node entries store te_local in 14 bits
 constexpr int CONSUMERS = 256;         // threads per tile CTA = chunk size = max tile nodes
-constexpr int OUT_MASK_SHIFT = 28;     // node_desc.w = out_offset | free_mask << 28
-constexpr unsigned CROSS_FLAG = 1u << 31;  // node_desc.w: the node has cross entries
+// node_desc = {x: entry offset (bits 0..12) | chunk counts 0..2 (bits 13..27) |
+//                 free-component mask (bits 28..30) | cross flag (bit 31),
+//              y: chunk counts 3..8, z: node id, w: output offset (31 bits, so a
+//              context holds up to 2^31 - 1 free dofs)}
+constexpr int DESC_MASK_SHIFT = 28;        // node_desc.x: free-component mask
+constexpr unsigned CROSS_FLAG = 1u << 31;  // node_desc.x: the node has cross entries
 constexpr int MAX_CHUNKS = 9;          // per-chunk entry counts in node_desc.x/.y (5 bits each)
 constexpr int ENTRY_OFF_MASK = (1 << 13) - 1;  // node_desc.x bits 0..12: tile-local entry offset
 constexpr int XCH_STRIDE = 12;  // ints per tile in xchunk (MAX_CHUNKS + 1, padded to 16 B)
@@ -40,8 +44,13 @@ constexpr int XCH_STRIDE = 12;  // ints per tile in xchunk (MAX_CHUNKS + 1, padd
 // entries of this node in chunk ch of its tile (node_desc packing, see k_node_desc)
 __device__ __forceinline__ int chunk_count(int4 nd, int ch) {
   const unsigned long long cc =
-      ((unsigned long long)(unsigned)nd.y << 15) | ((unsigned)nd.x >> 13);
+      ((unsigned long long)(unsigned)nd.y << 15) | (((unsigned)nd.x >> 13) & 0x7fffu);
   return (int)((cc >> (5 * ch)) & 31ull);
+}
+
+// free components of the node (bit j: dof d*node+j is free)
+__host__ __device__ __forceinline__ int desc_mask(int4 nd) {
+  return (int)(((unsigned)nd.x >> DESC_MASK_SHIFT) & 7u);
 }
 
 template <int DIM> struct RecBytes;
@@ -214,7 +223,7 @@ struct TileArgs {
   const int32_t *closure;      // node ids of the tile closures
   const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
   const int4 *node_desc;       // {entry_off | chunk counts, chunk counts, node id,
-                               //  out | mask << 28} (see chunk_count)
+                               //  out offset} (see chunk_count, desc_mask)
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
   const uint16_t *chunk_blocks;  // per tile and chunk: node offsets + entries (see blk_header)
   const int32_t *rank_of;      // node -> free rank or -1
@@ -282,7 +291,8 @@ struct fm_ctx {
   int32_t *xnodes = nullptr;  // tile nodes with cross entries (finishing pass)
   int64_t n_xnodes = 0;
   double *xbuf = nullptr, *partial = nullptr;
-  int32_t *node_outw = nullptr;  // per tile node: out offset | mask << 28
+  int32_t *node_outw = nullptr;  // per tile node: output offset (finishing pass)
+  uint8_t *node_fmask = nullptr;  // per tile node: free-component mask (finishing pass)
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units

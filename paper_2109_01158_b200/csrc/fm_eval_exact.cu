@@ -139,8 +139,20 @@ __device__ __forceinline__ double log_series(double det, double inv_dp1) {
 
 // NH: P' = vol * dW/dF = a F + b cof with a = 2 C1 vol, b = vol (2 D1 (det-1) - 2 C1/det)
 // (models.py:103-120 regrouped).  p-Laplace: P' = vol |g|^(p-2) g.
-template <int DIM, int MODEL>
+// Admissibility near det F = 0 follows the reference exactly: the FMA forms
+// of F and det F differ from numpy's in the last bits, which only matters for
+// the sign decision (J = +inf, models.py:94-99; the exact path's raise,
+// models.py:107-110) when det F is tiny.  Below DET_NEAR the element's F is
+// recomputed in einsum order (assembly.py:35-49) and det F as the six-term
+// left-to-right expansion (models.py:59-71), bit for bit numpy's values, and
+// that det decides and enters W and P'.  (A sign flip above DET_NEAR would need
+// |F_ij| ~ 1e4, i.e. fma / numpy differences of 1e-3.)
+constexpr double DET_NEAR = 1e-3;
+
+template <int DIM, int MODEL, int D>
 __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
+                                          const double (&vv)[D][DIM + 1],
+                                          const double (&g)[DIM][DIM + 1],
                                           double vol, const ModelArgs &m, bool want_w,
                                           double (&P)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
                                           double &W, bool &bad, bool &far, double &det_out,
@@ -151,6 +163,11 @@ __device__ __forceinline__ void element_P(const double (&F)[MODEL == FM_MODEL_NE
     double det = 0.0;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) det = fma(F[0][k], C[0][k], det);
+    if (!(det > DET_NEAR)) {  // rare: the reference's own det decides
+      double Fr[DIM][DIM];
+      grad_F<DIM, DIM>(vv, g, Fr);
+      det = det_F<DIM>(Fr);
+    }
     bad = !(det > 0.0);
     // 1/det and (for J) 1/(det+1) from one division
     const double dp1 = det + 1.0;
@@ -471,7 +488,8 @@ __global__ void __launch_bounds__(CT, MINB)
       const int *xch = xch_of(tb);
       const bool has_nodes = tm.node_count > 0;
       const bool my_node = tid < tm.node_count;
-      int outw = 0;
+      int outw = 0, fmask = 0;
+      bool cross = false;
       int4 nd = make_int4(0, 0, 0, 0);  // node descriptor (entry offset, per-chunk counts)
       double bj[D], acc[D];
 #pragma unroll
@@ -481,6 +499,8 @@ __global__ void __launch_bounds__(CT, MINB)
         cl = __ldg(a.node_clo + tm.node_begin + tid);
         nd = desc[tid];
         outw = nd.w;
+        fmask = desc_mask(nd);
+        cross = ((unsigned)nd.x & CROSS_FLAG) != 0;
         if (b && !HV) {
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
@@ -541,7 +561,8 @@ __global__ void __launch_bounds__(CT, MINB)
             bad_any |= bad;
           } else if (has_nodes) {
             bool bad;
-            element_P<DIM, MODEL>(F, E.vol, mdl, WJ && own, P, Wel, bad, far, det_el, ls_el);
+            element_P<DIM, MODEL, D>(F, vv, E.g, E.vol, mdl, WJ && own, P, Wel, bad, far, det_el,
+                                     ls_el);
             bad_any |= bad;
           } else if (WJ) {
             jsum += E.vol * density<DIM, MODEL>(F, mdl);
@@ -620,17 +641,16 @@ __global__ void __launch_bounds__(CT, MINB)
         for (int k = 0; k < D; ++k) bvsum += bj[k] * nv[k * CAP + cl];
       }
       if (my_node) {
-        if ((unsigned)outw & CROSS_FLAG) {
+        if (cross) {
           // cross entries follow in the finishing pass: dense partial by tile node
 #pragma unroll
           for (int k = 0; k < D; ++k)
             a.partial[(int64_t)(tm.node_begin + tid) * D + k] = acc[k] - bj[k];
         } else {
-          const int mask = (unsigned)outw >> OUT_MASK_SHIFT;
-          int o = outw & ((1 << OUT_MASK_SHIFT) - 1);
+          int o = outw;
 #pragma unroll
           for (int k = 0; k < D; ++k)
-            if (mask & (1 << k)) g[o++] = acc[k] - bj[k];
+            if (fmask & (1 << k)) g[o++] = acc[k] - bj[k];
         }
       }
       ++j;
@@ -665,6 +685,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int32_t *__restrict__ nodes,
                                                       const int32_t *__restrict__ xbase,
                                                       const int32_t *__restrict__ outw,
+                                                      const uint8_t *__restrict__ fmask,
                                                       const int32_t *__restrict__ xinv,
                                                       const double *__restrict__ xbuf,
                                                       const double *__restrict__ partial,
@@ -679,7 +700,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     const int lo = __ldg(xbase + k), hi = __ldg(xbase + k + 1);
     if (hi == lo) continue;
     const int w = __ldg(outw + k);
-    const int mask = (unsigned)w >> OUT_MASK_SHIFT;
+    const int mask = __ldg(fmask + k);
     if (!(mask & (1 << j))) continue;
     double sum = partial[k * D + j];
     // four entries per step: their slot loads, then their value loads, are
@@ -693,7 +714,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
       sum = (((sum + x0) + x1) + x2) + x3;
     }
     for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
-    g[(w & ((1 << OUT_MASK_SHIFT) - 1)) + __popc(mask & ((1 << j) - 1))] = sum;
+    g[w + __popc(mask & ((1 << j) - 1))] = sum;
   }
   if (!jf.out) return;
   __shared__ double red[32];
@@ -738,16 +759,17 @@ int finish_cross_grid(int d, int64_t ntn) {
 }
 
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,
-                                const int32_t *outw, const int32_t *xinv, const double *xbuf,
+                                const int32_t *outw, const uint8_t *fmask, const int32_t *xinv,
+                                const double *xbuf,
                                 const double *partial, double *g, const JFinal &jf,
                                 cudaStream_t s) {
   const int grid = finish_cross_grid(d, ntn);
   if (d == 3)
-    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
+    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
   else if (d == 2)
-    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
+    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
   else
-    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, xinv, xbuf, partial, g, jf);
+    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
   return cudaGetLastError();
 }
 

@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
   }
   if (mykey != ~0ull) atomicMin(badkey, mykey);
   if (my_node) {
-    const int mask = (unsigned)nd.w >> OUT_MASK_SHIFT;
-    int o = nd.w & ((1 << OUT_MASK_SHIFT) - 1);
+    const int mask = desc_mask(nd);
+    int o = nd.w;
     const double inv = 2.0 * eps;
 #pragma unroll
     for (int j = 0; j < D; ++j) {

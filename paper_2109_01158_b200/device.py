@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import ptr, require_cuda, stream_ptr, to_dev
+from ._device import checked, ptr, require_cuda, stream_ptr, to_dev
 
 DEFAULT_EPS = 1e-8  # gradients.py:20
 
@@ -80,7 +80,19 @@ class DeviceMesh:
         self.stats = {k: getattr(st, k) for k, _ in _lib.FmCtxStats._fields_}
         self.nodes_minim = nodes_minim
         self.nfree_dofs = self._count_free_dofs(fixed, nodes_minim)
+        self.device = torch.cuda.current_device()
         self._J = torch.empty(3, dtype=torch.float64, device="cuda")
+
+    # argument checks: raw pointers go to the kernels, so sizes / dtypes /
+    # devices are validated here (ValueError), never by assert
+    def _field(self, t, name):
+        return checked(t, name, self.nn * self.d, device=self.device)
+
+    def _free(self, t, name):
+        return checked(t, name, self.nfree_dofs, device=self.device)
+
+    def _jout(self, t, name="J"):
+        return checked(t, name, 3, at_least=True, device=self.device)
 
     def _count_free_dofs(self, fixed, nodes_minim):
         return int(fixed.numel() - int(fixed.sum().item()))
@@ -91,7 +103,10 @@ class DeviceMesh:
     # ---- evaluation (asynchronous on the current stream) --------------------
     def energy(self, v, model, b=None, densities=None, out=None):
         """J (device double[3]: J, sum vol*W, b.v) of assembly.py:94-106."""
-        out = self._J if out is None else out
+        out = self._J if out is None else self._jout(out, "out")
+        self._field(v, "v")
+        self._field(b, "b")
+        checked(densities, "densities", self.ne, device=self.device)
         m = _model(model)
         _lib.check(self._lib.fm_energy(self._h, C.byref(m), ptr(v), ptr(b), ptr(out),
                                        ptr(densities), stream_ptr()), "fm_energy")
@@ -101,6 +116,10 @@ class DeviceMesh:
         """gradients.py:124-149 into g (nfree_dofs,), fused with J when given."""
         if g is None:
             g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        self._field(v, "v")
+        self._field(b, "b")
+        self._free(g, "g")
+        self._jout(J)
         m = _model(model)
         _lib.check(self._lib.fm_grad_exact(self._h, C.byref(m), ptr(v), ptr(b), ptr(g), ptr(J),
                                            stream_ptr()), "fm_grad_exact")
@@ -111,6 +130,9 @@ class DeviceMesh:
         (fm_hvp_exact).  p: full field (d*nn,), zero on the Dirichlet dofs."""
         if out is None:
             out = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        self._field(v, "v")
+        self._field(p, "p")
+        self._free(out, "out")
         m = _model(model)
         _lib.check(self._lib.fm_hvp_exact(self._h, C.byref(m), ptr(v), ptr(p), ptr(out),
                                           stream_ptr()), "fm_hvp_exact")
@@ -120,6 +142,9 @@ class DeviceMesh:
         """gradients.py:84-121 into g (nfree_dofs,)."""
         if g is None:
             g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
+        self._field(v, "v")
+        self._field(b, "b")
+        self._free(g, "g")
         m = _model(model)
         _lib.check(self._lib.fm_grad_fd(self._h, C.byref(m), ptr(v), ptr(b), float(eps), ptr(g),
                                         stream_ptr()), "fm_grad_fd")
@@ -127,6 +152,8 @@ class DeviceMesh:
 
     def descent_step(self, v, g, alpha):
         """v_free <- v_free - alpha * g (Dirichlet dofs untouched)."""
+        self._field(v, "v")
+        self._free(g, "g")
         _lib.check(self._lib.fm_descent_step(self._h, ptr(v), ptr(g), float(alpha),
                                              stream_ptr()))
         return v
@@ -141,8 +168,11 @@ class DeviceMesh:
         so the shared interface values stay identical)."""
         if g is None:
             g = torch.empty(self.nfree_dofs, dtype=torch.float64, device="cuda")
-        if J_hist is not None and (J_hist.numel() < 3 * iters or not J_hist.is_contiguous()):
-            raise ValueError("J_hist must hold iters x 3 contiguous doubles")
+        self._field(v, "v")
+        self._field(b, "b")
+        self._free(g, "g")
+        if J_hist is not None:
+            checked(J_hist, "J_hist", 3 * int(iters), at_least=True, device=self.device)
         if exchange is None:
             m = _model(model)
             _lib.check(self._lib.fm_descent(self._h, C.byref(m), ptr(v), ptr(b), float(alpha),
@@ -235,24 +265,74 @@ def _model(model) -> _lib.FmModel:
 
 # ---------------------------------------------------------------------------
 # context cache for the numpy drop-in (frozen Mesh / Patches are immutable)
+#
+# One context per (mesh, d): build_patches is a deterministic function of the
+# mesh (patches.py:37-71), so the energy call (no patches) and the gradient
+# calls (the user's Patches) share it.  A Patches object is checked once
+# against the canonical CSR built on the device; only a non-canonical one
+# (a hand-made patch structure) gets a context of its own.
 
 _CTX: dict[tuple, DeviceMesh] = {}
+_CANONICAL: dict[tuple, set] = {}  # (id(mesh), d) -> ids of Patches equal to the canonical CSR
 
 
 def _drop(key):
     ctx = _CTX.pop(key, None)
     if ctx is not None:
         ctx.close()
+    _CANONICAL.pop(key, None)
+
+
+def _patch_arrays(patches):
+    pdev = attached(patches) or {}
+    prefix = pdev.get("prefix")
+    if prefix is None:
+        prefix = to_dev(np.asarray(patches.prefix, dtype=np.int64))
+    elems = pdev.get("elems")
+    if elems is None:
+        elems = to_dev(np.asarray(patches.elems, dtype=np.int64))
+    slot = pdev.get("slot")
+    if slot is None:
+        s = getattr(patches, "slot", None)
+        if s is None:
+            s = np.argmax(np.asarray(patches.logical), axis=1)
+        slot = to_dev(np.asarray(s, dtype=np.int64))
+    return prefix, elems, slot
+
+
+def _is_canonical(mesh, patches, d) -> bool:
+    if d != int(mesh.d):
+        return True  # the patches are not used (every dof free)
+    from .patches import build_patches_device
+    dev = attached(mesh) or {}
+    conn = dev.get("conn")
+    if conn is None:
+        conn = to_dev(np.asarray(mesh.elems2nodes, dtype=np.int64))
+    nm = dev.get("nodes_minim")
+    if nm is None:
+        nm = to_dev(np.asarray(mesh.nodes_minim, dtype=np.int64))
+    ref = build_patches_device(conn, nm, int(mesh.nn), int(mesh.dim) + 1)
+    got = _patch_arrays(patches)
+    return all(a.shape == b.shape and bool(torch.equal(a, b)) for a, b in zip(ref, got))
 
 
 def context_for(mesh, patches=None, d=None) -> DeviceMesh:
     d = int(mesh.d if d is None else d)
-    key = (id(mesh), id(patches) if patches is not None else 0, d)
+    key = (id(mesh), d)
+    if patches is not None:
+        seen = _CANONICAL.get(key)
+        if seen is None or id(patches) not in seen:
+            if not _is_canonical(mesh, patches, d):
+                key = (id(mesh), id(patches), d)
+            else:
+                _CANONICAL.setdefault(key, set()).add(id(patches))
+                weakref.finalize(patches, lambda k=key, i=id(patches):
+                                 _CANONICAL.get(k, set()).discard(i))
     ctx = _CTX.get(key)
     if ctx is None:
-        ctx = DeviceMesh.from_host(mesh, patches, d)
+        ctx = DeviceMesh.from_host(mesh, patches if len(key) == 3 else None, d)
         _CTX[key] = ctx
         weakref.finalize(mesh, _drop, key)
-        if patches is not None:
+        if len(key) == 3:
             weakref.finalize(patches, _drop, key)
     return ctx

@@ -77,13 +77,45 @@ class PLaplaceParams:
             raise ValueError("p-Laplacian exponent must satisfy p > 1")
 
 
+# the densities the CUDA engine implements: this package's classes and the
+# reference's own (femmin.models), matched by exact type
+_ENGINE_MODELS = {
+    ("paper_2109_01158_b200.models", "NeoHookean"): _lib.FM_MODEL_NEOHOOKEAN,
+    ("femmin.models", "NeoHookean"): _lib.FM_MODEL_NEOHOOKEAN,
+    ("paper_2109_01158_b200.models", "PLaplacian"): _lib.FM_MODEL_PLAPLACE,
+    ("femmin.models", "PLaplacian"): _lib.FM_MODEL_PLAPLACE,
+}
+
+
 def fm_model_struct(model) -> _lib.FmModel:
-    """C view of any model object with the reference protocol (.d .dim .params)."""
+    """C view of a model plugin (models.py:141-170: .d .dim .params).
+
+    The GPU kernels evaluate the Neo-Hookean and p-Laplace densities
+    themselves, so only models whose density IS one of those are accepted:
+    instances of exactly this package's or the reference's NeoHookean /
+    PLaplacian with their own density / ddensity.  A subclass, a duck-typed
+    plugin or an instance with an overridden density would otherwise get the
+    built-in law silently; it raises NotImplementedError instead (there is no
+    CPU fallback).
+    """
+    cls = type(model)
+    kind = _ENGINE_MODELS.get((cls.__module__, cls.__qualname__))
+    if kind is None:
+        raise NotImplementedError(
+            f"{cls.__module__}.{cls.__qualname__}: the GPU engine evaluates the built-in "
+            "NeoHookean and PLaplacian densities only (models.py:141-170); custom density "
+            "plugins are not supported")
+    for name in ("density", "ddensity"):
+        if name in getattr(model, "__dict__", {}):
+            raise NotImplementedError(
+                f"model.{name} is overridden on the instance; the GPU engine evaluates the "
+                "built-in density only")
     prm = model.params
-    if model.d == 1 and hasattr(prm, "p"):
-        return _lib.FmModel(_lib.FM_MODEL_PLAPLACE, int(model.dim), float(prm.p), 0.0, 0.0)
-    return _lib.FmModel(_lib.FM_MODEL_NEOHOOKEAN, int(model.dim), 0.0, float(prm.C1),
-                        float(prm.D1))
+    if kind == _lib.FM_MODEL_PLAPLACE:
+        if int(model.d) != 1:
+            raise ValueError("p-Laplacian model must have d = 1")
+        return _lib.FmModel(kind, int(model.dim), float(prm.p), 0.0, 0.0)
+    return _lib.FmModel(kind, int(model.dim), 0.0, float(prm.C1), float(prm.D1))
 
 
 def _stack(F):

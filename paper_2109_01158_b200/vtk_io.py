@@ -54,42 +54,65 @@ def write_vtk(path, points, cells, point_data=None, cell_data=None, title="femmi
 
 
 def read_vtk(path):
-    """Reader for files produced by :func:`write_vtk` (vtk_io.py:51-96).
+    """Read back a legacy ASCII unstructured grid as written by
+    :func:`write_vtk` (same contract as vtk_io.py:51-96: returns
+    ``(points, cells, point_data, cell_data)``; 2D files come back with the
+    z = 0 column).
 
-    Returns (points, cells, point_data, cell_data)."""
+    Token-stream parser: after the two header lines (version, title) the file
+    is a sequence of keyword sections, each followed by a known number of
+    numeric tokens, so the body is split once into tokens and walked with a
+    cursor (sections may span or share lines)."""
     with open(path) as fh:
-        lines = [ln.strip() for ln in fh]
-    i = 0
+        fh.readline()  # "# vtk DataFile Version 2.0"
+        fh.readline()  # title (free text)
+        tok = fh.read().split()
+    n_tok = len(tok)
+    pos = 0
+    points = np.zeros((0, 3))
+    cells = np.zeros((0, 0), dtype=np.int64)
+    data: dict[str, dict[str, np.ndarray]] = {"POINT_DATA": {}, "CELL_DATA": {}}
+    section, count = None, 0
 
-    def advance_to(prefix):
-        nonlocal i
-        while not lines[i].startswith(prefix):
-            i += 1
+    def take(n):
+        nonlocal pos
+        if pos + n > n_tok:
+            raise ValueError(f"{path}: truncated VTK file")
+        out = tok[pos:pos + n]
+        pos += n
+        return out
 
-    advance_to("POINTS")
-    npts = int(lines[i].split()[1])
-    points = np.array([[float(t) for t in lines[i + 1 + k].split()] for k in range(npts)])
-    i += 1 + npts
-    advance_to("CELLS")
-    ncells = int(lines[i].split()[1])
-    cells = np.array([[int(t) for t in lines[i + 1 + k].split()[1:]] for k in range(ncells)],
-                     dtype=np.int64)
-    i += 1 + ncells
-    point_data: dict[str, np.ndarray] = {}
-    cell_data: dict[str, np.ndarray] = {}
-    target, count = None, 0
-    while i < len(lines):
-        ln = lines[i]
-        if ln.startswith("POINT_DATA"):
-            target, count = point_data, npts
-        elif ln.startswith("CELL_DATA"):
-            target, count = cell_data, ncells
-        elif ln.startswith("SCALARS") and target is not None:
-            name = ln.split()[1]
-            target[name] = np.array([float(lines[i + 2 + k]) for k in range(count)])
-            i += 1 + count
-        i += 1
-    return points, cells, point_data, cell_data
+    while pos < n_tok:
+        key = take(1)[0]
+        if key in ("ASCII", "DATASET"):
+            if key == "DATASET":
+                take(1)
+        elif key == "POINTS":
+            n, _ = take(2)
+            points = np.asarray(take(3 * int(n)), dtype=float).reshape(int(n), 3)
+        elif key == "CELLS":
+            n, size = (int(x) for x in take(2))
+            flat = np.asarray(take(size), dtype=np.int64)
+            nv = int(flat[0]) if n else 0
+            cells = flat.reshape(n, nv + 1)[:, 1:] if n else np.zeros((0, 0), dtype=np.int64)
+        elif key == "CELL_TYPES":
+            take(int(take(1)[0]))
+        elif key in data:
+            section, count = key, int(take(1)[0])
+        elif key == "SCALARS":
+            name, _dtype = take(2)
+            ncomp = 1
+            if pos < n_tok and tok[pos] != "LOOKUP_TABLE":
+                ncomp = int(take(1)[0])
+            if pos < n_tok and tok[pos] == "LOOKUP_TABLE":
+                take(2)
+            if section is None:
+                raise ValueError(f"{path}: SCALARS outside POINT_DATA / CELL_DATA")
+            vals = np.asarray(take(count * ncomp), dtype=float)
+            data[section][name] = vals if ncomp == 1 else vals.reshape(count, ncomp)
+        else:
+            raise ValueError(f"{path}: unexpected VTK token {key!r}")
+    return points, cells, data["POINT_DATA"], data["CELL_DATA"]
 
 
 def write_solution_vtk(path, coords, conn, v, d, model=None, dm=None, b=None,

@@ -316,11 +316,163 @@ def case_vtk():
     print("vtk fixtures written")
 
 
+def case_hole(level=2, seed=2109):
+    """The reference's unstructured test domain (mesh.py:246-286,
+    bench.hole_problem): square with a circular hole, projected cavity nodes,
+    sliver removal and node compression.  Neo-Hookean (bench's BAR_MATERIAL,
+    HOLE_LOAD, Dirichlet on y = 0 and x = 0) at x + seeded noise, and a
+    p-Laplace p = 3 / p = 1.8 problem on the same mesh (d = 1, same Dirichlet
+    sets)."""
+    m = bench.hole_problem(level)
+    pt = femmin.build_patches(m)
+    model = NeoHookean(bench.BAR_MATERIAL, dim=2)
+    load = LinearLoad.assemble(m, bench.HOLE_LOAD, d=2)
+    h = float(np.sqrt(2.0 * m.volumes.mean()))
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    v[m.dofs_minim] += 1e-2 * h * (2.0 * O.uniform01(seed, m.dofs_minim) - 1.0)
+    out = _evaluate(m, pt, model, load, v, 1e-8)
+    tol = 1e-9
+    spec1 = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 1] < tol),
+                                 fmesh.DirichletRegion(where=lambda x: x[:, 0] < tol)])
+    m1 = fmesh.mark_dirichlet(fmesh._make_mesh(2, level, m.nodes2coord, m.elems2nodes), spec1,
+                              d=1)
+    p1 = femmin.build_patches(m1)
+    v1 = np.zeros(m1.nn)
+    v1[m1.dofs_minim] = O.uniform01(seed + 1, m1.dofs_minim)
+    load1 = LinearLoad.assemble(m1, -10.0, d=1)
+    extra = {}
+    for p in (3.0, 1.8):
+        r = _evaluate(m1, p1, PLaplacian(PLaplaceParams(p=p), dim=2), load1, v1, 1e-6)
+        extra.update({f"pl{p:g}_{k}": val for k, val in r.items()})
+    save(f"hole{level}", **_mesh_arrays(m), **_patch_arrays(pt), **out,
+         C1=np.float64(bench.BAR_MATERIAL.C1), D1=np.float64(bench.BAR_MATERIAL.D1),
+         **{"pl_" + k: val for k, val in _mesh_arrays(m1).items()},
+         **{"pl_" + k: val for k, val in _patch_arrays(p1).items()}, **extra)
+
+
+def case_renumbered(nx=6, ny=3, nz=3, seed=77):
+    """A generic (unstructured-numbering) mesh: the config-4 beam with nodes
+    and elements randomly permuted and every element's vertices rotated by an
+    even permutation (orientation kept), then the reference's own
+    _make_mesh (compute_p1_gradients), mark_dirichlet, build_patches and
+    evaluation."""
+    om = O.beam_mesh(nx, ny, nz, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    rng = np.random.default_rng(seed)
+    nn, ne = om.nodes2coord.shape[0], om.elems2nodes.shape[0]
+    pn = rng.permutation(nn)          # new node k = old node pn[k]
+    inv = np.empty(nn, np.int64)
+    inv[pn] = np.arange(nn)
+    coords = om.nodes2coord[pn]
+    conn = inv[om.elems2nodes][rng.permutation(ne)]
+    rot = [(0, 1, 2, 3), (1, 2, 0, 3), (2, 0, 1, 3), (0, 2, 3, 1), (3, 1, 0, 2)]
+    conn = np.stack([conn[k, list(rot[r])] for k, r in enumerate(rng.integers(0, 5, ne))])
+    m = fmesh._make_mesh(3, -1, coords, conn)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    m = fmesh.mark_dirichlet(m, spec, d=3)
+    pt = femmin.build_patches(m)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    model = NeoHookean(ElasticParams(E=E, nu=nu), dim=3)
+    model.params = Lame(mu / 2, lam / 2)
+    load = LinearLoad.assemble(m, (0.0, 0.0, -2.5e7), d=3)
+    v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+    v[m.dofs_minim] += 1e-2 * (2.0 / nx) * (2.0 * O.uniform01(seed, m.dofs_minim) - 1.0)
+    save(f"beam{nx}x{ny}x{nz}_renumbered", **_mesh_arrays(m), **_patch_arrays(pt),
+         **_evaluate(m, pt, model, load, v, 1e-8), C1=np.float64(mu / 2),
+         D1=np.float64(lam / 2), perm_nodes=pn)
+
+
+def case_exports(seed=5):
+    """The standalone helpers of the path on reference fixtures: gather /
+    evaluate_F (assembly.py:27-49), segment_sums with patch_prefix_indices
+    (patches.py:74-83), linear_term (assembly.py:89-91), the nodal-f
+    LinearLoad and the mass matrix (assembly.py:52-86)."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for tag, m, d in (("l", bench.lshape_problem(2), 1), ("b", bench.bar_problem(1), 3)):
+        from femmin import assembly as fas
+        pt = femmin.build_patches(m)
+        V = rng.normal(size=(m.nn, d))
+        vals = fas.gather(V, m.elems2nodes)
+        F = fas.evaluate_F(m.dphi, vals)
+        rows = rng.normal(size=d * pt.total_rows)
+        indx = fpatches.patch_prefix_indices(pt, d)
+        f_nodal = rng.normal(size=(m.nn, d))
+        load = LinearLoad.assemble(m, f_nodal, d=d)
+        M = fas.assemble_mass_matrix(m)
+        v = rng.normal(size=d * m.nn)
+        out.update({
+            f"{tag}_coords": m.nodes2coord, f"{tag}_conn": m.elems2nodes,
+            f"{tag}_volumes": m.volumes, f"{tag}_dphi": np.stack(m.dphi),
+            f"{tag}_V": V, f"{tag}_gather": np.stack(vals), f"{tag}_F": np.array(F),
+            f"{tag}_rows": rows, f"{tag}_indx": indx,
+            f"{tag}_segsum": fpatches.segment_sums(rows, indx),
+            f"{tag}_f_nodal": f_nodal, f"{tag}_b_nodal": load.b,
+            f"{tag}_M_indptr": M.indptr.astype(np.int64),
+            f"{tag}_M_indices": M.indices.astype(np.int64), f"{tag}_M_data": M.data,
+            f"{tag}_v": v, f"{tag}_linear_term": np.float64(fas.linear_term(load, v))})
+    save("exports", **out)
+
+
+def case_degenerate(n_cases=64, seed=3):
+    """Admissibility exactly at the det F = 0 boundary (models.py:59-71,
+    94-110): on the config-4 beam 4x2x2, element k's fourth node is moved onto
+    the plane of its other three (v3 = v0 + s (v1 - v0) + t (v2 - v0), random
+    s, t), so det F of that element is zero in exact arithmetic and a few ulps
+    of either sign (or exactly 0) in numpy's six-term expansion.  Recorded per
+    case: J (+inf or finite), whether exact_gradient raises, and the
+    element's det as numpy computes it."""
+    from femmin.models import batch_determinant
+    from femmin.assembly import evaluate_F, gather, unflatten
+    om = O.beam_mesh(4, 2, 2, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    m = fmesh._make_mesh(3, -1, om.nodes2coord, om.elems2nodes)
+    spec = fmesh.DirichletSpec([fmesh.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)])
+    m = fmesh.mark_dirichlet(m, spec, d=3)
+    pt = femmin.build_patches(m)
+    E, nu = 2e8, 0.3
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    model = NeoHookean(ElasticParams(E=E, nu=nu), dim=3)
+    model.params = Lame(mu / 2, lam / 2)
+    rng = np.random.default_rng(seed)
+    free = set(m.nodes_minim.tolist())
+    cand = [k for k in range(m.ne) if int(m.elems2nodes[k, 3]) in free]
+    vs, Js, raises, dets, elems = [], [], [], [], []
+    for c in range(n_cases):
+        k = cand[rng.integers(len(cand))]
+        v = np.ascontiguousarray(m.nodes2coord).ravel().copy()
+        n0, n1, n2, n3 = (int(x) for x in m.elems2nodes[k])
+        s, t = rng.uniform(0.1, 0.6, 2)
+        V = v.reshape(-1, 3)
+        V[n3] = V[n0] + s * (V[n1] - V[n0]) + t * (V[n2] - V[n0])
+        if c % 4 == 3:  # a hair off the plane: det ~ +-1e-16
+            V[n3] += rng.choice([-1.0, 1.0]) * 1e-16 * rng.uniform(0, 4, 3)
+        J, W = energy(v, m, model)
+        try:
+            exact_gradient(v, m, pt, model)
+            r = False
+        except InadmissibleStateError:
+            r = True
+        F = evaluate_F(m.dphi, gather(unflatten(v, 3), m.elems2nodes))
+        det = batch_determinant(F)
+        vs.append(v)
+        Js.append(J)
+        raises.append(r)
+        dets.append(det[k])
+        elems.append(k)
+    save("degenerate_beam4x2x2", **_mesh_arrays(m), **_patch_arrays(pt), v=np.array(vs),
+         J=np.array(Js), raises=np.array(raises), det=np.array(dets), elem=np.array(elems),
+         C1=np.float64(mu / 2), D1=np.float64(lam / 2))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # only the named cases, e.g. "descent"
         for name in sys.argv[1:]:
             globals()["case_" + name]()
         sys.exit(0)
+    case_hole()
+    case_renumbered()
+    case_exports()
+    case_degenerate()
     case_hessian()
     case_vtk()
     case_descent()

@@ -94,3 +94,73 @@ def test_product_package_never_imports_the_oracle():
                 bad = re.findall(r"(from\s+oracle|import\s+oracle|femmin_oracle|oracle/_ref)",
                                  src)
                 assert not bad, (f, bad)
+
+
+def test_model_dispatch_is_strict():
+    """Only the built-in densities reach the kernels (a subclass or a
+    duck-typed plugin must not silently get the Neo-Hookean / p-Laplace law)."""
+    from paper_2109_01158_b200 import (ElasticParams, NeoHookean, PLaplaceParams,
+                                       PLaplacian, _lib)
+    from paper_2109_01158_b200.models import LameParams, fm_model_struct
+    m = fm_model_struct(NeoHookean(ElasticParams(E=2e8, nu=0.3), dim=3))
+    assert m.kind == _lib.FM_MODEL_NEOHOOKEAN and m.dim == 3
+    m = fm_model_struct(NeoHookean(LameParams(1.0, 2.0), dim=2))
+    assert (m.C1, m.D1) == (1.0, 2.0)
+    m = fm_model_struct(PLaplacian(PLaplaceParams(p=1.8), dim=2))
+    assert m.kind == _lib.FM_MODEL_PLAPLACE and m.p == 1.8
+
+    class MyNH(NeoHookean):
+        def density(self, F):
+            return 0.0
+
+    with pytest.raises(NotImplementedError):
+        fm_model_struct(MyNH(ElasticParams(E=1.0, nu=0.3), dim=2))
+
+    class Duck:
+        d, dim = 1, 2
+        params = PLaplaceParams(p=3.0)
+
+        def density(self, G):
+            return 0.0
+
+    with pytest.raises(NotImplementedError):
+        fm_model_struct(Duck())
+    nh = NeoHookean(ElasticParams(E=1.0, nu=0.3), dim=2)
+    nh.density = lambda F: 0.0
+    with pytest.raises(NotImplementedError):
+        fm_model_struct(nh)
+
+
+def test_reference_model_objects_accepted():
+    """The reference's own NeoHookean / PLaplacian (femmin.models) dispatch to
+    the same kernels (drop-in: callers keep their model objects)."""
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present (GPU box)")
+    import sys
+    sys.path.insert(0, ref)
+    try:
+        import femmin.models as fmm
+    finally:
+        sys.path.remove(ref)
+    from paper_2109_01158_b200 import _lib
+    from paper_2109_01158_b200.models import fm_model_struct
+    m = fm_model_struct(fmm.NeoHookean(fmm.ElasticParams(E=2e8, nu=0.3), dim=3))
+    p = fmm.ElasticParams(E=2e8, nu=0.3)
+    assert m.kind == _lib.FM_MODEL_NEOHOOKEAN and (m.C1, m.D1) == (p.C1, p.D1)
+    m = fm_model_struct(fmm.PLaplacian(fmm.PLaplaceParams(p=3.0), dim=2))
+    assert m.kind == _lib.FM_MODEL_PLAPLACE and m.p == 3.0
+
+
+def test_device_argument_checks_on_cpu_tensors():
+    """Raw pointers reach the kernels only after a checked() pass: host
+    tensors, wrong dtypes or lengths raise ValueError (never an assert)."""
+    import torch
+    from paper_2109_01158_b200._device import checked, ptr
+    with pytest.raises(ValueError, match="CUDA"):
+        checked(torch.zeros(3, dtype=torch.float64), "v", 3)
+    with pytest.raises(ValueError, match="torch"):
+        checked([0.0] * 3, "v", 3)
+    with pytest.raises(ValueError):
+        ptr(torch.zeros(3))
+    assert checked(None, "b", 5) is None

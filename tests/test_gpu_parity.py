@@ -432,7 +432,7 @@ def test_plaplace_3d_vs_oracle(p):
     assert (np.abs(gn - gd) <= FD_FACTOR * scale + 1e-300).all()
 
 
-@pytest.mark.parametrize("cfg", ["cfg4", "cfg2"])
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg2", "cfg3", "cfg2_p1.8"])
 def test_full_size_sampled_dofs(cfg):
     """Full-size configs (too large for the CPU oracle whole): the fused
     gradient at 20,000 random free dofs against the oracle's per-dof

@@ -242,3 +242,98 @@ def test_sampled_exact_gradient_matches_full(golden):
                                   m.nodes_minim, 3, model, b, m.dofs_minim, sample)
     ref = g["g_exact"][sample]
     assert np.abs(gs - ref).max() <= 1e-12 * np.abs(g["g_exact"]).max()
+
+
+def _model_of(g, prefix=""):
+    if prefix == "" and "C1" in g:
+        return O.Model("nh", O.LameParams(float(g["C1"]), float(g["D1"])),
+                       int(g["coords"].shape[1]))
+    return None
+
+
+def test_hole_mesh_unstructured_bit_exact(golden):
+    """The reference's unstructured hole mesh (mesh.py:246-286): the oracle's
+    partitions / patches / P1 data and evaluation reproduce it bit for bit."""
+    g = golden("hole2")
+    m = _mesh_from_golden(g)
+    vol, dphi = O.p1_gradients(g["coords"], g["conn"])
+    np.testing.assert_array_equal(vol, g["volumes"])
+    np.testing.assert_array_equal(np.stack(dphi), g["dphi"])
+    p = O.build_patches(m)
+    _check_patches(p, g)
+    model = _model_of(g)
+    J, W = O.energy(g["v"], m, model, g["b"])
+    assert J == g["J"]
+    np.testing.assert_array_equal(W, g["densities"])
+    np.testing.assert_array_equal(O.exact_gradient(g["v"], m, p, model, g["b"]), g["g_exact"])
+    np.testing.assert_array_equal(O.numeric_gradient(g["v"], m, p, model, g["b"], 1e-8),
+                                  g["g_fd"])
+    gl = {k[3:]: val for k, val in g.items() if k.startswith("pl_")}
+    m1 = _mesh_from_golden(gl)
+    p1 = O.build_patches(m1)
+    np.testing.assert_array_equal(p1.elems, gl["p_elems"])
+    for pexp in (3.0, 1.8):
+        pre = f"pl{pexp:g}_"
+        model1 = O.Model("plap", O.PParams(pexp), 2)
+        assert O.energy(g[pre + "v"], m1, model1, g[pre + "b"])[0] == g[pre + "J"]
+        np.testing.assert_array_equal(O.exact_gradient(g[pre + "v"], m1, p1, model1, g[pre + "b"]),
+                                      g[pre + "g_exact"])
+
+
+def test_renumbered_beam_bit_exact(golden):
+    """Generic numbering (nodes / elements permuted, vertices rotated)."""
+    g = golden("beam6x3x3_renumbered")
+    m = _mesh_from_golden(g)
+    vol, dphi = O.p1_gradients(g["coords"], g["conn"])
+    np.testing.assert_array_equal(vol, g["volumes"])
+    np.testing.assert_array_equal(np.stack(dphi), g["dphi"])
+    fixed = O.fixed_mask(m, [(O.left_face, None)], 3)
+    mm = O.mark_dirichlet(m, fixed, 3)
+    _check_mesh(mm, g)
+    p = O.build_patches(mm)
+    _check_patches(p, g)
+    model = _model_of(g)
+    assert O.energy(g["v"], mm, model, g["b"])[0] == g["J"]
+    np.testing.assert_array_equal(O.exact_gradient(g["v"], mm, p, model, g["b"]), g["g_exact"])
+    np.testing.assert_array_equal(O.numeric_gradient(g["v"], mm, p, model, g["b"], 1e-8),
+                                  g["g_fd"])
+
+
+def test_standalone_helpers_bit_exact(golden):
+    """gather / evaluate_F / segment sums / nodal load / mass matrix /
+    linear term of the reference (assembly.py:27-91, patches.py:74-83)."""
+    g = golden("exports")
+    for tag, d in (("l", 1), ("b", 3)):
+        conn, V = g[f"{tag}_conn"], g[f"{tag}_V"]
+        vals = O.element_values(V.ravel(), d, conn)
+        np.testing.assert_array_equal(np.stack(vals), g[f"{tag}_gather"])
+        F = O.grad_field(list(g[f"{tag}_dphi"]), vals)
+        np.testing.assert_array_equal(np.array(F), g[f"{tag}_F"])
+        np.testing.assert_array_equal(O.cumsum_segments(g[f"{tag}_rows"], g[f"{tag}_indx"]),
+                                      g[f"{tag}_segsum"])
+        m = O.OMesh(int(g[f"{tag}_coords"].shape[1]), -1, g[f"{tag}_coords"], conn,
+                    g[f"{tag}_volumes"], list(g[f"{tag}_dphi"]), d, None, None, None, None,
+                    None)
+        M = O.mass_matrix(m)
+        np.testing.assert_array_equal(M.indptr, g[f"{tag}_M_indptr"])
+        np.testing.assert_array_equal(M.indices, g[f"{tag}_M_indices"])
+        np.testing.assert_array_equal(M.data, g[f"{tag}_M_data"])
+        np.testing.assert_array_equal(O.load_vector(m, g[f"{tag}_f_nodal"], d),
+                                      g[f"{tag}_b_nodal"])
+        assert float(g[f"{tag}_b_nodal"] @ g[f"{tag}_v"]) == g[f"{tag}_linear_term"]
+
+
+def test_degenerate_decisions_match_reference(golden):
+    """det F exactly at 0 (flattened element): +inf energy and the exact
+    path's raise decided by the six-term determinant, as the reference."""
+    g = golden("degenerate_beam4x2x2")
+    m = _mesh_from_golden(g)
+    p = _patches_from_golden(g)
+    model = _model_of(g)
+    for v, J, r in zip(g["v"], g["J"], g["raises"]):
+        assert O.energy(v, m, model)[0] == J
+        if r:
+            with pytest.raises(O.OracleInadmissible):
+                O.exact_gradient(v, m, p, model)
+        else:
+            O.exact_gradient(v, m, p, model)
