@@ -553,11 +553,18 @@ def _perturbed_row_densities(v, mesh, P, model, eps, with_libm=False):
                for m in range(dim)] for j in range(d)]             # gradients.py:35-51
         W = model.density(GG)
         if with_libm:
-            # magnitude of the libm-evaluated term of W (its ulp differs between
-            # numpy and CUDA): 2 C1 |log det| for Neo-Hookean, |W| for p-Laplace
+            # magnitude of the terms W is assembled from: each is rounded at
+            # the u level by any evaluation (numpy's, or the GPU's rank-one
+            # update of the same invariants, csrc/fm_eval_fd.cu), so two
+            # evaluations of one W+- differ by O(u * L):
+            # Neo-Hookean C1 (|F|^2 + dim + 2 |log det|) + D1 (det - 1)^2
+            # (models.py:89-100); p-Laplace |W| (one pow, models.py:123-126)
             if model.kind == "nh":
                 det = det_batch(GG)
-                L = 2.0 * model.params.C1 * np.abs(np.log(np.where(det > 0, det, 1.0)))
+                I1 = sum(GG[j][m] ** 2 for j in range(d) for m in range(dim))
+                ld = np.abs(np.log(np.where(det > 0, det, 1.0)))
+                L = (model.params.C1 * (I1 + dim + 2.0 * ld)
+                     + model.params.D1 * (det - 1.0) ** 2)
             else:
                 L = np.abs(W)
             out.append((W, L))
@@ -591,7 +598,8 @@ def numeric_gradient_direct(v, mesh: OMesh, P: OPatches, model, b=None, eps=1e-8
     """Same central differences with per-patch sequential sums instead of the
     global cumsum; also returns a per-dof roundoff scale
     u * sum_patch vol*(|W+| + |W-| + L+ + L-) / (2 eps) used as the FD parity
-    bound, L the magnitude of the libm-evaluated term (log / pow)."""
+    bound, L the magnitude of the terms W+- is assembled from (their rounding
+    is what two evaluations of the same W+- may differ by)."""
     d = model.d
     (Wm, Lm), (Wp, Lp) = _perturbed_row_densities(v, mesh, P, model, eps, with_libm=True)
     T = P.total_rows

@@ -30,6 +30,7 @@ UNITS = {
     "fm_ctx.cu": [],
     "fm_eval_exact.cu": [],
     "fm_eval_ref.cu": [],
+    "fm_eval_fd.cu": [],
     "fm_hessian.cu": [],
 }
 

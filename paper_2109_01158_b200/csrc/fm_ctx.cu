@@ -471,6 +471,58 @@ __global__ void k_chunk_blocks(int n_tiles, const TileMeta *meta, const int4 *de
   }
 }
 
+// Row-major FD items: per tile (one CTA) and chunk, the chunk's node entries
+// (node-major in its entry block) re-listed in (row, slot) order with their
+// node-major position p, so that the FD kernel's consecutive threads work on
+// consecutive element rows (shared-memory row reads broadcast instead of
+// conflicting) and still write their results to the node-major slots.
+// (row, slot) pairs are unique, so the order is deterministic.
+__global__ void k_fd_items(int n_tiles, const TileMeta *meta, const uint16_t *blocks, int ct,
+                           uint32_t *items) {
+  extern __shared__ uint32_t rmask[];  // ct row masks | ct row starts
+  uint32_t *rstart = rmask + ct;
+  __shared__ int wsum[32];
+  const int t = blockIdx.x;
+  const TileMeta tm = meta[t];
+  const int nch = (tm.own_count + tm.halo_count + ct - 1) / ct;
+  const int H = blk_header(tm.node_count);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int ch = 0; ch < nch; ++ch) {
+    const uint16_t *blk = blocks + tm.blk_base + (int64_t)ch * tm.blk_stride;
+    uint32_t *out = items + tm.blk_base + (int64_t)ch * tm.blk_stride;
+    const int total = blk[tm.node_count];
+    for (int r = threadIdx.x; r < ct; r += blockDim.x) rmask[r] = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < total; p += blockDim.x) {
+      const int en = blk[H + p];
+      atomicOr(&rmask[(en >> 2) - ch * ct], 1u << (en & 3));
+    }
+    __syncthreads();
+    // exclusive scan of the rows' entry counts (blockDim.x == ct)
+    const int r = threadIdx.x;
+    const int cnt = __popc(rmask[r]);
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int u = 0; u < w; ++u) before += wsum[u];
+    rstart[r] = before + incl - cnt;
+    (void)nw;
+    __syncthreads();
+    for (int p = threadIdx.x; p < total; p += blockDim.x) {
+      const int en = blk[H + p];
+      const int rr = (en >> 2) - ch * ct, l = en & 3;
+      const int pos = rstart[rr] + __popc(rmask[rr] & ((1u << l) - 1u));
+      out[pos] = ((uint32_t)p << 16) | ((uint32_t)rr << 2) | (uint32_t)l;
+    }
+    __syncthreads();
+  }
+}
+
 // (tile, halo?, element) keys of every patch row: te order = own first, then halo
 __global__ void k_pair_keys(int64_t nfree, const int64_t *prefix, const int64_t *elems,
                             const int64_t *slot, const int32_t *tile_of_rank,
@@ -1353,6 +1405,7 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
       c->blk_cap = std::max(c->blk_cap, stride);
     }
     CK(cudaMemcpyAsync(c->meta, hm.data(), hm.size() * sizeof(TileMeta), cudaMemcpyHostToDevice, s));
+    c->blk_total = blk_total;
     CK(dmalloc(&c->chunk_blocks, blk_total + 8, &B));
     CK(cudaMemsetAsync(c->chunk_blocks, 0, (blk_total + 8) * 2, s));
     k_chunk_blocks<<<n_tiles, c->tile_nodes, 0, s>>>(n_tiles, c->meta, c->node_desc,
@@ -1589,7 +1642,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw, c->node_fmask,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
-                  c->xnodes,    c->dof_pos};
+                  c->xnodes,    c->dof_pos,   c->fd_items};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1704,9 +1757,17 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   if (c->n_tiles == 0) return FM_OK;
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
-  TimedLaunch tl(c, s);
   const int dm = model->kind == FM_MODEL_NEOHOOKEAN ? c->dim : 1;
-  if (tile_fd_smem(c->dim, dm, c->clo_cap, c->chunk_entry_cap, c->tile_nodes, c->blk_cap) >
+  if (!c->fd_items) {  // first FD call: the row-major item lists (4 B per entry slot)
+    FM_CUDA(cudaMalloc(&c->fd_items, (size_t)(c->blk_total + 8) * 4));
+    c->bytes += (size_t)(c->blk_total + 8) * 4;
+    k_fd_items<<<c->n_tiles, c->tile_nodes, 2 * c->tile_nodes * 4, s>>>(
+        c->n_tiles, c->meta, c->chunk_blocks, c->tile_nodes, c->fd_items);
+    FM_CUDA(cudaGetLastError());
+    c->launches++;
+  }
+  TimedLaunch tl(c, s);
+  if (tile_fd_smem(c->dim, model->kind, c->clo_cap, c->chunk_entry_cap, c->tile_nodes) >
       227 * 1024) {
     set_error("FD tile staging exceeds shared memory; use smaller tiles");
     return FM_INVALID_ARG;

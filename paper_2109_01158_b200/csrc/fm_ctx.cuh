@@ -243,6 +243,10 @@ struct TileArgs {
   int entry_cap;               // max entries of one tile, rounded up to 8
   int blk_cap;                 // max chunk entry block, u16 units
   int clo_cap;                 // max closure size, rounded up to 4
+  // FD items (built on the first FD call): per tile and chunk, at the chunk
+  // block's index range, the chunk's entries in ROW-major order, each
+  // p << 16 | row << 2 | slot with p its node-major position (stg slot)
+  const uint32_t *fd_items;
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
@@ -296,6 +300,8 @@ struct fm_ctx {
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units
+  int64_t blk_total = 0;             // size of chunk_blocks, u16 units
+  uint32_t *fd_items = nullptr;      // row-major FD items (TileArgs::fd_items), lazily built
   int64_t n_cross = 0;
   int32_t *fixed_nodes = nullptr;  // nodes without a free dof (their b.v: finishing pass)
   int64_t n_fixed_nodes = 0;
@@ -316,6 +322,6 @@ struct fm_ctx {
                         loc,     closure, flags,   node_desc,       node_entries, chunk_blocks,
                         rank_of, xkey,
                         xpos,    xchunk,  xbuf,            partial,   node_clo,    n_tiles,
-                        n_tiles_all, entry_cap, blk_cap, clo_cap};
+                        n_tiles_all, entry_cap, blk_cap, clo_cap, fd_items};
   }
 };

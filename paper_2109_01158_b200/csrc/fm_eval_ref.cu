@@ -1,4 +1,5 @@
-// Energy-only streaming kernel and the nodal-patch finite-difference kernel.
+// Energy-only streaming kernel, the descent update and the row-batch model
+// plugin (the nodal-patch finite-difference kernel is in fm_eval_fd.cu).
 // F, det, I1, W follow the reference's rounding order exactly through the
 // explicit round-to-nearest forms of fm_density.cuh (assembly.py:35-49,
 // models.py:59-126); only the libm ulps of log/pow differ from numpy.
@@ -64,322 +65,6 @@ __global__ void __launch_bounds__(1024) k_finalize(const double *__restrict__ jp
   }
 }
 
-// ----------------------------------------------------------------- FD
-// gradients.py:84-121.  One CTA per node tile; its element list (own + halo,
-// dealt order) in chunks of CT rows, three phases per chunk:
-//  rows   thread r loads record c0 + r (halo rows take this tile's closure
-//         indices from halo_loc), gathers v from the tile's node values
-//         (closure gathered once per tile) and forms the unperturbed F
-//         (einsum order); record and F go to shared memory.
-//  items  the chunk's node entries (te << 2 | slot) flattened in node order (a
-//         block scan of the per-chunk counts in node_desc), times the D
-//         components.  Item (j, f) recomputes row j of F from the perturbed
-//         nodal values v_l -/+ eps (gradients.py:105-106, einsum order); the
-//         other rows are the unperturbed F (evaluate_GG, gradients.py:35-51);
-//         vol*W of both signs is staged.  Work per thread is even whatever the
-//         mix of own / halo elements and owned slots.
-//  nodes  node thread n sums its entries' minus and plus values separately in
-//         ascending tile-element order; g = (S+ - S-)/(2 eps) - b
-//         (gradients.py:118-120).
-// A non-finite density latches the smallest key (sign, j, free rank, element),
-// i.e. the first offending stacked row in reference order (gradients.py:77-81).
-template <int DIM, int CT>
-struct FdLayout {
-  // expanded shared-memory rows: vol | dphi[DIM][DIM + 1] | loc word
-  // (2D: +1 pad double, an odd number of 8-byte words per row, so the
-  // row-per-lane stores of the rows phase hit distinct bank pairs: cfg3 FD
-  // 0.52 -> 0.45 ms; in 3D the pad was slower, 6.89 -> 7.08 ms)
-  static constexpr int FRB = 8 * (2 + DIM * (DIM + 1) + (DIM == 2 ? 1 : 0));
-  __host__ __device__ static size_t r16(size_t x) { return (x + 15) / 16 * 16; }
-  __host__ __device__ static size_t nodev(int D, int cap) { return r16((size_t)D * cap * 8); }
-  __host__ __device__ static size_t recs() { return (size_t)CT * FRB; }
-  __host__ __device__ static size_t fbuf(int D) { return r16((size_t)CT * D * DIM * 8); }
-  __host__ __device__ static size_t stg(int D, int ech) { return (size_t)D * ech * 16; }
-  __host__ __device__ static size_t flat(int blk_cap) { return r16((size_t)blk_cap * 2); }
-  // 3D Neo-Hookean: per row det0, 1/det0, log(det0) of the unperturbed F
-  // (2D: register-bound at 4 CTAs per SM, the reuse spills; measured slower)
-  __host__ __device__ static size_t lrow(int D) {
-    return D == DIM && DIM == 3 ? (size_t)CT * 3 * 8 : 0;
-  }
-  __host__ __device__ static size_t total(int D, int cap, int ech, int blk_cap) {
-    return nodev(D, cap) + recs() + fbuf(D) + lrow(D) + stg(D, ech) + flat(blk_cap) + 32 * 4;
-  }
-};
-
-// exclusive block scan of x (CT threads); total in every thread
-template <int CT>
-__device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
-  constexpr int NW = CT / 32;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int incl = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < NW ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < NW) wsum[lane] = t;
-  }
-  __syncthreads();
-  total = wsum[NW - 1];
-  return (w ? wsum[w - 1] : 0) + incl - x;
-}
-
-#ifndef FM_FD_PREFETCH
-#define FM_FD_PREFETCH 1
-#endif
-
-// 3D: 2 x 256 threads per SM (<= 128 registers); 2D: 4 x 256 (<= 64; FD at
-// cfg2 3.59 ms with 2, 2.69 with 3, 2.34 with 4 CTAs per SM)
-template <int DIM, int MODEL, int CT>
-__global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
-    k_tile_fd(TileArgs a, const double *__restrict__ v, const double *__restrict__ b, double eps,
-              double *__restrict__ g, unsigned long long *badkey, ModelArgs mdl, int ech) {
-  constexpr int NV = DIM + 1;
-  constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  constexpr int RB = RecBytes<DIM>::value;
-  constexpr int NQ = RB / 16;
-  constexpr int NF = D * DIM;
-  using L = FdLayout<DIM, CT>;
-  constexpr int FRB = L::FRB;
-  constexpr int LW = 1 + DIM * NV;  // shared row word holding the closure indices
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int CAP = a.clo_cap;
-  double *nodev = reinterpret_cast<double *>(smem);
-  unsigned char *recs = smem + L::nodev(D, CAP);
-  double *Fb = reinterpret_cast<double *>(recs + L::recs());
-  double *lrow = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(Fb) + L::fbuf(D));
-  double2 *stg = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(lrow) + L::lrow(D));
-  uint16_t *flat = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(stg) +
-                                                L::stg(D, ech));
-  int *wsum = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(flat) + L::flat(a.blk_cap));
-  (void)wsum;
-  const int tid = threadIdx.x;
-
-  const TileMeta tm = a.meta[blockIdx.x];
-  if (tm.node_count == 0) return;  // orphan tile: no free node, nothing to differentiate
-  for (int i = tid; i < tm.clo_count; i += CT) {
-    const double *src = v + (int64_t)__ldg(a.closure + tm.clo_begin + i) * D;
-#pragma unroll
-    for (int k = 0; k < D; ++k) nodev[k * CAP + i] = __ldg(src + k);
-  }
-  const bool my_node = tid < tm.node_count;
-  int4 nd = make_int4(0, 0, 0, 0);
-  if (my_node) nd = a.node_desc[tm.node_begin + tid];
-  double accm[D], accp[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) accm[j] = accp[j] = 0.0;
-  unsigned long long mykey = ~0ull;
-  __syncthreads();
-
-  const int ne_t = tm.own_count + tm.halo_count;
-  // storage id of this thread's row of the next chunk, loaded one chunk ahead
-  auto row_src = [&](int e) -> int64_t {
-    if (e >= ne_t) return -1;
-    return e >= tm.own_count ? (int64_t)__ldg(a.halo_ids + tm.halo_begin + e - tm.own_count)
-                             : (int64_t)tm.own_begin + e;
-  };
-  int64_t s_next = row_src(tid);
-  for (int c0 = 0, ch = 0; c0 < ne_t; c0 += CT, ++ch) {
-    // ---- rows: record + unperturbed F of tile element c0 + tid
-    const int e = c0 + tid;
-    const int64_t s = s_next;
-    if (e < ne_t) {
-      const bool halo = e >= tm.own_count;
-      const int h = tm.halo_begin + e - tm.own_count;
-      const double2 *p = reinterpret_cast<const double2 *>(a.aos + s * RB);
-      double2 q[NQ];
-#pragma unroll
-      for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
-      const uint2 lw = halo ? __ldg(a.halo_loc + h) : __ldg(a.loc + s);
-      Elem<DIM> E;
-      decode_elem<DIM>(q, E);
-      decode_loc(lw, E.loc);
-      double *dst = reinterpret_cast<double *>(recs + tid * FRB);
-      dst[0] = E.vol;
-#pragma unroll
-      for (int m = 0; m < DIM; ++m)
-#pragma unroll
-        for (int l = 0; l < NV; ++l) dst[1 + m * NV + l] = E.g[m][l];
-      *reinterpret_cast<uint2 *>(dst + LW) = lw;
-      double vv[D][NV];
-#pragma unroll
-      for (int l = 0; l < NV; ++l)
-#pragma unroll
-        for (int k = 0; k < D; ++k) vv[k][l] = nodev[k * CAP + E.loc[l]];
-      double F[D][DIM];
-      grad_F<DIM, D>(vv, E.g, F);
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int m = 0; m < DIM; ++m) Fb[tid * NF + j * DIM + m] = F[j][m];
-      if constexpr (MODEL == FM_MODEL_NEOHOOKEAN && DIM == 3) {
-        // the row's log(det F) once: the 2 D perturbed states of each of its
-        // entries differ from it by O(eps) (log_near)
-        const double det0 = det_F<DIM>(F);
-        lrow[tid] = det0;
-        lrow[CT + tid] = 1.0 / det0;
-        lrow[2 * CT + tid] = det0 > 0.0 ? log(det0) : NAN;
-      }
-    }
-    // next chunk: its storage ids now, its own records towards L2
-    s_next = row_src(e + CT);
-    if (FM_FD_PREFETCH && s_next >= 0 && e + CT < tm.own_count) {
-      const uint8_t *pn = a.aos + s_next * RB;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + RB - 1));
-    }
-    // ---- this chunk's entries in node order: the chunk's entry block (node
-    // offsets + entries), copied as is
-    {
-      const uint4 *src = reinterpret_cast<const uint4 *>(a.chunk_blocks + tm.blk_base +
-                                                         (int64_t)ch * tm.blk_stride);
-      uint4 *dst = reinterpret_cast<uint4 *>(flat);
-      for (int i = tid; i < tm.blk_stride / 8; i += CT) dst[i] = __ldg(src + i);
-    }
-    __syncthreads();  // (also publishes the rows)
-    const int H = blk_header(tm.node_count);
-    const int base = my_node ? flat[tid] : 0;
-    const int cnt = my_node ? flat[tid + 1] - base : 0;
-    const int total = flat[tm.node_count];
-    // ---- items f (one entry: element row r, slot l), all D components and both
-    // signs.  The row's data (dphi, unperturbed F, closure indices) are read
-    // once per entry; j is a compile-time constant of each unrolled pass (no
-    // selects between rows), the slot l is not, so the words of slot l are
-    // addressed directly.  Row j of F keeps the einsum order (p0+p2)+(p1+p3)
-    // [NV = 3: (p0+p2)+p1]: the pair holding p_l is (p_l + partner), the other
-    // pair is unperturbed, and IEEE addition is commutative, so only p_l
-    // depends on the sign.
-    for (int f = tid; f < total; f += CT) {
-      const int en = flat[H + f];
-      const int r = (en >> 2) - c0, l = en & 3;
-      const unsigned char *rec = recs + r * FRB;
-      const double *rd = reinterpret_cast<const double *>(rec);  // vol | dphi[m][k]
-      const unsigned long long lw = *reinterpret_cast<const unsigned long long *>(rec + LW * 8);
-      auto gat = [&](int m, int k) { return rd[1 + m * NV + k]; };
-      double F0[D][DIM];
-#pragma unroll
-      for (int jj = 0; jj < D; ++jj)
-#pragma unroll
-        for (int m = 0; m < DIM; ++m) F0[jj][m] = Fb[r * NF + jj * DIM + m];
-      int lp, la = 0, lb = 0;
-      if constexpr (NV == 4) {
-        lp = l ^ 2;
-        la = (l + 1) & 3;
-        lb = (l + 3) & 3;
-      } else {
-        lp = l == 1 ? 0 : 2 - l;
-        la = l == 1 ? 2 : 1;
-      }
-      double gl[DIM];
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) gl[m] = gat(m, l);
-      const int cl = (int)((lw >> (16 * l)) & 0xffffull), cp = (int)((lw >> (16 * lp)) & 0xffffull);
-      const int ca = (int)((lw >> (16 * la)) & 0xffffull), cb = (int)((lw >> (16 * lb)) & 0xffffull);
-      const double vol = rd[0];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const double *nvj = nodev + j * CAP;
-        const double vl = nvj[cl];
-        double q1[DIM], q2[DIM];
-        if constexpr (NV == 4) {
-          const double vp = nvj[cp], va = nvj[ca], vb = nvj[cb];
-#pragma unroll
-          for (int m = 0; m < DIM; ++m) {
-            q1[m] = rmul(vp, gat(m, lp));                               // partner of p_l
-            q2[m] = radd(rmul(va, gat(m, la)), rmul(vb, gat(m, lb)));  // the other pair
-          }
-        } else {
-          const double vp = nvj[cp], vo = nvj[ca];
-#pragma unroll
-          for (int m = 0; m < DIM; ++m) {
-            q1[m] = rmul(vp, gat(m, lp));
-            q2[m] = rmul(vo, gat(m, la));
-          }
-        }
-        double w[2];
-#pragma unroll
-        for (int sg = 0; sg < 2; ++sg) {
-          const double ve = radd(vl, sg ? eps : -eps);
-          double Fp[D][DIM];
-#pragma unroll
-          for (int jj = 0; jj < D; ++jj)
-#pragma unroll
-            for (int m = 0; m < DIM; ++m) Fp[jj][m] = F0[jj][m];
-#pragma unroll
-          for (int m = 0; m < DIM; ++m) {
-            const double pl = rmul(ve, gl[m]);
-            if constexpr (NV == 4) {
-              Fp[j][m] = radd(radd(pl, q1[m]), q2[m]);
-            } else {  // (p0+p2)+p1: l = 1 is the lone term
-              Fp[j][m] = l == 1 ? radd(radd(q1[m], q2[m]), pl) : radd(radd(pl, q1[m]), q2[m]);
-            }
-          }
-          double W;
-          if constexpr (MODEL == FM_MODEL_NEOHOOKEAN && DIM == 3) {
-            W = density_nh_near<DIM>(Fp, mdl, lrow[r], lrow[CT + r], lrow[2 * CT + r]);
-          } else {
-            W = density<DIM, MODEL>(Fp, mdl);
-          }
-          if (!isfinite(W)) {
-            const int node = __ldg(a.closure + tm.clo_begin + cl);
-            const int te = r + c0;
-            const int64_t s = te < tm.own_count
-                                  ? (int64_t)tm.own_begin + te
-                                  : (int64_t)__ldg(a.halo_ids + tm.halo_begin + te - tm.own_count);
-            const unsigned long long key = ((unsigned long long)sg << 63) |
-                                           ((unsigned long long)j << 61) |
-                                           ((unsigned long long)__ldg(a.rank_of + node) << 31) |
-                                           (unsigned long long)__ldg(a.s2o + s);
-            mykey = key < mykey ? key : mykey;
-          }
-          w[sg] = rmul(vol, W);
-        }
-        stg[j * ech + f] = make_double2(w[0], w[1]);
-      }
-    }
-    __syncthreads();
-    // ---- nodes: ascending tile-element order, minus and plus separately
-    if (my_node) {
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-        for (int k = 0; k < cnt; ++k) {
-          const double2 x = stg[j * ech + base + k];
-          accm[j] += x.x;
-          accp[j] += x.y;
-        }
-    }
-    __syncthreads();
-  }
-  if (mykey != ~0ull) atomicMin(badkey, mykey);
-  if (my_node) {
-    const int mask = desc_mask(nd);
-    int o = nd.w;
-    const double inv = 2.0 * eps;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      if (mask & (1 << j)) {
-        const double q = (accp[j] - accm[j]) / inv;
-        g[o++] = b ? q - __ldg(b + (int64_t)nd.z * D + j) : q;
-      }
-    }
-  }
-}
-
-size_t tile_fd_smem(int dim, int d, int clo_cap, int ech, int ct, int blk_cap) {
-  if (ct == 128)
-    return dim == 3 ? FdLayout<3, 128>::total(d, clo_cap, ech, blk_cap) : FdLayout<2, 128>::total(d, clo_cap, ech, blk_cap);
-  return dim == 3 ? FdLayout<3, 256>::total(d, clo_cap, ech, blk_cap) : FdLayout<2, 256>::total(d, clo_cap, ech, blk_cap);
-}
-
 // ----------------------------------------------------------------- descent
 // free dof q (the order of g and dofs_minim) -> its position in v
 __global__ void k_dof_pos(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,
@@ -435,38 +120,6 @@ cudaError_t launch_finalize(const double *jp, int nj, const double *dp, int nd, 
                             cudaStream_t s) {
   k_finalize<<<1, 1024, 0, s>>>(jp, nj, dp, nd, out);
   return cudaGetLastError();
-}
-
-template <int DIM, int MODEL, int CT>
-static cudaError_t fd_t(const TileArgs &a, int n_tiles, int ech, const double *v, const double *b,
-                        double eps, double *g, unsigned long long *badkey, const ModelArgs &m,
-                        cudaStream_t s) {
-  constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  const size_t smem = FdLayout<DIM, CT>::total(D, a.clo_cap, ech, a.blk_cap);
-  auto k = k_tile_fd<DIM, MODEL, CT>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<n_tiles, CT, smem, s>>>(a, v, b, eps, g, badkey, m, ech);
-  return cudaGetLastError();
-}
-
-template <int DIM, int MODEL>
-static cudaError_t fd_ct(const TileArgs &a, int n_tiles, int ct, int ech, const double *v,
-                         const double *b, double eps, double *g, unsigned long long *badkey,
-                         const ModelArgs &m, cudaStream_t s) {
-  if (ct == 128) return fd_t<DIM, MODEL, 128>(a, n_tiles, ech, v, b, eps, g, badkey, m, s);
-  return fd_t<DIM, MODEL, 256>(a, n_tiles, ech, v, b, eps, g, badkey, m, s);
-}
-
-cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
-                           const double *v, const double *b, double eps, double *g,
-                           unsigned long long *badkey, const ModelArgs &m, cudaStream_t s) {
-  if (dim == 2 && model == FM_MODEL_PLAPLACE)
-    return fd_ct<2, FM_MODEL_PLAPLACE>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
-  if (dim == 3 && model == FM_MODEL_PLAPLACE)
-    return fd_ct<3, FM_MODEL_PLAPLACE>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
-  if (dim == 2)
-    return fd_ct<2, FM_MODEL_NEOHOOKEAN>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
-  return fd_ct<3, FM_MODEL_NEOHOOKEAN>(a, n_tiles, ct, ech, v, b, eps, g, badkey, m, s);
 }
 
 cudaError_t launch_dof_pos(int64_t nfree, int d, const int32_t *free_node, const int32_t *free_out,

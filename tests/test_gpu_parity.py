@@ -23,7 +23,13 @@ from paper_2109_01158_b200 import problems  # noqa: E402
 
 J_TOL = 1e-10
 G_TOL = 1e-10
-FD_FACTOR = 64.0      # FD bound: 64 u * sum_patch vol*(|W+|+|W-|) / (2 eps)
+# FD bound: 64 u * sum_patch vol*(|W+| + |W-| + L+ + L-) / (2 eps), L the
+# magnitude of the terms W is assembled from (oracle numeric_gradient_direct);
+# and the GPU FD must be no farther from the exact gradient than the oracle's
+# own direct-sum FD (FD_DEV_FACTOR x; observed 0.5-0.7x: the rank-one update of
+# the perturbed invariants rounds less than recomputing F)
+FD_FACTOR = 64.0
+FD_DEV_FACTOR = 1.5
 
 GOLDEN_CASES = ["cfg1_lshape4_p3", "lshape4_p1.8", "bar1_nh", "rect32x16_nh", "beam8x4x4_nh"]
 
@@ -70,6 +76,8 @@ def _check_fd(g_gpu, v, om, op, omodel, b, eps, g_ref_fd, g_exact):
     # and within the reference FD's own deviation from the exact gradient
     ref_dev = np.abs(g_ref_fd - g_exact).max() / gmax
     assert np.abs(g_gpu - g_ref_fd).max() / gmax <= 2 * ref_dev + 1e-12
+    # no farther from the exact gradient than the oracle's own FD
+    assert np.abs(g_gpu - g_exact).max() <= FD_DEV_FACTOR * np.abs(gd - g_exact).max() + 1e-300
 
 
 # ---------------------------------------------------------------- preprocessing
@@ -272,6 +280,7 @@ def test_mid_size_vs_oracle(kind, size):
     ratio = np.abs(gn - gd) / (FD_FACTOR * scale + 1e-300)
     assert ratio.max() <= 1.0, (ratio.max(), int(ratio.argmax()), gn[ratio.argmax()],
                                 gd[ratio.argmax()], int((ratio > 1).sum()))
+    assert np.abs(gn - go).max() <= FD_DEV_FACTOR * np.abs(gd - go).max() + 1e-300
 
 
 def test_descent_loop_vs_reference(golden):
@@ -398,6 +407,7 @@ def test_tilings_vs_oracle(kind, tiling):
     ratio = np.abs(gn - gd) / (FD_FACTOR * scale + 1e-300)
     assert ratio.max() <= 1.0, (ratio.max(), int(ratio.argmax()), gn[ratio.argmax()],
                                 gd[ratio.argmax()], int((ratio > 1).sum()))
+    assert np.abs(gn - go).max() <= FD_DEV_FACTOR * np.abs(gd - go).max() + 1e-300
 
 
 @pytest.mark.parametrize("p", [3.0, 1.8])
@@ -482,3 +492,5 @@ def test_full_size_sampled_dofs(cfg):
     gd, scale = O.numeric_gradient_direct(v.cpu().numpy(), sub, P, omodel, b.cpu().numpy(), eps)
     pos = np.searchsorted(mt["dofs_minim"].cpu().numpy(), sub_dofs)
     assert (np.abs(gfd[pos] - gd) <= FD_FACTOR * scale + 1e-300).all()
+    # no farther from the (verified) exact gradient than the oracle's FD
+    assert np.abs(gfd[pos] - g[pos]).max() <= FD_DEV_FACTOR * np.abs(gd - g[pos]).max() + 1e-300
