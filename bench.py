@@ -43,6 +43,27 @@ def algorithmic_bytes(dim, d, ne, nn, nfree_dofs):
     return ne * per_elem + 8 * d * nn * 2 + 8 * nfree_dofs
 
 
+# FD gradient (gradients.py:84-121) FP64 roofline: algorithmic flops of the
+# reference formulation per perturbed state = row j of F recomputed from the
+# perturbed nodal values (dim entries x (dim+1 mul + dim add)) + det (dim 3:
+# 12 mul + 5 add; 2: 2 + 1) + |F|^2 (d*dim mul + d*dim-1 add) + W (8; log and
+# pow not counted) -> 3D Neo-Hookean 63, 2D 29; 2 d ||T|| states per launch
+def fd_flops_per_state(dim, d):
+    row = dim * ((dim + 1) + dim)
+    det = 17 if dim == 3 else 3
+    i1 = 2 * d * dim - 1
+    return row + det + i1 + 8
+
+
+def _fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["fp64_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "nominal B200 FP64 (no measurement found)"
+
+
 def _peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -137,17 +158,18 @@ def cpu_baseline_sample(nx=96, ny=48, nz=48, repeats=2):
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
     from oracle import femmin_oracle as O
     m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109)
-    P = O.build_patches(m)
+    RP = O.reference_patches(m, O.build_patches(m))
     best = float("inf")
     for _ in range(repeats):
         t0 = time.perf_counter()
         O.energy(v, m, model, b)
-        O.exact_gradient(v, m, P, model, b)
+        O.exact_gradient_femmin(v, m, RP, model, b)
         best = min(best, time.perf_counter() - t0)
     return {"value": m.ne / best / 1e6, "unit": "Melem/s",
             "cores": 1, "kind": "port",
-            "sample": f"beam {nx}x{ny}x{nz} ({m.ne} tets), femmin algorithm (oracle port: "
-                      f"energy + exact_gradient, numpy ufuncs single-threaded, OpenBLAS ddot "
+            "sample": f"beam {nx}x{ny}x{nz} ({m.ne} tets), femmin algorithm (oracle port doing "
+                      f"the reference's per-call work: energy + exact_gradient with patch-row "
+                      f"copies; numpy ufuncs single-threaded, OpenBLAS ddot "
                       f"with {os.environ.get('OMP_NUM_THREADS')} threads), best of {repeats}",
             "seconds_per_eval": best}
 
@@ -160,43 +182,51 @@ def _ref_worker(q, bar, nx, ny, nz, ix0, ix1, warmup, steps):
     port) on the x1-slab [ix0, ix1) of the beam, timed between barriers."""
     from oracle import femmin_oracle as O
     m, model, b, v = O.problem_beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1)
-    P = O.build_patches(m)
+    RP = O.reference_patches(m, O.build_patches(m))
     for _ in range(warmup):
         O.energy(v, m, model, b)
-        O.exact_gradient(v, m, P, model, b)
+        O.exact_gradient_femmin(v, m, RP, model, b)
     bar.wait()
     t0 = time.perf_counter()
     for _ in range(steps):
         O.energy(v, m, model, b)
-        O.exact_gradient(v, m, P, model, b)
+        O.exact_gradient_femmin(v, m, RP, model, b)
     q.put((m.ne, t0, time.perf_counter()))
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm (femmin's numpy energy +
-    exact_gradient, restated in oracle/ and pinned bit-exactly against it) on
-    ALL host cores of this box: one single-threaded process per core, each on
-    its own one-cube x1-slab of the same cfg4 beam (a bounded sample of the
-    workload; rank 0 only).  Throughput = elements x steps of all processes /
-    (last stop - first start) on the host's monotonic clock."""
+    exact_gradient, restated in oracle/ with the reference's per-call work and
+    pinned bit-exactly against it) on ALL host cores of this box: the cfg4
+    beam's 256 x1-slabs of cubes are split among one single-threaded process
+    per core (contiguous ranges; each slab's J and gradient partials are what
+    a rank of the multi-GPU split computes), all timed between one barrier and
+    the last stop (rank 0 only).  When the whole beam does not fit the host
+    memory or (K + W) steps of it would exceed ~2 minutes, every process runs a
+    shorter range and the line says which fraction of cfg4 one step covers."""
     if rank != 0:
         return
     import multiprocessing as mp
     nx, ny, nz = 256, 128, 128
     cores = len(os.sched_getaffinity(0))
-    # one process per core, bounded by host memory (about 0.5 GB per process)
     try:
         with open("/proc/meminfo") as fh:
             avail_gb = int(next(x for x in fh if x.startswith("MemAvailable")).split()[1]) / 2**20
     except Exception:
         avail_gb = 16.0
-    nproc = max(1, min(cores, args.ref_procs or cores, nx, int(avail_gb / 2 / 0.5)))
+    nproc = max(1, min(cores, args.ref_procs or cores, nx))
+    per = nx // nproc  # cube slabs per process for the whole beam
+    # ~0.14 s per single-threaded step of one 98,304-tet cube slab, ~0.35 GB each
+    per_time = max(1, int(120.0 / (0.14 * (args.steps + args.warmup))))
+    per_mem = max(1, int(0.7 * avail_gb / nproc / 0.35))
+    per = max(1, min(per, per_time, per_mem))
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
     ctx = mp.get_context("spawn")
     q, bar = ctx.Queue(), ctx.Barrier(nproc)
     procs = [ctx.Process(target=_ref_worker,
-                         args=(q, bar, nx, ny, nz, w, w + 1, args.warmup, args.steps))
+                         args=(q, bar, nx, ny, nz, w * (nx // nproc), w * (nx // nproc) + per,
+                               args.warmup, args.steps))
              for w in range(nproc)]
     for p in procs:
         p.start()
@@ -206,16 +236,20 @@ def run_reference(args, rank, world):
     ne = sum(r[0] for r in res)
     dt = (max(r[2] for r in res) - min(r[1] for r in res)) / args.steps
     value = ne / dt / 1e6
-    sample = (f"{nproc} single-threaded processes, each one 1-cube x1-slab of the cfg4 beam "
-              f"({ne // nproc} tets each, {ne} total = {ne / (6 * nx * ny * nz):.3f} of cfg4), "
-              f"femmin algorithm (oracle port of energy + exact_gradient)")
+    frac = ne / (6 * nx * ny * nz)
+    same = nproc * per == nx
+    sample = (f"{nproc} single-threaded processes, each {per} cube x1-slab(s) of the cfg4 beam "
+              f"({ne // nproc} tets each, {ne} total = {frac:.3f} of cfg4"
+              f"{' = the whole beam' if same else ''}), femmin algorithm (oracle port of energy "
+              f"+ exact_gradient doing the reference's per-call work)")
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "Melem/s", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 3D Neo-Hookean Kuhn beam {nx}x{ny}x{nz} on [0,2]x[0,1]^2, "
-                               f"sample of {ne} tets", "parallelism": f"host CPU x{nproc} processes"},
+        "config": {"workload": f"cfg4 3D Neo-Hookean Kuhn beam {nx}x{ny}x{nz} on [0,2]x[0,1]^2"
+                               + ("" if same else f", sample of {ne} tets"),
+                   "parallelism": f"host CPU x{nproc} processes", "same_config": same},
         "cpu_baseline": {"value": value, "unit": "Melem/s", "cores": nproc, "kind": "port",
                          "sample": sample, "host_cores": cores},
         "e2e": {"value": value, "unit": "Melem/s", "h2d_bytes_per_step": 0,
@@ -350,6 +384,40 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, kms = float(tt[0]), float(tt[1])
     dm.check()
+
+    # ---- FD gradient on the same problem: its own (FP64) roofline --------
+    fd_line = None
+    if world == 1:
+        gfd0 = torch.empty_like(g)
+        fd_eps = 1e-8 if dm.d > 1 else 1e-6
+        dm.numeric_gradient(v, model, b, fd_eps, g=gfd0)  # first call builds the item lists
+        dm.check()
+        nfd = 5
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(nfd)]
+        for a_, z_ in fev:  # materialise the CUDA events before the library records them
+            a_.record(stream)
+            z_.record(stream)
+        torch.cuda.synchronize()
+        for a_, z_ in fev:
+            dm.time_next(a_, z_)
+            dm.numeric_gradient(v, model, b, fd_eps, g=gfd0)
+        torch.cuda.synchronize()
+        dm.check()
+        fd_ms = statistics.median(a_.elapsed_time(z_) for a_, z_ in fev)
+        states = 2 * dm.d * dm.stats["node_entries_total"]
+        flop = states * fd_flops_per_state(dm.dim, dm.d)
+        fpk, fsrc = _fp64_peak()
+        fd_line = {"bound": "fp64", "kernel": "k_tile_fd", "kernel_ms": fd_ms,
+                   "eps": fd_eps, "perturbed_states": states,
+                   "flop_per_state": fd_flops_per_state(dm.dim, dm.d),
+                   "achieved": flop / (fd_ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
+                   "frac": flop / (fd_ms * 1e-3) / 1e12 / fpk, "peak_source": fsrc,
+                   "Melem_s": ne_total / fd_ms / 1e3,
+                   "W_evals_per_s": states / (fd_ms * 1e-3),
+                   "definition": "algorithmic flops of the reference formulation (F row "
+                                 "recompute, det, |F|^2, W; log/pow not counted) per perturbed "
+                                 "state x 2 d ||T|| states / median kernel time"}
 
     extras = {}
     if args.extras:
@@ -517,6 +585,44 @@ def main():
     # results of the streamed path equal the serial ones bit for bit
     stream_ok = bool(torch.equal(g_hosts[(e2e_steps - 1) % nbuf], g_host))
 
+    # ---- the reference-facing numpy drop-in: energy_and_gradient(v, mesh,
+    # patches, model, load) with host numpy in and out (pageable copies) ---
+    numpy_e2e = None
+    if world == 1 and args.config == "cfg4":
+        import numpy as np
+        import paper_2109_01158_b200 as fb
+        hm = fb.generate_beam_mesh_3d(nx, ny, nz)
+        hm = fb.mark_dirichlet(hm, fb.DirichletSpec(
+            [fb.DirichletRegion(where=lambda x: x[:, 0] < 1e-9)]), d=3)
+        # the CSR fields of Patches (patches.py:22-34; the drop-in reads only
+        # these), built on the GPU; the per-row copies are not materialised
+        from paper_2109_01158_b200.patches import build_patches_device
+        pfx, pel, psl = build_patches_device(torch.as_tensor(hm.elems2nodes).cuda(),
+                                             torch.as_tensor(hm.nodes_minim).cuda(), hm.nn, 4)
+        hp = fb.Patches(lengths=np.diff(pfx.cpu().numpy(), prepend=0), elems=pel.cpu().numpy(),
+                        volumes=None, elems2nodes=None, dphi=None, logical=None,
+                        prefix=pfx.cpu().numpy(), slot=psl.cpu().numpy())
+        del pfx, pel, psl
+        hload = fb.LinearLoad(b=b.cpu().numpy())
+        v_np = v.cpu().numpy().copy()
+        Jn, gn_ = fb.energy_and_gradient(v_np, hm, hp, model, hload)  # builds the context
+        ncall = 10
+        torch.cuda.synchronize()
+        tn0 = time.perf_counter()
+        for _ in range(ncall):
+            Jn, gn_ = fb.energy_and_gradient(v_np, hm, hp, model, hload)
+        tn = (time.perf_counter() - tn0) / ncall
+        same = bool(np.array_equal(gn_, g.cpu().numpy()))
+        numpy_e2e = {"value": ne_total / tn / 1e6, "unit": "Melem/s", "ms_per_call": tn * 1e3,
+                     "api": "paper_2109_01158_b200.energy_and_gradient(v_numpy, mesh, patches, "
+                            "model, load) -> (J, g_numpy): the femmin signature "
+                            "(assembly.py:94-106 + gradients.py:124-149), host numpy in and "
+                            "out (staged through pinned buffers inside the call), wall clock over 10 calls after the first "
+                            "(context build)",
+                     "h2d_bytes_per_call": int(v_np.nbytes), "d2h_bytes_per_call": int(gn_.nbytes + 24),
+                     "equals_device_path": same}
+        del hm, hp
+
     value = ne_total / (ms * 1e-3) / 1e6
     peak, peak_src = _peaks()
     alg = algorithmic_bytes(dm.dim, dm.d, dm.ne, dm.nn, dm.nfree_dofs)
@@ -569,7 +675,9 @@ def main():
                     "serial_value": ne_total / (e2e_serial_ms * 1e-3) / 1e6,
                     "serial_api": "DeviceMesh.exact_gradient(v, model, b, g, J) between "
                                   "blocking-order H2D / D2H copies on one stream",
-                    "streamed_equals_serial": stream_ok},
+                    "streamed_equals_serial": stream_ok,
+                    "numpy_drop_in": numpy_e2e},
+            "fd_roofline": fd_line,
             "gpu_launches": int(launches),
             "clocks": clk,
         }

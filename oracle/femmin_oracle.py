@@ -485,6 +485,50 @@ def exact_gradient(v, mesh: OMesh, P: OPatches, model, b=None):
     return g
 
 
+@dataclass(frozen=True)
+class RPatches(OPatches):
+    """patches.py:22-34 as the reference keeps them: the CSR plus the per-row
+    copies of volumes, connectivity, basis gradients and the one-hot owner
+    mask (patches.py:61-71).  Used where the reference's per-call WORK must be
+    reproduced (bench.py --impl reference), not only its results."""
+    volumes: np.ndarray = None
+    elems2nodes: np.ndarray = None
+    dphi: list = None
+    logical: np.ndarray = None
+
+
+def reference_patches(mesh: OMesh, P: OPatches) -> RPatches:
+    """The row copies of patches.py:61-71 on top of the CSR."""
+    e2n = mesh.elems2nodes[P.elems]
+    owners = mesh.nodes_minim[np.repeat(np.arange(P.lengths.size), P.lengths)]
+    return RPatches(P.lengths, P.elems, P.slot, P.prefix, mesh.volumes[P.elems], e2n,
+                    [g[P.elems] for g in mesh.dphi], e2n == owners[:, None])
+
+
+def exact_gradient_femmin(v, mesh: OMesh, RP: RPatches, model, b=None):
+    """gradients.py:124-149 doing the reference's per-call work step for step:
+    _patch_data (gradients.py:59-65: the element gather and F, the patch-row
+    gather v_patches the exact path computes and drops, the F copies to patch
+    rows), ddensity on the patch rows, dF_dv_table by the boolean owner mask
+    (gradients.py:54-56), the weighted blocks on the stored row volumes and
+    the cumsum segment sums (patches.py:80-83).  Same result as
+    exact_gradient bit for bit (tests/test_oracle_golden.py)."""
+    d, dim = model.d, mesh.dim
+    V = v.reshape(-1, d)
+    F_el = grad_field(mesh.dphi, [V[mesh.elems2nodes, j] for j in range(d)])
+    v_patches = [V[RP.elems2nodes, j] for j in range(d)]  # gradients.py:63 (unused here)
+    del v_patches
+    Fp = [[fm[RP.elems] for fm in fj] for fj in F_el]
+    dW = model.ddensity(Fp)
+    dF = [dm[RP.logical] for dm in RP.dphi]
+    blocks = np.concatenate([RP.volumes * sum(dW[j][m] * dF[m] for m in range(dim))
+                             for j in range(d)])
+    g = _rows_to_dofs(cumsum_segments(blocks, prefix_indices(RP, d)), mesh, d)
+    if b is not None:
+        g = g - b[mesh.dofs_minim]
+    return g
+
+
 def descent_loop(v, mesh: OMesh, P: OPatches, model, b, alpha, iters):
     """Config-5 first-order loop (BASELINE.json configs[4]): ``iters`` times
     J_i = energy(v) (assembly.py:94-106), g = exact_gradient(v)

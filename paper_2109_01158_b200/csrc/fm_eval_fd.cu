@@ -335,9 +335,9 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
     __syncthreads();
     // ---- nodes: ascending tile-element order
     if (my_node) {
+      for (int k = 0; k < cnt; ++k)  // the D component sums advance together
 #pragma unroll
-      for (int j = 0; j < D; ++j)
-        for (int k = 0; k < cnt; ++k) acc[j] += stg[j * ech + base + k];
+        for (int j = 0; j < D; ++j) acc[j] += stg[j * ech + base + k];
     }
     __syncthreads();
   }

@@ -337,3 +337,19 @@ def test_degenerate_decisions_match_reference(golden):
                 O.exact_gradient(v, m, p, model)
         else:
             O.exact_gradient(v, m, p, model)
+
+
+def test_femmin_work_variant_bit_exact(golden):
+    """The reference-arm variant (the reference's per-call work, patch-row
+    copies and boolean owner mask) gives the reference's exact gradient."""
+    for name in ("beam8x4x4_nh", "cfg1_lshape4_p3"):
+        g = golden(name)
+        m = _mesh_from_golden(g)
+        p = _patches_from_golden(g)
+        rp = O.reference_patches(m, p)
+        if "C1" in g:
+            model = O.Model("nh", O.LameParams(float(g["C1"]), float(g["D1"])), m.dim)
+        else:
+            model = O.Model("plap", O.PParams(float(g["p"])), 2)
+        np.testing.assert_array_equal(O.exact_gradient_femmin(g["v"], m, rp, model, g["b"]),
+                                      g["g_exact"])
