@@ -202,6 +202,26 @@ int fm_descent_step(fm_ctx *ctx, double *v, const double *g, double alpha, void 
 int fm_descent(fm_ctx *ctx, const fm_model *model, double *v, const double *b, double alpha,
                int iters, double *g, double *J_hist, void *stream);
 
+/* Device-resident Steihaug truncated CG of the trust-region minimizer
+ * (solver.py:77-113).  `state` is a device double[32]
+ * holding the CG scalars: [4] radius, [5] rtol, [13] h scale sqrt(eps)(1+|x|),
+ * [18] fixed FD step (0: h = scale / |d|) are set by the caller; [16] done,
+ * [17] hit the boundary, [15] iterations are read back.  `part` / `ticket`:
+ * device scratch of fm_cg_scratch_doubles() doubles / one zeroed unsigned.
+ * fm_cg_init: z = 0, r = -g, d = r.  fm_cg_embed: out[free dof q] = x[q] +
+ * sign * h * d[q] (x NULL: 0; use_h 0: h = 1), the full field of a
+ * Hessian-vector product.  fm_cg_iterate: one CG iteration after the product
+ * (Hd given, or gp / gm the gradients at x -/+ h d: Hd = (gp - gm) / (2 h)),
+ * all decisions on the device; no-op once done. */
+int fm_cg_scratch_doubles(void);
+int fm_cg_init(int64_t n, const double *g, double *r, double *d, double *z, double *state,
+               double *part, unsigned *ticket, void *stream);
+int fm_cg_embed(fm_ctx *ctx, const double *x, const double *d, const double *state, int use_h,
+                double sign, double *out, void *stream);
+int fm_cg_iterate(int64_t n, const double *gp, const double *gm, double *Hd, double *z,
+                  double *znew, double *r, double *d, double *state, double *part,
+                  unsigned *ticket, void *stream);
+
 /* Synchronises `stream`, returns the latched condition of the evaluations
  * since the last check and clears it: FM_OK or FM_INADMISSIBLE with
  * *index_host = offending dof (FD, gradients.py:77-81) or -1 (exact path). */

@@ -79,6 +79,10 @@ SIGNATURES = {
     "fm_hvp_exact": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, vp, vp]),
     "fm_descent_step": (C.c_int, [vp, vp, vp, dbl, vp]),
     "fm_descent": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, dbl, C.c_int, vp, vp, vp]),
+    "fm_cg_scratch_doubles": (C.c_int, []),
+    "fm_cg_init": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "fm_cg_embed": (C.c_int, [vp, vp, vp, vp, C.c_int, dbl, vp, vp]),
+    "fm_cg_iterate": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fm_ctx_check": (C.c_int, [vp, vp, P64]),
     "fm_hessian_pattern": (C.c_int, [i64, i64, C.c_int, C.c_int, vp, i64, vp, vp, vp, P64, vp]),
     "fm_color_d2": (C.c_int, [i64, vp, vp, vp, C.POINTER(i32), vp]),

@@ -32,6 +32,7 @@ UNITS = {
     "fm_eval_ref.cu": [],
     "fm_eval_fd.cu": [],
     "fm_hessian.cu": [],
+    "fm_cg.cu": [],
 }
 
 

@@ -59,6 +59,9 @@ class SolveOptions:
     # CG use the engine's exact Hessian-vector product (fm_hvp_exact, one
     # launch) instead of central differences of two gradients
     hvp: str = "fd"
+    # new: minimize_device runs the trust region's CG on the device
+    # (csrc/fm_cg.cu, one flag read per CG iteration); False: the host loop
+    device_cg: bool = True
 
     def __post_init__(self):
         if min(self.tol_g, self.tol_step, self.tol_f) <= 0:
@@ -134,7 +137,7 @@ def _steihaug(g, hvp, radius, rtol, maxiter):
     return z, False
 
 
-def _trust_region(fx, gx, x, f, opts, hx=None):
+def _trust_region(fx, gx, x, f, opts, hx=None, cg=None):
     g = gx(x)
     gn0 = _nrm_inf(g)
     gtol = opts.tol_g * max(1.0, gn0)
@@ -162,7 +165,10 @@ def _trust_region(fx, gx, x, f, opts, hx=None):
 
         g2 = _nrm(g)
         eta = min(0.5, math.sqrt(g2 / max(gn0, 1e-300)))
-        p, _ = _steihaug(g, hvp, radius, eta * g2, max_cg)
+        if cg is not None:  # device-resident CG: scalars and decisions on the GPU
+            p, _ = cg.solve(g, x, xnorm, radius, eta * g2, max_cg, opts.hvp_step)
+        else:
+            p, _ = _steihaug(g, hvp, radius, eta * g2, max_cg)
         pred = -(_dot(g, p) + 0.5 * _dot(p, hvp(p)))
         pn = _nrm(p)
         if pred <= 0.0 or pn == 0.0:
@@ -249,13 +255,86 @@ def _lbfgs(fx, gx, x, f, opts):
     return x, f, it, _nrm_inf(g), converged, status
 
 
-def _run(fx, gx, x0, opts, hx=None):
+def _run(fx, gx, x0, opts, hx=None, cg=None):
     f0 = fx(x0)
     if not math.isfinite(f0):
         raise InvalidStartError("initial field has non-finite energy")
     if opts.solver == "lbfgs":
         return _lbfgs(fx, gx, x0, f0, opts)
-    return _trust_region(fx, gx, x0, f0, opts, hx)
+    return _trust_region(fx, gx, x0, f0, opts, hx, cg)
+
+
+class _DeviceSteihaug:
+    """Steihaug truncated CG (solver.py:77-113) with every vector and scalar
+    on the device (csrc/fm_cg.cu): per iteration the Hessian-vector product
+    (two gradient launches around x -/+ h d, or one exact-HVP launch), three
+    fused vector kernels that also decide alpha / beta / boundary / tolerance,
+    and ONE 24-byte read of the done flags; the host never waits on a CG
+    scalar.  Same iterates as _steihaug up to the summation order of the dot
+    products."""
+
+    def __init__(self, dm, model, b, work, count, exact, embed):
+        from . import _lib
+        self.lib = _lib.load()
+        self._lib = _lib
+        self.dm, self.model, self.b, self.work, self.count = dm, model, b, work, count
+        self.exact, self.embed = exact, embed
+        n = dm.nfree_dofs
+        f64 = dict(dtype=torch.float64, device=work.device)
+        self.z, self.znew, self.r, self.d, self.Hd = (torch.empty(n, **f64) for _ in range(5))
+        self.gp, self.gm = torch.empty(n, **f64), torch.empty(n, **f64)
+        self.st = torch.zeros(32, **f64)
+        self.part = torch.empty(self.lib.fm_cg_scratch_doubles(), **f64)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=work.device)
+        self.flags = torch.empty(3, dtype=torch.float64, pin_memory=True)
+        self.pfull = torch.zeros_like(work) if exact else None
+        self.n = n
+
+    def _p(self, t):
+        return None if t is None else t.data_ptr()
+
+    def solve(self, g, x, xnorm, radius, rtol, maxiter, hvp_step=None):
+        from ._device import stream_ptr
+        lib, P, s = self.lib, self._p, stream_ptr()
+        init = torch.zeros(32, dtype=torch.float64)
+        init[4], init[5] = radius, rtol
+        init[13] = _SQRT_EPS * (1.0 + xnorm)
+        init[18] = hvp_step or 0.0
+        self.st.copy_(init)
+        chk = self._lib.check
+        chk(lib.fm_cg_init(self.n, P(g), P(self.r), P(self.d), P(self.z), P(self.st),
+                           P(self.part), P(self.ticket), s))
+        if not self._done():
+            work = self.work
+            if self.exact:
+                xf = self.embed(x)  # the field is fixed during one CG solve
+            for _ in range(maxiter):
+                if self.exact:
+                    chk(lib.fm_cg_embed(self.dm._h, None, P(self.d), P(self.st), 0, 1.0,
+                                        P(self.pfull), s))
+                    self.dm.hvp(xf, self.pfull, self.model, out=self.Hd)
+                    self.count["h"] = self.count.get("h", 0) + 1
+                    gp = gm = None
+                else:
+                    for sign, out in ((1.0, self.gp), (-1.0, self.gm)):
+                        chk(lib.fm_cg_embed(self.dm._h, P(x), P(self.d), P(self.st), 1, sign,
+                                            P(work), s))
+                        self.dm.exact_gradient(work, self.model, self.b, g=out)
+                    self.count["g"] += 2
+                    gp, gm = self.gp, self.gm
+                chk(lib.fm_cg_iterate(self.n, P(gp), P(gm), P(self.Hd), P(self.z),
+                                      P(self.znew), P(self.r), P(self.d), P(self.st),
+                                      P(self.part), P(self.ticket), s))
+                if self._done():
+                    break
+        return self.z.clone(), bool(self.flags[1] != 0.0)
+
+    def _done(self) -> bool:
+        # one small read per iteration; dm.check() synchronises the stream and
+        # raises for an inadmissible gradient / product (models.py:107-110)
+        self.flags.copy_(self.st[16:19], non_blocking=True)
+        self.dm.check()
+        return bool(self.flags[0] != 0.0)
 
 
 def minimize(J, g, v0, dofs_minim, opts: SolveOptions | None = None) -> MinimizeResult:
@@ -323,8 +402,11 @@ def minimize_device(dm, model, b, v0: torch.Tensor, dofs_minim: torch.Tensor,
             count["h"] = count.get("h", 0) + 1
             return dm.hvp(embed(x), pfull.index_copy_(0, dofs, p), model)
 
+    cg = None
+    if opts.solver == "tr" and opts.device_cg:
+        cg = _DeviceSteihaug(dm, model, b, work, count, opts.hvp == "exact", embed)
     t0 = time.perf_counter()
-    x, f, it, gn, conv, status = _run(fx, gx, template.index_select(0, dofs), opts, hx)
+    x, f, it, gn, conv, status = _run(fx, gx, template.index_select(0, dofs), opts, hx, cg)
     torch.cuda.synchronize()
     res = MinimizeResult(u=template.index_copy(0, dofs, x), J_u=f, iters=it, grad_norm=gn,
                          time=time.perf_counter() - t0, converged=conv, status=status,

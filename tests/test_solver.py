@@ -159,3 +159,30 @@ def test_minimize_device_beam_decreases_energy(hvp):
     g = pr.dm.exact_gradient(res.u, pr.model, pr.b)
     g0 = pr.dm.exact_gradient(v0, pr.model, pr.b)
     assert float(g.abs().max()) <= 1e-7 * max(1.0, float(g0.abs().max())) * 1.0001
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hvp", ["fd", "exact"])
+def test_device_cg_matches_host_cg(golden, hvp):
+    """The device-resident CG (csrc/fm_cg.cu) takes the host loop's iterates:
+    same outer iterations, status and gradient-call count, J to 1e-12."""
+    import paper_2109_01158_b200 as fb
+    from paper_2109_01158_b200.solver import minimize_device
+    g = golden("lshape1_plap")
+    ref = golden("minimize_lshape1")
+    m = fb.Mesh(dim=2, level=-1, nodes2coord=g["coords"], elems2nodes=g["conn"],
+                volumes=g["volumes"], dphi=list(g["dphi"]), d=1,
+                nodes_dirichlet=g["nodes_dirichlet"], nodes_minim=g["nodes_minim"],
+                dofs_dirichlet=g["dofs_dirichlet"], dofs_minim=g["dofs_minim"],
+                dofs_minim_local=g["dofs_minim_local"])
+    dm = fb.context_for(m)
+    model = fb.PLaplacian(fb.PLaplaceParams(p=3.0), dim=2)
+    b = torch.from_numpy(ref["b"]).cuda()
+    v0 = torch.zeros(m.nn, dtype=torch.float64, device="cuda")
+    dofs = torch.from_numpy(np.asarray(m.dofs_minim)).cuda()
+    a = minimize_device(dm, model, b, v0, dofs, SolveOptions(hvp=hvp, device_cg=True))
+    h = minimize_device(dm, model, b, v0, dofs, SolveOptions(hvp=hvp, device_cg=False))
+    assert a.converged and h.converged and a.status == h.status
+    assert a.iters == h.iters and a.n_grad == h.n_grad
+    assert abs(a.J_u - h.J_u) <= 1e-12 * abs(h.J_u)
+    assert float((a.u - h.u).abs().max()) <= 1e-9
