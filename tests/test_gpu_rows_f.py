@@ -179,3 +179,22 @@ def test_exact_hvp_matches_reference_fd_hessian(golden):
                    pr.model)
     ref = Href @ x
     assert np.abs(hp.cpu().numpy() - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_reports_bench1_3_on_gpu(tmp_path):
+    """The reference's hot-path benchmarks 1-3 as CSV reports on the engine
+    (reports.py; bench.py:208-296): counts of test_reports_io.py, the twisted
+    bar's J at level 1 (test_acceptance.py:66) and exact-vs-FD agreement."""
+    from paper_2109_01158_b200 import reports
+    r1 = reports.bench1([1])
+    c = {k: i for i, k in enumerate(r1.columns)}
+    row = r1.rows[0]
+    assert (row[c["nodes"]], row[c["elements"]], row[c["free_dofs"]],
+            row[c["patch_rows"]]) == (729, 1920, 2133, 7584)
+    r2 = reports.bench2([1], repeats=1)
+    assert abs(r2.column("J_grad")[0] - 12.6623) < 5e-5
+    r3 = reports.bench3([1], repeats=1)
+    assert r3.column("rel_agreement")[0] < 1e-4
+    path = tmp_path / "b3.csv"
+    r3.to_csv(path)
+    assert reports.BenchmarkReport.from_csv("bench3", path).rows == r3.rows

@@ -4,6 +4,7 @@ written by the reference's own writer (tests/golden/make_golden.py case_vtk)."""
 import os
 
 import numpy as np
+import pytest
 
 from paper_2109_01158_b200 import vtk_io
 
@@ -37,3 +38,43 @@ def test_vtk_bytes_3d(tmp_path, golden):
     lines = _read(out).decode().splitlines()
     i = lines.index(f"CELL_TYPES {g['conn'].shape[0]}")
     assert set(lines[i + 1:i + 1 + g["conn"].shape[0]]) == {"10"}
+
+
+def test_report_csv_contract(tmp_path):
+    """BenchmarkReport (reference bench.py:44-98): row-length check, exact
+    float round trip through the CSV text and the file, table formatting."""
+    from paper_2109_01158_b200.reports import BenchmarkReport
+    rep = BenchmarkReport(benchmark="demo", columns=["level", "J", "name"])
+    with pytest.raises(ValueError):
+        rep.add_row(1)
+    rep.add_row(1, 0.1 + 0.2, "run-a")
+    rep.add_row(2, -8.16254321e7, "run-b")
+    back = BenchmarkReport.from_csv_string("demo", rep.to_csv_string())
+    assert back.columns == rep.columns and back.rows == rep.rows
+    path = tmp_path / "r.csv"
+    rep.to_csv(path)
+    assert BenchmarkReport.from_csv("demo", path).rows == rep.rows
+    assert rep.column("J") == [0.1 + 0.2, -8.16254321e7]
+    table = rep.format_table()
+    assert "level" in table and "run-b" in table and "0.3" in table
+
+
+def test_report_csv_matches_reference_writer():
+    """Same bytes as the reference's writer for the same rows."""
+    import os
+    import sys
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present")
+    sys.path.insert(0, ref)
+    try:
+        from femmin.bench import BenchmarkReport as RefReport
+    finally:
+        sys.path.remove(ref)
+    from paper_2109_01158_b200.reports import BenchmarkReport
+    rows = [(1, 0.1 + 0.2, "a"), (3, 6.425476e0, "b,c"), (7, float("inf"), "x")]
+    a, b = BenchmarkReport("t", ["l", "J", "s"]), RefReport("t", ["l", "J", "s"])
+    for r in rows:
+        a.add_row(*r)
+        b.add_row(*r)
+    assert a.to_csv_string() == b.to_csv_string()
