@@ -378,6 +378,18 @@ __global__ void k_cross_items(int64_t ntn, const int32_t *tile_node_rank,
   }
 }
 
+// finishing-pass descriptors of the tile nodes with cross entries (one 16-B
+// load per node instead of four dependent ones)
+__global__ void k_xdesc(int64_t n, const int32_t *xnodes, const int32_t *xbase,
+                        const int32_t *outw, const uint8_t *fmask, int4 *xdesc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int k = xnodes[r];
+    const int lo = xbase[k], cnt = xbase[k + 1] - lo;
+    xdesc[r] = make_int4(k, lo, cnt | ((int)fmask[k] << 16), outw[k]);
+  }
+}
+
 __global__ void k_nonzero_flags(int64_t n, const int32_t *x, int32_t *flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1494,6 +1506,11 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
       CK(dmalloc(&c->xnodes, std::max(hn, 1), &B));
       k_scatter_flagged<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, fl, ps, c->xnodes);
       CK(cudaGetLastError());
+      CK(dmalloc(&c->xdesc, std::max(hn, 1), &B));
+      k_xdesc<<<grid_for(std::max(hn, 1), 256), 256, 0, s>>>(hn, c->xnodes, c->node_xbase,
+                                                            c->node_outw, c->node_fmask,
+                                                            c->xdesc);
+      CK(cudaGetLastError());
     }
     CK(dmalloc(&c->node_clo, nfree + 8, &B));
     k_node_clo<<<grid_for(nfree, 256), 256, 0, s>>>(nfree, s_tnr.as<int32_t>(), s_tor.as<int32_t>(),
@@ -1554,12 +1571,15 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
   }
 
   // build-only tables: the kernels read the chunk entry blocks instead of the
-  // node-major entry lists, and no kernel reads the owned-slot flags
+  // node-major entry lists, no kernel reads the owned-slot flags, and the
+  // finishing pass reads the packed xdesc instead of the per-node arrays
   CK(cudaStreamSynchronize(s));
-  if (c->node_entries) CK(cudaFree(c->node_entries));
-  if (c->flags) CK(cudaFree(c->flags));
-  c->node_entries = nullptr;
-  c->flags = nullptr;
+  for (void **p : {(void **)&c->node_entries, (void **)&c->flags, (void **)&c->node_xbase,
+                   (void **)&c->node_xn, (void **)&c->node_outw, (void **)&c->node_fmask,
+                   (void **)&c->xnodes}) {
+    if (*p) CK(cudaFree(*p));
+    *p = nullptr;
+  }
 
   memlog("scratch", s);
   // scratch ------------------------------------------------------------------
@@ -1642,7 +1662,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw, c->node_fmask,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
-                  c->xnodes,    c->dof_pos,   c->fd_items};
+                  c->xnodes,    c->dof_pos,   c->fd_items,  c->xdesc};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1706,9 +1726,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
     // free dof are added here)
     JFinal jf{c->jpart, c->dotpart, ta.n_tiles_all > 0 ? grid : 0, c->fixed_nodes,
               c->n_fixed_nodes, b, v, c->fpart, c->ticket, wj ? J_out : nullptr};
-    FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->n_xnodes : 0, c->xnodes,
-                                c->node_xbase, c->node_outw, c->node_fmask, c->xpos, c->xbuf, c->partial, g,
-                                jf, s));
+    FM_CUDA(launch_finish_cross(c->d, c->n_cross > 0 ? c->n_xnodes : 0, c->xdesc, c->xpos,
+                                c->xbuf, c->partial, g, jf, s));
     c->launches++;
   }
   return FM_OK;
@@ -1740,8 +1759,8 @@ int fm_hvp_exact(fm_ctx *c, const fm_model *model, const double *v, const double
   if (c->n_cross > 0) {
     JFinal jf{c->jpart, c->dotpart, 0, c->fixed_nodes, 0, nullptr, v, c->fpart, c->ticket,
               nullptr};
-    FM_CUDA(launch_finish_cross(c->d, c->n_xnodes, c->xnodes, c->node_xbase, c->node_outw,
-                                c->node_fmask, c->xpos, c->xbuf, c->partial, hp, jf, s));
+    FM_CUDA(launch_finish_cross(c->d, c->n_xnodes, c->xdesc, c->xpos, c->xbuf, c->partial, hp,
+                                jf, s));
     c->launches++;
   }
   return FM_OK;

@@ -292,7 +292,9 @@ struct fm_ctx {
   uint16_t *xkey = nullptr;                        // cross-tile exchange (see TileArgs)
   int32_t *xpos = nullptr, *xchunk = nullptr;
   int32_t *node_xbase = nullptr, *node_xn = nullptr;  // per tile node: its cross entries
-  int32_t *xnodes = nullptr;  // tile nodes with cross entries (finishing pass)
+  int32_t *xnodes = nullptr;  // tile nodes with cross entries (build only)
+  int4 *xdesc = nullptr;      // finishing pass, per tile node with cross entries:
+                              // {tile node, first exchange slot, count | free mask << 16, out}
   int64_t n_xnodes = 0;
   double *xbuf = nullptr, *partial = nullptr;
   int32_t *node_outw = nullptr;  // per tile node: output offset (finishing pass)

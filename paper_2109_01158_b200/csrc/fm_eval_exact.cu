@@ -682,10 +682,7 @@ __global__ void __launch_bounds__(CT, MINB)
 // does not depend on which block is last; the ticket is reset for the next call.
 template <int D>
 __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
-                                                      const int32_t *__restrict__ nodes,
-                                                      const int32_t *__restrict__ xbase,
-                                                      const int32_t *__restrict__ outw,
-                                                      const uint8_t *__restrict__ fmask,
+                                                      const int4 *__restrict__ xdesc,
                                                       const int32_t *__restrict__ xinv,
                                                       const double *__restrict__ xbuf,
                                                       const double *__restrict__ partial,
@@ -696,13 +693,10 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / D;
     const int j = (int)(i - r * D);
-    const int64_t k = __ldg(nodes + r);  // a tile node with cross entries
-    const int lo = __ldg(xbase + k), hi = __ldg(xbase + k + 1);
-    if (hi == lo) continue;
-    const int w = __ldg(outw + k);
-    const int mask = __ldg(fmask + k);
+    const int4 xd = __ldg(xdesc + r);  // {tile node, first slot, count | mask << 16, out}
+    const int mask = xd.z >> 16, lo = xd.y, hi = lo + (xd.z & 0xffff);
     if (!(mask & (1 << j))) continue;
-    double sum = partial[k * D + j];
+    double sum = partial[(int64_t)xd.x * D + j];
     // four entries per step: their slot loads, then their value loads, are
     // issued back to back; the sum stays sequential in entry order
     int p = lo;
@@ -714,7 +708,7 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
       sum = (((sum + x0) + x1) + x2) + x3;
     }
     for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
-    g[w + __popc(mask & ((1 << j) - 1))] = sum;
+    g[xd.w + __popc(mask & ((1 << j) - 1))] = sum;
   }
   if (!jf.out) return;
   __shared__ double red[32];
@@ -758,18 +752,16 @@ int finish_cross_grid(int d, int64_t ntn) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, finish_max_blocks()));
 }
 
-cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,
-                                const int32_t *outw, const uint8_t *fmask, const int32_t *xinv,
-                                const double *xbuf,
-                                const double *partial, double *g, const JFinal &jf,
-                                cudaStream_t s) {
+cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
+                                const double *xbuf, const double *partial, double *g,
+                                const JFinal &jf, cudaStream_t s) {
   const int grid = finish_cross_grid(d, ntn);
   if (d == 3)
-    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
+    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
   else if (d == 2)
-    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
+    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
   else
-    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, nodes, xbase, outw, fmask, xinv, xbuf, partial, g, jf);
+    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
   return cudaGetLastError();
 }
 

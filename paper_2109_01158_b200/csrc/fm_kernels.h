@@ -38,10 +38,9 @@ struct JFinal {
 // finishing-pass grid cap (32 blocks per SM); sizes the per-block b.v partials
 inline int finish_max_blocks() { return sm_count() * 32; }
 int finish_cross_grid(int d, int64_t ntn);
-cudaError_t launch_finish_cross(int d, int64_t ntn, const int32_t *nodes, const int32_t *xbase,
-                                const int32_t *outw, const uint8_t *fmask,
-                                const int32_t *xinv, const double *xbuf, const double *partial,
-                                double *g, const JFinal &jf, cudaStream_t s);
+cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
+                                const double *xbuf, const double *partial, double *g,
+                                const JFinal &jf, cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
                        int dn = 0);
 

@@ -41,20 +41,27 @@ def full(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
-    h, u, v = r[0], r[1], r[2]
-    print(f"kernel: {v[h.index('Kernel Name')][:120]}")
-    print("| metric | value | unit |")
-    print("|---|---|---|")
-    for k in KEYS:
-        if k in h:
-            i = h.index(k)
-            print(f"| {k} | {v[i]} | {u[i]} |")
-    st = [(n, float(v[i])) for i, n in enumerate(h)
-          if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio")
-          and v[i] not in ("", "n/a")]
-    print("\nwarp stall reasons (per issued instruction):")
-    for n, x in sorted(st, key=lambda t: -t[1])[:8]:
-        print(f"- {n.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}: {x:.2f}")
+    h, u = r[0], r[1]
+    seen = set()
+    for v in r[2:]:  # the first captured launch of every kernel
+        name = v[h.index('Kernel Name')]
+        if name in seen:
+            continue
+        seen.add(name)
+        print(f"kernel: {name[:120]}")
+        print("| metric | value | unit |")
+        print("|---|---|---|")
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                print(f"| {k} | {v[i]} | {u[i]} |")
+        st = [(n, float(v[i])) for i, n in enumerate(h)
+              if n.startswith("smsp__average_warps_issue_stalled")
+              and n.endswith("per_issue_active.ratio") and v[i] not in ("", "n/a")]
+        print("\nwarp stall reasons (per issued instruction):")
+        for n, x in sorted(st, key=lambda t: -t[1])[:8]:
+            print(f"- {n.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')}: {x:.2f}")
+        print()
 
 
 if __name__ == "__main__":
