@@ -222,6 +222,23 @@ int fm_cg_iterate(int64_t n, const double *gp, const double *gm, double *Hd, dou
                   double *znew, double *r, double *d, double *state, double *part,
                   unsigned *ticket, void *stream);
 
+/* x1-slab exchange of the multi-GPU split (one process per GPU).
+ * NCCL is resolved at run time (the process's already-loaded libnccl.so.2
+ * first).  fm_comm_unique_id: rank 0's 128-byte ncclUniqueId, to be
+ * broadcast by the caller.  fm_slab_create: the communicator (current device)
+ * and the device positions in g of the interface-plane dofs shared with the
+ * left / right neighbour (n_plane each; NULL where there is no neighbour).
+ * fm_slab_reduce (stream-ordered): g += the neighbours' partials at the plane
+ * dofs and J (device double[3]) = the sum over ranks of every rank's J
+ * partials in rank order; one pack kernel, one grouped NCCL launch (planes
+ * both ways + J all-gather), one unpack kernel.  Either g or J may be NULL. */
+typedef struct fm_slab fm_slab;
+int fm_comm_unique_id(void *id_host);
+int fm_slab_create(const void *id_host, int rank, int world, int64_t n_plane,
+                   const int64_t *left_pos, const int64_t *right_pos, fm_slab **out);
+int fm_slab_reduce(fm_slab *x, double *g, double *J, void *stream);
+int fm_slab_destroy(fm_slab *x);
+
 /* Synchronises `stream`, returns the latched condition of the evaluations
  * since the last check and clears it: FM_OK or FM_INADMISSIBLE with
  * *index_host = offending dof (FD, gradients.py:77-81) or -1 (exact path). */

@@ -79,6 +79,10 @@ SIGNATURES = {
     "fm_hvp_exact": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, vp, vp]),
     "fm_descent_step": (C.c_int, [vp, vp, vp, dbl, vp]),
     "fm_descent": (C.c_int, [vp, C.POINTER(FmModel), vp, vp, dbl, C.c_int, vp, vp, vp]),
+    "fm_comm_unique_id": (C.c_int, [vp]),
+    "fm_slab_create": (C.c_int, [vp, C.c_int, C.c_int, i64, vp, vp, vp]),
+    "fm_slab_reduce": (C.c_int, [vp, vp, vp, vp]),
+    "fm_slab_destroy": (C.c_int, [vp]),
     "fm_cg_scratch_doubles": (C.c_int, []),
     "fm_cg_init": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fm_cg_embed": (C.c_int, [vp, vp, vp, vp, C.c_int, dbl, vp, vp]),

@@ -33,6 +33,7 @@ UNITS = {
     "fm_eval_fd.cu": [],
     "fm_hessian.cu": [],
     "fm_cg.cu": [],
+    "fm_slab.cu": [],
 }
 
 
@@ -72,7 +73,7 @@ def _build(lib: str, objdir: str, defines: list[str], force: bool, verbose: bool
     log = [l for _, l in res if l is not None]
     if (force or log or not os.path.exists(lib)
             or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
-        cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

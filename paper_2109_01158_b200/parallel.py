@@ -19,6 +19,9 @@ The descent update of config 5 then needs no further exchange.
 
 from __future__ import annotations
 
+import os
+import weakref
+
 import torch
 import torch.distributed as dist
 
@@ -43,6 +46,41 @@ def plane_dof_positions(nodes: torch.Tensor, d: int, dofs_minim: torch.Tensor) -
     return pos
 
 
+class NativeSlab:
+    """The exchange through the C ABI (include/femmin_b200.h fm_slab_*): its
+    own NCCL communicator (unique id from rank 0, broadcast over the torch
+    process group), the plane positions uploaded once."""
+
+    def __init__(self, left, right, n_plane, rank, world, group=None):
+        import ctypes as C
+
+        from . import _lib
+        from ._device import ptr
+        self._lib = _lib
+        self.lib = _lib.load()
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _lib.check(self.lib.fm_comm_unique_id(uid), "fm_comm_unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(box[0])
+        self.left = left.contiguous() if left is not None else None
+        self.right = right.contiguous() if right is not None else None
+        for plane in (self.left, self.right):
+            if plane is not None and plane.numel() != n_plane:
+                raise ValueError("interface plane size mismatch")
+        h = C.c_void_p()
+        _lib.check(self.lib.fm_slab_create(uid, rank, world, int(n_plane), ptr(self.left),
+                                           ptr(self.right), C.byref(h)), "fm_slab_create")
+        self._h = h
+        self._fin = weakref.finalize(self, self.lib.fm_slab_destroy, h)
+
+    def reduce(self, g, J):
+        from ._device import ptr, stream_ptr
+        self._lib.check(self.lib.fm_slab_reduce(self._h, ptr(g), ptr(J), stream_ptr()),
+                        "fm_slab_reduce")
+
+
 class SlabExchange:
     """Reduction of slab-local (J, grad J) partials across the x1-slab ranks."""
 
@@ -65,7 +103,15 @@ class SlabExchange:
         self.jall = torch.empty((world, 3), dtype=torch.float64, device=dev)
         # NCCL moves device buffers; a gloo group (CPU tests, or the one-GPU
         # functional smoke test of the multi-rank bench) needs host copies
-        self.host = dev.type == "cuda" and dist.get_backend(group) != "nccl"
+        backend = dist.get_backend(group)
+        self.host = dev.type == "cuda" and backend != "nccl"
+        # with NCCL the exchange runs in the C ABI (fm_slab_reduce: pack, one
+        # grouped NCCL launch for both planes and the J all-gather, unpack);
+        # FM_SLAB_TORCH=1 keeps the torch.distributed path below
+        self.native = None
+        if (dev.type == "cuda" and backend == "nccl"
+                and os.environ.get("FM_SLAB_TORCH", "0") != "1"):
+            self.native = NativeSlab(self.left, self.right, n, rank, world, group)
 
     @classmethod
     def from_problem(cls, pr, rank, world, group=None):
@@ -77,6 +123,9 @@ class SlabExchange:
         """In place: g += neighbours' interface partials; J <- global J
         (the all-gathered per-rank partials summed by one fixed reduction, the
         same on every rank).  Either may be None."""
+        if self.native is not None:
+            self.native.reduce(g, J)
+            return g, J
         if g is not None and self.pos is not None:
             torch.index_select(g, 0, self.pos, out=self.send)
             send = self.send.cpu() if self.host else self.send
