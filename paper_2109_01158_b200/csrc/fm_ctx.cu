@@ -1706,7 +1706,8 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   FM_NVTX("fm_grad_exact");
   int st = check_model(c, model);
   if (st) return st;
-  FM_ARG(v && g, "null field or output");
+  // an empty gradient (no free dof) may come as a null pointer
+  FM_ARG(v && (g || c->nfree_dofs == 0), "null field or output");
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
   const bool wj = J_out != nullptr;
@@ -1738,7 +1739,7 @@ int fm_hvp_exact(fm_ctx *c, const fm_model *model, const double *v, const double
   FM_NVTX("fm_hvp_exact");
   int st = check_model(c, model);
   if (st) return st;
-  FM_ARG(v && p && hp, "null field, direction or output");
+  FM_ARG(v && p && (hp || c->nfree_dofs == 0), "null field, direction or output");
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
   TileArgs ta = c->tile_args();
@@ -1771,7 +1772,8 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   FM_NVTX("fm_grad_fd");
   int st = check_model(c, model);
   if (st) return st;
-  FM_ARG(v && g, "null field or output");
+  // an empty gradient (no free dof) may come as a null pointer
+  FM_ARG(v && (g || c->nfree_dofs == 0), "null field or output");
   FM_ARG(eps > 0.0, "central-difference step must be positive");
   if (c->n_tiles == 0) return FM_OK;
   cudaStream_t s = as_stream(stream);
@@ -1799,7 +1801,7 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
 
 int fm_descent_step(fm_ctx *c, double *v, const double *g, double alpha, void *stream) {
   FM_NVTX("fm_descent_step");
-  FM_ARG(c && v && g, "null argument");
+  FM_ARG(c && v && (g || c->nfree_dofs == 0), "null argument");
   FM_CUDA(launch_descent(c->nfree_dofs, c->dof_pos, g, alpha, v, as_stream(stream)));
   c->launches++;
   return FM_OK;
@@ -1808,7 +1810,7 @@ int fm_descent_step(fm_ctx *c, double *v, const double *g, double alpha, void *s
 int fm_descent(fm_ctx *c, const fm_model *model, double *v, const double *b, double alpha,
                int iters, double *g, double *J_hist, void *stream) {
   FM_NVTX("fm_descent");
-  FM_ARG(c && v && g, "null argument");
+  FM_ARG(c && v && (g || c->nfree_dofs == 0), "null argument");
   FM_ARG(iters >= 0, "negative iteration count");
   // every iteration: (J,) grad J at v, then v_free -= alpha * g; the kernels
   // of consecutive iterations are ordered on the stream, nothing syncs
