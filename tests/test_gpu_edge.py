@@ -132,3 +132,26 @@ def test_flipped_element():
     with pytest.raises(fb.DegenerateElementError, match="element 1 has nonpositive measure"):
         fb.compute_p1_gradients(coords, conn)
     assert issubclass(fb.DegenerateElementError, ValueError)
+
+
+@pytest.mark.parametrize("scale", [1e-4, 1e5])
+def test_scaled_coordinates(scale):
+    """Meshes far from unit size (the tile boxes derive from the mean element
+    measure; det F is dimensionless): J and the gradients follow the oracle."""
+    om = O.beam_mesh(10, 5, 5, 0.0, 2.0 * scale, 0.0, scale, 0.0, scale)
+    om = O.mark_dirichlet(om, O.fixed_mask(om, [(lambda x: x[:, 0] < 1e-9 * scale, None)], 3), 3)
+    model, omodel = _nh(3)
+    v = O.field_nh(om, 23, 1e-2 * 0.2 * scale)
+    b = O.load_vector(om, (0.0, 0.0, -2.5e7), 3)
+    _check_all(om, v, b, model, omodel, eps=1e-8 * scale)
+
+
+def test_componentwise_dirichlet_2d():
+    """2D Neo-Hookean with x fixed on the left edge and y on the bottom edge."""
+    om = O.rect_mesh(16, 8)
+    om = O.mark_dirichlet(om, O.fixed_mask(om, [(lambda x: x[:, 0] < 1e-9, [0]),
+                                                (lambda x: x[:, 1] < 1e-9, [1])], 2), 2)
+    model, omodel = _nh(2)
+    v = O.field_nh(om, 29, 1e-2 * 2.0 / 16)
+    b = O.load_vector(om, (0.0, -3.5e7), 2)
+    _check_all(om, v, b, model, omodel)
