@@ -49,3 +49,45 @@ def test_native_slab_single_rank():
         assert torch.equal(J, J0)
     finally:
         dist.destroy_process_group()
+
+
+def test_step_graph_capture():
+    """The fused evaluation and the C-ABI exchange are capture-safe: one CUDA
+    graph of (tile kernel, finishing pass, pack, grouped NCCL, unpack) replays
+    to the eager results bit for bit (what bench.py uses for N > 1 ranks)."""
+    from paper_2109_01158_b200 import problems
+    from paper_2109_01158_b200.parallel import SlabExchange
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        pr = problems.beam(12, 6, 6, seed=4)
+        ex = SlabExchange.from_problem(pr, 0, 1)
+        g = torch.empty(pr.dm.nfree_dofs, dtype=torch.float64, device="cuda")
+        J = torch.empty(3, dtype=torch.float64, device="cuda")
+
+        def step():
+            pr.dm.exact_gradient(pr.v, pr.model, pr.b, g=g, J=J)
+            ex.reduce(g, J)
+
+        step()
+        torch.cuda.synchronize()
+        g_ref, J_ref = g.clone(), J.clone()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()  # warm-up on the capture stream
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(3):
+            g.zero_()
+            J.zero_()
+            graph.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(g, g_ref) and torch.equal(J, J_ref)
+        pr.dm.check()
+    finally:
+        dist.destroy_process_group()
