@@ -203,19 +203,34 @@ int fm_slab_reduce(fm_slab *x, double *g, double *J, void *stream) {
     k_slab_pack<<<grid_for(n, 256), 256, 0, s>>>(n, x->pos, g, x->send);
     FM_CHECK_LAUNCH();
   }
-  // one grouped NCCL launch: both planes each way and the J all-gather
+  // one grouped NCCL launch: both planes each way and the J all-gather (the
+  // group is always closed, also when a call inside it fails)
   FM_NCCL(api.groupStart());
+  ncclResult_t r = ncclSuccess;
+  const char *what = "";
   int64_t o = 0;
-  for (int side = 0; side < 2 && n; ++side) {
+  for (int side = 0; side < 2 && n && r == ncclSuccess; ++side) {
     const bool has = side == 0 ? x->has_left : x->has_right;
     if (!has) continue;
     const int peer = side == 0 ? x->rank - 1 : x->rank + 1;
-    FM_NCCL(api.send(x->send + o, (size_t)x->n_plane, ncclFloat64, peer, x->comm, s));
-    FM_NCCL(api.recv(x->recv + o, (size_t)x->n_plane, ncclFloat64, peer, x->comm, s));
+    r = api.send(x->send + o, (size_t)x->n_plane, ncclFloat64, peer, x->comm, s);
+    what = "ncclSend";
+    if (r == ncclSuccess) {
+      r = api.recv(x->recv + o, (size_t)x->n_plane, ncclFloat64, peer, x->comm, s);
+      what = "ncclRecv";
+    }
     o += x->n_plane;
   }
-  if (J) FM_NCCL(api.allGather(J, x->jall, 3, ncclFloat64, x->comm, s));
-  FM_NCCL(api.groupEnd());
+  if (J && r == ncclSuccess) {
+    r = api.allGather(J, x->jall, 3, ncclFloat64, x->comm, s);
+    what = "ncclAllGather";
+  }
+  const ncclResult_t r_end = api.groupEnd();
+  if (r != ncclSuccess || r_end != ncclSuccess) {
+    set_error(std::string(r != ncclSuccess ? what : "ncclGroupEnd") + ": " +
+              api.errorString(r != ncclSuccess ? r : r_end));
+    return FM_CUDA_ERROR;
+  }
   k_slab_unpack<<<n ? grid_for(n, 256) : 1, 256, 0, s>>>(n, x->pos, x->recv, g, x->jall, x->world,
                                                          J);
   FM_CHECK_LAUNCH();
