@@ -185,6 +185,25 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
   };
   int64_t s_next = row_src(tid);
   const int H = blk_header(tm.node_count);
+  // p-Laplace (small row block, registers to spare): this thread's row of the
+  // NEXT chunk (record and closure indices) is loaded into registers right
+  // after the current rows phase, so that the items and node-sum phases hide
+  // its latency (cfg2 1.156 -> 1.109 ms).  Neo-Hookean keeps an L2 prefetch:
+  // the extra live registers spill in its items loop (cfg4 4.51 -> 4.93 ms),
+  // although the record loads are ~19 % of its time (profiling ablation
+  // FM_FD_ABL_REC: 3.65 ms with every row reading one cached record).
+  constexpr bool REGPF = MODEL == FM_MODEL_PLAPLACE;
+  double2 qn[NQ];
+  uint2 lwn = make_uint2(0, 0);
+  auto fetch = [&](int e, int64_t st) {
+    if (e >= ne_t) return;
+    const double2 *p = reinterpret_cast<const double2 *>(a.aos + st * RB);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) qn[k] = ld_stream(p + k);
+    lwn = e >= tm.own_count ? __ldg(a.halo_loc + tm.halo_begin + e - tm.own_count)
+                            : __ldg(a.loc + st);
+  };
+  if constexpr (REGPF) fetch(tid, s_next);
   for (int c0 = 0, ch = 0; c0 < ne_t; c0 += CT, ++ch) {
     // ---- the chunk's node offsets (its entry block's header) and its
     // row-major items: asynchronous copies (LDGSTS), landing during the rows
@@ -204,13 +223,26 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
     const int e = c0 + tid;
     const int64_t s = s_next;
     if (e < ne_t) {
-      const bool halo = e >= tm.own_count;
-      const int h = tm.halo_begin + e - tm.own_count;
-      const double2 *p = reinterpret_cast<const double2 *>(a.aos + s * RB);
       double2 q[NQ];
+      uint2 lw;
+      if constexpr (REGPF) {
 #pragma unroll
-      for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
-      const uint2 lw = halo ? __ldg(a.halo_loc + h) : __ldg(a.loc + s);
+        for (int k = 0; k < NQ; ++k) q[k] = qn[k];
+        lw = lwn;
+      } else {
+        const bool halo = e >= tm.own_count;
+        const int h = tm.halo_begin + e - tm.own_count;
+#ifdef FM_FD_ABL_REC
+        // profiling ablation: every row reads the tile's first record (cached)
+        const int64_t sr = tm.own_begin;
+#else
+        const int64_t sr = s;
+#endif
+        const double2 *p = reinterpret_cast<const double2 *>(a.aos + sr * RB);
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) q[k] = ld_stream(p + k);
+        lw = halo ? __ldg(a.halo_loc + h) : __ldg(a.loc + s);
+      }
       Elem<DIM> E;
       decode_elem<DIM>(q, E);
       decode_loc(lw, E.loc);
@@ -261,9 +293,12 @@ __global__ void __launch_bounds__(CT, (DIM == 2 ? 1024 : 512) / CT)
         fld(R::BASE, tid) = sumsq_rn<DIM, D>(F);
       }
     }
-    // next chunk: its storage ids now, its own records towards L2
+    // next chunk: its storage ids now, its records (into registers, or
+    // towards L2)
     s_next = row_src(e + CT);
-    if (s_next >= 0) {
+    if constexpr (REGPF) {
+      fetch(e + CT, s_next);
+    } else if (s_next >= 0) {
       const uint8_t *pn = a.aos + s_next * RB;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + RB - 1));
