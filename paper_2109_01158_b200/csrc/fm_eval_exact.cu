@@ -73,6 +73,11 @@ struct PipeLayout {
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
   // per-tile tables: node descriptors | exchange-item chunk starts
   __host__ __device__ static size_t tabs() { return (size_t)CT * 16 + XCH_STRIDE * 4; }
+  // contributions staging: [slot][component][row], except D = 2 (2D
+  // Neo-Hookean): [slot][row][2] (one 16-B store / load per entry; cfg3 tile
+  // kernel 0.1086 -> 0.1064 ms — the same with 4 padded doubles for D = 3
+  // conflicts on the stores: 0.843 -> 0.975 ms at cfg4)
+  static constexpr bool AOS(int D) { return D == 2; }
   __host__ __device__ static size_t staging(int D) { return r16((size_t)CT * (DIM + 1) * D * 8); }
   // nb node-value buffers, tb table buffers (2: the next tile's tables load a
   // tile ahead)
@@ -352,6 +357,11 @@ __global__ void __launch_bounds__(CT, MINB)
   double *stage_d = reinterpret_cast<double *>(tabs0 + TB * L::tabs());
   double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stage_d) +
                                            L::staging(D));
+  // address of (slot, row) in the staging and the stride between components
+  auto st_at = [&](int slot, int row) -> double * {
+    return L::AOS(D) ? stage_d + (slot * CT + row) * D : stage_d + row + slot * D * CT;
+  };
+  constexpr int CS = L::AOS(D) ? 1 : CT;
   uint64_t *full = reinterpret_cast<uint64_t *>(red + 32);  // record stages
   uint64_t *nfull = full + 2;                               // node-value buffers
   uint64_t *cfull = nfull + 2;                              // closure ids
@@ -578,7 +588,7 @@ __global__ void __launch_bounds__(CT, MINB)
               double sdot = P[k][0] * E.g[0][l];
 #pragma unroll
               for (int m = 1; m < DIM; ++m) sdot = fma(P[k][m], E.g[m][l], sdot);
-              stage_d[(l * D + k) * CT + tid] = sdot;  // [slot][comp][row]
+              st_at(l, tid)[k * CS] = sdot;
             }
           if (WJ) {
             if (far) Wel += 2.0 * mdl.C1 * (ls_el - log(det_el));
@@ -600,32 +610,32 @@ __global__ void __launch_bounds__(CT, MINB)
           for (; i + 1 < n; i += 2) {
             const int e0 = ents[i], e1 = ents[i + 1];
             if ((e1 >> 2) >= ne_t) break;  // cross entries (finishing pass) from here on
-            const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
-            const double *s1 = stage_d + ((e1 >> 2) - c0) + (e1 & 3) * D * CT;
+            const double *s0 = st_at(e0 & 3, (e0 >> 2) - c0);
+            const double *s1 = st_at(e1 & 3, (e1 >> 2) - c0);
             double x0[D], x1[D];
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-              x0[k] = s0[k * CT];
-              x1[k] = s1[k * CT];
+              x0[k] = s0[k * CS];
+              x1[k] = s1[k * CS];
             }
 #pragma unroll
             for (int k = 0; k < D; ++k) acc[k] = (acc[k] + x0[k]) + x1[k];
           }
           if (i < n) {
             const int e0 = ents[i];
-            const double *s0 = stage_d + ((e0 >> 2) - c0) + (e0 & 3) * D * CT;
+            const double *s0 = st_at(e0 & 3, (e0 >> 2) - c0);
             if ((e0 >> 2) < ne_t) {
 #pragma unroll
-              for (int k = 0; k < D; ++k) acc[k] += s0[k * CT];
+              for (int k = 0; k < D; ++k) acc[k] += s0[k * CS];
             }
           }
         }
         for (int i = xb + tid; i < xe; i += CT) {
           const int key = i == xb + tid ? xkey0 : (int)__ldg(a.xkey + i);
           const int64_t pos = i;  // item i -> exchange slot i (coalesced stores)
-          const double *sp = stage_d + ((key >> 2) - c0) + (key & 3) * D * CT;
+          const double *sp = st_at(key & 3, (key >> 2) - c0);
 #pragma unroll
-          for (int k = 0; k < D; ++k) a.xbuf[pos * D + k] = sp[k * CT];
+          for (int k = 0; k < D; ++k) a.xbuf[pos * D + k] = sp[k * CS];
         }
         // one staging buffer: it must be consumed before the next chunk writes
         // it; two: the next chunk's barrier already orders this consumption
