@@ -151,9 +151,11 @@ def energy(v: np.ndarray, mesh: Mesh, model, load: LinearLoad | None = None):
     ctx = context_for(mesh, None, d)
     vd = to_dev(v)
     dens = torch.empty(mesh.ne, dtype=torch.float64, device="cuda")
-    J = ctx.energy(vd, model, _load_device(load), dens)
-    Jh = to_host(J)
-    return float(Jh[0]), to_host(dens)
+    with ctx.lock:
+        J = torch.empty(3, dtype=torch.float64, device="cuda")
+        ctx.energy(vd, model, _load_device(load), dens, out=J)
+        Jh = to_host(J)
+        return float(Jh[0]), to_host(dens)
 
 
 def interpolate(fn, mesh: Mesh, d: int) -> np.ndarray:

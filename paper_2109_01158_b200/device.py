@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import sys
+import threading
 import weakref
 
 import numpy as np
@@ -82,6 +83,11 @@ class DeviceMesh:
         self.nfree_dofs = self._count_free_dofs(fixed, nodes_minim)
         self.device = torch.cuda.current_device()
         self._J = torch.empty(3, dtype=torch.float64, device="cuda")
+        # the context's scratch (exchange buffer, partials, status latch) is
+        # shared by its launches: the numpy drop-in holds this lock around
+        # each call so concurrent callers behave like the pure reference
+        # functions
+        self.lock = threading.RLock()
 
     # argument checks: raw pointers go to the kernels, so sizes / dtypes /
     # devices are validated here (ValueError), never by assert
@@ -316,7 +322,15 @@ def _is_canonical(mesh, patches, d) -> bool:
     return all(a.shape == b.shape and bool(torch.equal(a, b)) for a, b in zip(ref, got))
 
 
+_CTX_LOCK = threading.RLock()
+
+
 def context_for(mesh, patches=None, d=None) -> DeviceMesh:
+    with _CTX_LOCK:
+        return _context_for(mesh, patches, d)
+
+
+def _context_for(mesh, patches=None, d=None) -> DeviceMesh:
     d = int(mesh.d if d is None else d)
     key = (id(mesh), d)
     if patches is not None:

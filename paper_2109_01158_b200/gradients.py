@@ -54,9 +54,10 @@ def exact_gradient(v: np.ndarray, mesh: Mesh, patches: Patches, model,
                    load: LinearLoad | None = None) -> np.ndarray:
     """Chain-rule gradient through dW/dF on the free dofs (gradients.py:124-149)."""
     ctx, vd = _prep(v, mesh, patches, model)
-    g = ctx.exact_gradient(vd, model, _load_device(load))
-    ctx.check()
-    return to_host(g)
+    with ctx.lock:
+        g = ctx.exact_gradient(vd, model, _load_device(load))
+        ctx.check()
+        return to_host(g)
 
 
 def numeric_gradient(v: np.ndarray, mesh: Mesh, patches: Patches, model,
@@ -65,9 +66,10 @@ def numeric_gradient(v: np.ndarray, mesh: Mesh, patches: Patches, model,
     if eps <= 0:
         raise ValueError("central-difference step must be positive")
     ctx, vd = _prep(v, mesh, patches, model)
-    g = ctx.numeric_gradient(vd, model, _load_device(load), eps)
-    ctx.check()
-    return to_host(g)
+    with ctx.lock:
+        g = ctx.numeric_gradient(vd, model, _load_device(load), eps)
+        ctx.check()
+        return to_host(g)
 
 
 def gradient(v, mesh, patches, model, load=None, cfg: GradientConfig | None = None):
@@ -85,10 +87,11 @@ def energy_and_gradient(v, mesh, patches, model, load=None, cfg: GradientConfig 
     ctx, vd = _prep(v, mesh, patches, model)
     b = _load_device(load)
     J = torch.empty(3, dtype=torch.float64, device="cuda")
-    if cfg.mode == "exact":
-        g = ctx.exact_gradient(vd, model, b, J=J)
-    else:
-        ctx.energy(vd, model, b, out=J)
-        g = ctx.numeric_gradient(vd, model, b, cfg.eps)
-    ctx.check()
-    return float(to_host(J)[0]), to_host(g)
+    with ctx.lock:
+        if cfg.mode == "exact":
+            g = ctx.exact_gradient(vd, model, b, J=J)
+        else:
+            ctx.energy(vd, model, b, out=J)
+            g = ctx.numeric_gradient(vd, model, b, cfg.eps)
+        ctx.check()
+        return float(to_host(J)[0]), to_host(g)

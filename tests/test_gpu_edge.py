@@ -155,3 +155,43 @@ def test_componentwise_dirichlet_2d():
     v = O.field_nh(om, 29, 1e-2 * 2.0 / 16)
     b = O.load_vector(om, (0.0, -3.5e7), 2)
     _check_all(om, v, b, model, omodel)
+
+
+def test_concurrent_drop_in_calls():
+    """The reference functions are pure: concurrent calls on one
+    mesh from several threads, one of them on an inadmissible field, give the
+    serial results and raise only in the offending thread."""
+    import threading
+    om = O.beam_mesh(12, 6, 6, 0.0, 2.0, 0.0, 1.0, 0.0, 1.0)
+    om = O.mark_dirichlet(om, O.fixed_mask(om, [(O.left_face, None)], 3), 3)
+    m = _fb_mesh(om)
+    pt = fb.build_patches(m)
+    model, _ = _nh(3)
+    load = fb.LinearLoad(b=O.load_vector(om, (0.0, 0.0, -2.5e7), 3))
+    fields = [O.field_nh(om, 100 + k, 1e-2 * 2.0 / 12) for k in range(6)]
+    fields[3] = np.zeros_like(fields[3])  # inadmissible: det F = 0
+    serial = []
+    for k, v in enumerate(fields):
+        try:
+            serial.append(fb.energy_and_gradient(v, m, pt, model, load))
+        except fb.InadmissibleStateError:
+            serial.append("raise")
+    assert serial[3] == "raise"
+    out = [None] * len(fields)
+
+    def work(k):
+        for _ in range(5):
+            try:
+                out[k] = fb.energy_and_gradient(fields[k], m, pt, model, load)
+            except fb.InadmissibleStateError:
+                out[k] = "raise"
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(fields))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for a, b in zip(out, serial):
+        if isinstance(b, str):
+            assert a == b
+        else:
+            assert a[0] == b[0] and np.array_equal(a[1], b[1])
