@@ -273,6 +273,10 @@ def main():
     ap.add_argument("--stream-depth", type=int, default=2)
     ap.add_argument("--ref-procs", type=int, default=0,
                     help="--impl reference: host processes (default: all cores)")
+    ap.add_argument("--max-context-elems", type=int, default=1 << 28,
+                    help="beams: a rank slab with more tets is held as sub-slab contexts")
+    ap.add_argument("--sub-elems", type=int, default=50_000_000,
+                    help="beams: max tets per sub-slab context when a slab is split")
     ap.add_argument("--shard", type=str, default="",
                     help="r/w: run rank r's x1-slab of a w-way partition on this one GPU")
     ap.add_argument("--descent-iters", type=int, default=100,
@@ -318,7 +322,20 @@ def main():
                 raise SystemExit("--shard emulates one rank on one GPU; not under torchrun")
             prank, pworld = (int(x) for x in args.shard.split("/"))
         ix0, ix1 = slab_range(nx, prank, pworld)
-        pr = problems.beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1, tiling=tiling)
+        ne_rank = 6 * (ix1 - ix0) * ny * nz
+        if ne_rank > args.max_context_elems:
+            # a slab too large for one context (config 5 at 2 GPUs: 805 M tets
+            # per rank): sub-slab contexts built one after another
+            from types import SimpleNamespace
+
+            from paper_2109_01158_b200.parallel import SlabStack, stack_parts
+            stack = SlabStack(nx, ny, nz, ix0, ix1, stack_parts(ne_rank, args.sub_elems),
+                              seed=2109, tiling=tiling)
+            pr = SimpleNamespace(dm=stack, model=stack.model, b=stack.B, v=stack.V,
+                                 ne=stack.ne, nn=stack.nn,
+                                 meta=dict(nx=nx, ny=ny, nz=nz, ix0=ix0, ix1=ix1))
+        else:
+            pr = problems.beam(nx, ny, nz, seed=2109, ix0=ix0, ix1=ix1, tiling=tiling)
         workload = (f"{args.config}: 3D compressible Neo-Hookean beam [0,2]x[0,1]^2, "
                     f"{nx}x{ny}x{nz} hexes x 6 Kuhn tets ({6 * nx * ny * nz:,} tets, "
                     f"{(nx + 1) * (ny + 1) * (nz + 1):,} nodes), f=(0,0,-2.5e7), v=x on x1=0")
@@ -327,6 +344,9 @@ def main():
             workload += (f"; ONE rank's x1-slab [{ix0},{ix1}) of the {pworld}-way partition "
                          f"({pr.ne:,} tets) on this GPU, no exchange")
             ne_total = pr.ne
+        if hasattr(pr.dm, "ranges"):
+            workload += (f"; each rank's slab held as {pr.dm.K} sub-slab contexts "
+                         f"(<= {args.sub_elems:,} tets each, interfaces summed on the device)")
     else:
         if world > 1:
             raise SystemExit("only the beams (cfg4, cfg5) are partitioned across GPUs")
@@ -410,7 +430,11 @@ def main():
     free_b, total_b = torch.cuda.mem_get_info()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
-    kms = sum(a.elapsed_time(z) for a, z in kev) / args.steps
+    if hasattr(dm, "kernel_ms"):  # sub-slab stack: the sub-slabs' tile kernels summed
+        kl = dm.kernel_ms()
+        kms = sum(kl) / max(1, len(kl))
+    else:
+        kms = sum(a.elapsed_time(z) for a, z in kev) / args.steps
     if world > 1:
         tt = torch.tensor([ms, kms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -436,7 +460,10 @@ def main():
             dm.numeric_gradient(v, model, b, fd_eps, g=gfd0)
         torch.cuda.synchronize()
         dm.check()
-        fd_ms = statistics.median(a_.elapsed_time(z_) for a_, z_ in fev)
+        if hasattr(dm, "kernel_ms"):
+            fd_ms = statistics.median(dm.kernel_ms())
+        else:
+            fd_ms = statistics.median(a_.elapsed_time(z_) for a_, z_ in fev)
         states = 2 * dm.d * dm.stats["node_entries_total"]
         flop = states * fd_flops_per_state(dm.dim, dm.d)
         fpk, fsrc = _fp64_peak()

@@ -239,6 +239,17 @@ int fm_slab_create(const void *id_host, int rank, int world, int64_t n_plane,
 int fm_slab_reduce(fm_slab *x, double *g, double *J, void *stream);
 int fm_slab_destroy(fm_slab *x);
 
+/* Sub-slab stack (new): a rank's slab held as K evaluation contexts on one
+ * GPU (cfg5 at 2 GPUs: 805 M tetrahedra per rank exceed one context), their
+ * gradients back to back in g.  For the n interface dofs shared by
+ * consecutive sub-slabs (positions a[k], b[k] in g, device int64):
+ * g[a[k]] = g[b[k]] = g[a[k]] + g[b[k]]; with J non-NULL, J (device
+ * double[3]) = the K sub-slab partials jk (K x 3) summed in order.  No
+ * reference counterpart (the reference is single-domain); the sums are the
+ * element sums of gradients.py:124-149 split at the sub-slab planes. */
+int fm_stack_reduce(int64_t n, const int64_t *a, const int64_t *b, double *g, const double *jk,
+                    int K, double *J, void *stream);
+
 /* Synchronises `stream`, returns the latched condition of the evaluations
  * since the last check and clears it: FM_OK or FM_INADMISSIBLE with
  * *index_host = offending dof (FD, gradients.py:77-81) or -1 (exact path). */

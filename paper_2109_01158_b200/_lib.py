@@ -83,6 +83,7 @@ SIGNATURES = {
     "fm_slab_create": (C.c_int, [vp, C.c_int, C.c_int, i64, vp, vp, vp]),
     "fm_slab_reduce": (C.c_int, [vp, vp, vp, vp]),
     "fm_slab_destroy": (C.c_int, [vp]),
+    "fm_stack_reduce": (C.c_int, [i64, vp, vp, vp, vp, C.c_int, vp, vp]),
     "fm_cg_scratch_doubles": (C.c_int, []),
     "fm_cg_init": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fm_cg_embed": (C.c_int, [vp, vp, vp, vp, C.c_int, dbl, vp, vp]),

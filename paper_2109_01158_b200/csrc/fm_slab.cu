@@ -98,6 +98,28 @@ __global__ void k_slab_unpack(int64_t n, const int64_t *__restrict__ pos,
   }
 }
 
+// Sub-slab stack on one GPU (a rank's slab split into several contexts):
+// the partials of the n interface dofs shared by consecutive sub-slabs,
+// s = g[a[k]] + g[b[k]], stored to both copies (bitwise equal, like the
+// NCCL exchange's own + received); block 0 also J[0..2] = the K sub-slab
+// partials summed in sub-slab order
+__global__ void k_stack_reduce(int64_t n, const int64_t *__restrict__ a,
+                               const int64_t *__restrict__ b, double *__restrict__ g,
+                               const double *__restrict__ jk, int K, double *J) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = a[k], j = b[k];
+    const double s = g[i] + g[j];
+    g[i] = s;
+    g[j] = s;
+  }
+  if (J && blockIdx.x == 0 && threadIdx.x < 3) {
+    double s = 0.0;
+    for (int r = 0; r < K; ++r) s += jk[3 * r + threadIdx.x];
+    J[threadIdx.x] = s;
+  }
+}
+
 }  // namespace
 }  // namespace fm
 
@@ -179,6 +201,20 @@ int fm_slab_create(const void *id_host, int rank, int world, int64_t n_plane,
       cudaMemcpy(x->pos + o, right_pos, n_plane * 8, cudaMemcpyDeviceToDevice) != cudaSuccess)
     return fail(FM_CUDA_ERROR);
   *out = x;
+  return FM_OK;
+}
+
+int fm_stack_reduce(int64_t n, const int64_t *a, const int64_t *b, double *g, const double *jk,
+                    int K, double *J, void *stream) {
+  FM_NVTX("fm_stack_reduce");
+  FM_ARG(n >= 0 && K >= 0, "negative size");
+  FM_ARG(n == 0 || (a && b && g), "null plane positions or gradient");
+  FM_ARG(!J || (jk && K > 0), "J needs the sub-slab partials");
+  if (n == 0 && !J) return FM_OK;
+  cudaStream_t s = as_stream(stream);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184));
+  k_stack_reduce<<<grid, 256, 0, s>>>(n, a, b, g, jk, K, J);
+  FM_CUDA(cudaGetLastError());
   return FM_OK;
 }
 
