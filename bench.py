@@ -467,7 +467,7 @@ def main():
         states = 2 * dm.d * dm.stats["node_entries_total"]
         flop = states * fd_flops_per_state(dm.dim, dm.d)
         fpk, fsrc = _fp64_peak()
-        fd_line = {"bound": "fp64", "kernel": "k_tile_fd", "kernel_ms": fd_ms,
+        fd_line = {"bound": "fp64", "kernel": "k_tile_exact<FD mode>", "kernel_ms": fd_ms,
                    "eps": fd_eps, "perturbed_states": states,
                    "flop_per_state": fd_flops_per_state(dm.dim, dm.d),
                    "achieved": flop / (fd_ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",

@@ -30,7 +30,6 @@ UNITS = {
     "fm_ctx.cu": [],
     "fm_eval_exact.cu": [],
     "fm_eval_ref.cu": [],
-    "fm_eval_fd.cu": [],
     "fm_hessian.cu": [],
     "fm_cg.cu": [],
     "fm_slab.cu": [],

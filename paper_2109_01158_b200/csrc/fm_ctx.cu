@@ -451,7 +451,9 @@ __global__ void k_chunk_blocks(int n_tiles, const TileMeta *meta, const int4 *de
   __shared__ int wsum[32];
   const int t = blockIdx.x;
   const TileMeta tm = meta[t];
-  const int nch = (tm.own_count + tm.halo_count + ct - 1) / ct;
+  // the own chunks only: the tile kernels compute each element once, by its
+  // owner, and never load a block for the halo (cross) elements
+  const int nch = (tm.own_count + ct - 1) / ct;
   const int k = threadIdx.x;  // blockDim.x >= node_count (<= 256)
   const bool my = k < tm.node_count;
   const int4 nd = my ? desc[tm.node_begin + k] : make_int4(0, 0, 0, 0);
@@ -479,58 +481,6 @@ __global__ void k_chunk_blocks(int n_tiles, const TileMeta *meta, const int4 *de
       cur += cnt;
     }
     if (k == 0) blk[tm.node_count] = (uint16_t)total;
-    __syncthreads();
-  }
-}
-
-// Row-major FD items: per tile (one CTA) and chunk, the chunk's node entries
-// (node-major in its entry block) re-listed in (row, slot) order with their
-// node-major position p, so that the FD kernel's consecutive threads work on
-// consecutive element rows (shared-memory row reads broadcast instead of
-// conflicting) and still write their results to the node-major slots.
-// (row, slot) pairs are unique, so the order is deterministic.
-__global__ void k_fd_items(int n_tiles, const TileMeta *meta, const uint16_t *blocks, int ct,
-                           uint32_t *items) {
-  extern __shared__ uint32_t rmask[];  // ct row masks | ct row starts
-  uint32_t *rstart = rmask + ct;
-  __shared__ int wsum[32];
-  const int t = blockIdx.x;
-  const TileMeta tm = meta[t];
-  const int nch = (tm.own_count + tm.halo_count + ct - 1) / ct;
-  const int H = blk_header(tm.node_count);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int ch = 0; ch < nch; ++ch) {
-    const uint16_t *blk = blocks + tm.blk_base + (int64_t)ch * tm.blk_stride;
-    uint32_t *out = items + tm.blk_base + (int64_t)ch * tm.blk_stride;
-    const int total = blk[tm.node_count];
-    for (int r = threadIdx.x; r < ct; r += blockDim.x) rmask[r] = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < total; p += blockDim.x) {
-      const int en = blk[H + p];
-      atomicOr(&rmask[(en >> 2) - ch * ct], 1u << (en & 3));
-    }
-    __syncthreads();
-    // exclusive scan of the rows' entry counts (blockDim.x == ct)
-    const int r = threadIdx.x;
-    const int cnt = __popc(rmask[r]);
-    int incl = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    int before = 0;
-    for (int u = 0; u < w; ++u) before += wsum[u];
-    rstart[r] = before + incl - cnt;
-    (void)nw;
-    __syncthreads();
-    for (int p = threadIdx.x; p < total; p += blockDim.x) {
-      const int en = blk[H + p];
-      const int rr = (en >> 2) - ch * ct, l = en & 3;
-      const int pos = rstart[rr] + __popc(rmask[rr] & ((1u << l) - 1u));
-      out[pos] = ((uint32_t)p << 16) | ((uint32_t)rr << 2) | (uint32_t)l;
-    }
     __syncthreads();
   }
 }
@@ -744,6 +694,7 @@ static ModelArgs model_args(const fm_model *m) {
   a.D1 = m->D1;
   a.e_w = m->p / 2.0;
   a.e_dw = (m->p - 2.0) / 2.0;
+  a.eps = 0.0;
 #if FM_ABLATE
   static const int ablate = [] {
     const char *e = getenv("FM_TILE_ABLATE");
@@ -1400,14 +1351,14 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
     CK(cudaMemcpyAsync(&h_cmax, cmax.p, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_pch.data(), pch.p, h_pch.size() * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    c->chunk_entry_cap = ((int)h_cmax + 7) / 8 * 8;
+    (void)h_cmax;
 
     // 5a. chunk-major entry blocks (the tile kernels load a chunk's block with
     // its records): per tile a fixed stride = its largest block
     int64_t blk_total = 0;
     c->blk_cap = 0;
     for (int t = 0; t < n_tiles; ++t) {
-      const int nch = (hm[t].own_count + hm[t].halo_count + c->tile_nodes - 1) / c->tile_nodes;
+      const int nch = (hm[t].own_count + c->tile_nodes - 1) / c->tile_nodes;  // own chunks
       int mx = 0;
       for (int ch = 0; ch < nch; ++ch) mx = std::max(mx, h_pch[(size_t)t * MAX_CHUNKS + ch]);
       const int stride = blk_header(hm[t].node_count) + (mx + 7) / 8 * 8;
@@ -1571,12 +1522,13 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
   }
 
   // build-only tables: the kernels read the chunk entry blocks instead of the
-  // node-major entry lists, no kernel reads the owned-slot flags, and the
+  // node-major entry lists, no kernel reads the owned-slot flags or the halo
+  // lists (every element is computed once, by its owner tile), and the
   // finishing pass reads the packed xdesc instead of the per-node arrays
   CK(cudaStreamSynchronize(s));
   for (void **p : {(void **)&c->node_entries, (void **)&c->flags, (void **)&c->node_xbase,
                    (void **)&c->node_xn, (void **)&c->node_outw, (void **)&c->node_fmask,
-                   (void **)&c->xnodes}) {
+                   (void **)&c->xnodes, (void **)&c->halo_ids, (void **)&c->halo_loc}) {
     if (*p) CK(cudaFree(*p));
     *p = nullptr;
   }
@@ -1662,7 +1614,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw, c->node_fmask,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
-                  c->xnodes,    c->dof_pos,   c->fd_items,  c->xdesc};
+                  c->xnodes,    c->dof_pos,   c->xdesc};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1778,24 +1730,25 @@ int fm_grad_fd(fm_ctx *c, const fm_model *model, const double *v, const double *
   if (c->n_tiles == 0) return FM_OK;
   cudaStream_t s = as_stream(stream);
   ModelArgs ma = model_args(model);
-  const int dm = model->kind == FM_MODEL_NEOHOOKEAN ? c->dim : 1;
-  if (!c->fd_items) {  // first FD call: the row-major item lists (4 B per entry slot)
-    FM_CUDA(cudaMalloc(&c->fd_items, (size_t)(c->blk_total + 8) * 4));
-    c->bytes += (size_t)(c->blk_total + 8) * 4;
-    k_fd_items<<<c->n_tiles, c->tile_nodes, 2 * c->tile_nodes * 4, s>>>(
-        c->n_tiles, c->meta, c->chunk_blocks, c->tile_nodes, c->fd_items);
-    FM_CUDA(cudaGetLastError());
+  ma.eps = eps;
+  // every element once, by its owner tile (the fused tile kernel in FD mode:
+  // records by bulk copy, per-element perturbed states, the gradient's node
+  // sums / cross-tile exchange), then the finishing pass scales by 1 / (2 eps)
+  TileArgs ta = c->tile_args();
+  ta.n_tiles_all = c->n_tiles;  // orphan tiles have no free node
+  const int cps = std::min(c->ctas_per_sm, tile_fd_minb(c->dim, c->tile_nodes, model->kind));
+  const int grid = std::min(c->n_sm * cps, std::max(1, c->n_tiles));
+  {
+    TimedLaunch tl(c, s);
+    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
+                              c->table_bufs, 3, v, b, g, c->jpart, c->dotpart, c->status, ma, s));
     c->launches++;
   }
-  TimedLaunch tl(c, s);
-  if (tile_fd_smem(c->dim, model->kind, c->clo_cap, c->chunk_entry_cap, c->tile_nodes) >
-      227 * 1024) {
-    set_error("FD tile staging exceeds shared memory; use smaller tiles");
-    return FM_INVALID_ARG;
+  if (c->n_cross > 0) {
+    FM_CUDA(launch_finish_cross_fd(c->d, c->n_xnodes, c->xdesc, c->xpos, c->xbuf, c->partial, g,
+                                   eps, b, c->node_desc, s));
+    c->launches++;
   }
-  FM_CUDA(launch_tile_fd(c->dim, model->kind, c->tile_args(), c->n_tiles, c->tile_nodes,
-                         c->chunk_entry_cap, v, b, eps, g, c->status + 1, ma, s));
-  c->launches++;
   return FM_OK;
 }
 

@@ -185,6 +185,7 @@ struct ModelArgs {
   // p-Laplace exponents classified like numpy's fast scalar power
   // (ndarray ** scalar: 0.5 -> sqrt, 1 -> copy, 2 -> square, -1 -> reciprocal)
   double e_w, e_dw;  // p/2 and (p-2)/2
+  double eps;       // FD step (fm_grad_fd; 0 otherwise)
   int dbg;           // profiling ablations of the tile kernel, read through FM_DBG (FM_TILE_ABLATE,
                      // tools/ablate.py: 1 no constitutive, 2 no consume, 8 no compute, 32 no
                      // closure gathers; results are wrong on purpose), 0 = off
@@ -246,7 +247,6 @@ struct TileArgs {
   // FD items (built on the first FD call): per tile and chunk, at the chunk
   // block's index range, the chunk's entries in ROW-major order, each
   // p << 16 | row << 2 | slot with p its node-major position (stg slot)
-  const uint32_t *fd_items;
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
@@ -275,7 +275,6 @@ struct fm_ctx {
   int32_t n_tiles = 0, n_tiles_all = 0;
   int64_t n_tile_elems = 0, n_node_entries = 0;
   int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, clo_cap = 0;
-  int chunk_entry_cap = 0;  // max node entries of one chunk of one tile (FD staging)
   int n_sm = 0, ctas_per_sm = 2, node_bufs = 2, table_bufs = 2;
   uint8_t *aos = nullptr;
   int4 *conn4 = nullptr;
@@ -303,7 +302,6 @@ struct fm_ctx {
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units
   int64_t blk_total = 0;             // size of chunk_blocks, u16 units
-  uint32_t *fd_items = nullptr;      // row-major FD items (TileArgs::fd_items), lazily built
   int64_t n_cross = 0;
   int32_t *fixed_nodes = nullptr;  // nodes without a free dof (their b.v: finishing pass)
   int64_t n_fixed_nodes = 0;
@@ -324,6 +322,6 @@ struct fm_ctx {
                         loc,     closure, flags,   node_desc,       node_entries, chunk_blocks,
                         rank_of, xkey,
                         xpos,    xchunk,  xbuf,            partial,   node_clo,    n_tiles,
-                        n_tiles_all, entry_cap, blk_cap, clo_cap, fd_items};
+                        n_tiles_all, entry_cap, blk_cap, clo_cap};
   }
 };

@@ -103,42 +103,6 @@ __device__ __forceinline__ double density(const double (&F)[MODEL == FM_MODEL_NE
   }
 }
 
-// log(det) of a perturbed state from its unperturbed row's det0, 1/det0 and
-// ld0 = log(det0): ld0 + log1p(x), x = (det - det0) / det0 (the subtraction is
-// exact for det within a factor 2 of det0), log1p by its Taylor polynomial to
-// x^7 when |x| < 1e-3 (relative truncation < 1.5e-19); otherwise log(det).
-// The error stays within a few ulps of log(det), the libm term the FD
-// tolerance already allows for.
-__device__ __forceinline__ double log_near(double det, double det0, double rdet0, double ld0) {
-  const double x = (det - det0) * rdet0;
-  if (!(fabs(x) < 1e-3)) return log(det);  // also det0 <= 0 (NaN ld0, huge x)
-  double p = fma(x, 1.0 / 7.0, -1.0 / 6.0);
-  p = fma(p, x, 1.0 / 5.0);
-  p = fma(p, x, -0.25);
-  p = fma(p, x, 1.0 / 3.0);
-  p = fma(p, x, -0.5);
-  p = fma(p, x, 1.0);
-  return ld0 + p * x;
-}
-
-// Neo-Hookean W of a perturbed FD state (density() with log_near).
-template <int DIM>
-__device__ __forceinline__ double density_nh_near(const double (&F)[DIM][DIM], const ModelArgs &m,
-                                                  double det0, double rdet0, double ld0) {
-  double det = det_F<DIM>(F);
-  double I1 = rmul(F[0][0], F[0][0]);
-#pragma unroll
-  for (int j = 0; j < DIM; ++j)
-#pragma unroll
-    for (int k = 0; k < DIM; ++k)
-      if (j + k > 0) I1 = radd(I1, rmul(F[j][k], F[j][k]));
-  if (!(det > 0.0)) return INFINITY;
-  double ld = log_near(det, det0, rdet0, ld0);
-  double dm1 = rsub(det, 1.0);
-  return radd(rmul(m.C1, rsub(rsub(I1, (double)DIM), rmul(2.0, ld))),
-              rmul(m.D1, rmul(dm1, dm1)));
-}
-
 // dW/dF; sets bad when det <= 0 (Neo-Hookean).
 template <int DIM, int MODEL>
 __device__ __forceinline__ void ddensity(const double (&F)[MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1][DIM],
@@ -170,6 +134,61 @@ __device__ __forceinline__ void ddensity(const double (&F)[MODEL == FM_MODEL_NEO
       fac = n2 > 0.0 ? pow(n2, m.e_dw) : 0.0;
 #pragma unroll
     for (int k = 0; k < DIM; ++k) P[0][k] = rmul(fac, F[0][k]);
+  }
+}
+
+// ---- FD states (gradients.py:84-121) from the unperturbed invariants ------
+// states with det below this (absolute; det ~ 1 for the elastic configs) are
+// recomputed in the reference's operation order by the caller
+constexpr double FD_DET_NEAR = 1e-3;
+
+// log1p(x) for |x| < 1e-3 (degree 7, relative truncation < 1.5e-19)
+__device__ __forceinline__ double log1p_small(double x) {
+  double p = fma(x, 1.0 / 7.0, -1.0 / 6.0);
+  p = fma(p, x, 1.0 / 5.0);
+  p = fma(p, x, -0.25);
+  p = fma(p, x, 1.0 / 3.0);
+  p = fma(p, x, -0.5);
+  p = fma(p, x, 1.0);
+  return p * x;
+}
+
+// |F|^2 in the reference's order (models.py:89-100: sequential sum of squares)
+template <int DIM, int D>
+__device__ __forceinline__ double sumsq_rn(const double (&F)[D][DIM]) {
+  double s = rmul(F[0][0], F[0][0]);
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+      if (j + k > 0) s = radd(s, rmul(F[j][k], F[j][k]));
+  return s;
+}
+
+// W of one perturbed state: row j of F moved by dl * dphi[:, l] (dl = the
+// step the rounded perturbed value carries), so det = det0 + dl c,
+// |F|^2 = I1_0 + dl (a + dl b), log det = log det0 + log1p(dl c / det0)
+// (NH; p-Laplace: |g|^2 = n2_0 + dl (a + dl b)), W the reference's expression
+// of those invariants (models.py:89-100, 123-126).  exact = true (W not
+// computed): det near 0, the caller recomputes the state the reference's way.
+template <int DIM, int MODEL>
+__device__ __forceinline__ double fd_state_w(double dl, double cj, double aj, double bb,
+                                             double base0, double rdet0, double ld0, double i10,
+                                             const ModelArgs &m, bool &exact) {
+  if constexpr (MODEL == FM_MODEL_NEOHOOKEAN) {
+    const double det = fma(dl, cj, base0);
+    if (!(det > FD_DET_NEAR)) {
+      exact = true;
+      return 0.0;
+    }
+    const double I1 = fma(dl, fma(dl, bb, aj), i10);
+    const double x = (dl * cj) * rdet0;
+    const double ld = fabs(x) < 1e-3 ? ld0 + log1p_small(x) : log(det);
+    const double dm1 = det - 1.0;
+    return m.C1 * ((I1 - (double)DIM) - 2.0 * ld) + m.D1 * (dm1 * dm1);
+  } else {
+    const double n2 = fmax(fma(dl, fma(dl, bb, aj), base0), 0.0);
+    return np_scalar_pow(n2, m.e_w) / m.p;
   }
 }
 

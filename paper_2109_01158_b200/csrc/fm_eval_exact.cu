@@ -310,6 +310,180 @@ __device__ __forceinline__ void grad_F_fma(const double (&vv)[D][DIM + 1],
     }
 }
 
+// Unperturbed invariants of an element for the FD states: F in einsum order
+// (the reference's unperturbed F), det, 1/det, log det and |F|^2 in the
+// reference's order (p-Laplace: |g|^2 in base0), and the rank-one
+// coefficients a_jl = 2 F_j . dphi_l, c_jl = cof(F)_j . dphi_l and
+// b_l = |dphi_l|^2 of every node l and component j.
+template <int DIM, int MODEL, int D>
+struct FdElem {
+  static constexpr int NV = DIM + 1;
+  static constexpr bool NH = MODEL == FM_MODEL_NEOHOOKEAN;
+  double A[D][NV], Cc[NH ? D : 1][NV], BB[NV];
+  double base0, rdet0 = 0.0, ld0 = 0.0, i10 = 0.0;
+  __device__ __forceinline__ FdElem(const double (&vv)[D][NV], const Elem<DIM> &E) {
+    double F[D][DIM];
+    grad_F<DIM, D>(vv, E.g, F);
+    double C[NH ? DIM : 1][DIM];
+    if constexpr (NH) {
+      base0 = det_F<DIM>(F);
+      rdet0 = 1.0 / base0;
+      ld0 = base0 > 0.0 ? log(base0) : NAN;
+      i10 = sumsq_rn<DIM, D>(F);
+      cof_F<DIM>(F, C);
+    } else {
+      base0 = sumsq_rn<DIM, D>(F);
+    }
+#pragma unroll
+    for (int l = 0; l < NV; ++l) {
+      double bb = E.g[0][l] * E.g[0][l];
+#pragma unroll
+      for (int q = 1; q < DIM; ++q) bb = fma(E.g[q][l], E.g[q][l], bb);
+      BB[l] = bb;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double s2 = F[j][0] * E.g[0][l];
+#pragma unroll
+        for (int q = 1; q < DIM; ++q) s2 = fma(F[j][q], E.g[q][l], s2);
+        A[j][l] = 2.0 * s2;
+        if constexpr (NH) {
+          double cj = C[j][0] * E.g[0][l];
+#pragma unroll
+          for (int q = 1; q < DIM; ++q) cj = fma(C[j][q], E.g[q][l], cj);
+          Cc[j][l] = cj;
+        }
+      }
+    }
+  }
+};
+
+// Where the FD states of a tile-kernel element report to: the staging row,
+// and the tile data that turns a non-finite state into the reference's
+// offending-row key (gradients.py:77-81: sign, component, free rank of the
+// node, element).
+struct FdSink {
+  double *st;       // staging of (slot 0, this row); slot l at st + l * sstride
+  int sstride, cs;  // slot stride, component stride (doubles)
+  const int32_t *closure, *rank_of, *s2o;
+  int clo_begin;
+  int64_t storage;  // the element's storage index
+};
+
+// The FD states of one element that the fast path left (det near 0, or
+// |dl c / det0| >= 1e-3): both signs of every flagged (l, j) recomputed with
+// the full rule of fd_state_w (the reference's own evaluation near det 0),
+// the difference restaged; non-finite states latch their key.  Out of line
+// and rare (flags: bit 2 (l D + j) + sg).
+template <int DIM, int MODEL>
+__device__ __noinline__ void fd_slow_states(unsigned flags, const unsigned char *stage, int row,
+                                            const double *nv, int CAP, int4 cl,
+                                            const ModelArgs &m, FdSink k,
+                                            unsigned long long *key) {
+  constexpr int NV = DIM + 1;
+  constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
+  Elem<DIM> E;
+  load_elem_smem<DIM>(stage, row, E);
+  const int c[4] = {cl.x, cl.y, cl.z, cl.w};
+  double vv[D][NV];
+#pragma unroll
+  for (int ll = 0; ll < NV; ++ll)
+#pragma unroll
+    for (int q = 0; q < D; ++q) vv[q][ll] = nv[q * CAP + c[ll]];
+  const FdElem<DIM, MODEL, D> fe(vv, E);
+#pragma unroll
+  for (int l = 0; l < NV; ++l)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (!((flags >> (2 * (l * D + j))) & 3u)) continue;
+      const double vl = vv[j][l];
+      double w[2];
+#pragma unroll
+      for (int sg = 0; sg < 2; ++sg) {
+        const double ve = radd(vl, sg ? m.eps : -m.eps);
+        const double dl = ve - vl;
+        bool exact = false;
+        double cj = 0.0;
+        if constexpr (FdElem<DIM, MODEL, D>::NH) cj = fe.Cc[j][l];
+        double W = fd_state_w<DIM, MODEL>(dl, cj, fe.A[j][l], fe.BB[l], fe.base0, fe.rdet0,
+                                          fe.ld0, fe.i10, m, exact);
+        if (exact) {  // the reference's own evaluation: row j of F from ve
+          double v2[D][NV];
+#pragma unroll
+          for (int ll = 0; ll < NV; ++ll)
+#pragma unroll
+            for (int q = 0; q < D; ++q) v2[q][ll] = vv[q][ll];
+          v2[j][l] = ve;
+          double F[D][DIM];
+          grad_F<DIM, D>(v2, E.g, F);
+          W = density<DIM, MODEL>(F, m);
+        }
+        if (!isfinite(W)) {
+          const int node = __ldg(k.closure + k.clo_begin + c[l]);
+          const int rk = __ldg(k.rank_of + node);
+          if (rk >= 0) {  // a fixed node: the reference never perturbs it
+            const unsigned long long kk = ((unsigned long long)sg << 63) |
+                                          ((unsigned long long)j << 61) |
+                                          ((unsigned long long)rk << 31) |
+                                          (unsigned long long)__ldg(k.s2o + k.storage);
+            *key = kk < *key ? kk : *key;
+          }
+        }
+        w[sg] = rmul(E.vol, W);
+      }
+      k.st[l * k.sstride + j * k.cs] = w[1] - w[0];
+    }
+}
+
+// FD contributions of one element (gradients.py:84-121 for the element's
+// patch rows): per node l and component j the two perturbed states by
+// rank-one updates of the unperturbed invariants (FdElem) and
+// st[l][j] = vol W+ - vol W-.  The fast path (every state of the configs:
+// det far from 0, |dl c / det0| < 1e-3) is branch-free; other states are
+// flagged and redone by fd_slow_states.  Every state's W equals fd_state_w's
+// (the same operations in the same order).
+template <int DIM, int MODEL, int D>
+__device__ __forceinline__ void fd_element(const double (&vv)[D][DIM + 1], const Elem<DIM> &E,
+                                           const ModelArgs &m, const FdSink &k,
+                                           const unsigned char *stage, int row, const double *nv,
+                                           int CAP, int4 cl, unsigned long long *key) {
+  constexpr int NV = DIM + 1;
+  constexpr bool NH = MODEL == FM_MODEL_NEOHOOKEAN;
+  const FdElem<DIM, MODEL, D> fe(vv, E);
+  const double eps = m.eps, vol = E.vol;
+  const int c[4] = {cl.x, cl.y, cl.z, cl.w};
+  unsigned flags = 0;
+#pragma unroll
+  for (int l = 0; l < NV; ++l)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double vl = nv[j * CAP + c[l]];  // re-read: vv and the gradients die after fe
+      double w[2];
+#pragma unroll
+      for (int sg = 0; sg < 2; ++sg) {
+        const double ve = radd(vl, sg ? eps : -eps);  // the perturbed nodal value
+        const double dl = ve - vl;                     // the step it carries
+        double W;
+        if constexpr (NH) {
+          const double cj = fe.Cc[j][l];
+          const double det = fma(dl, cj, fe.base0);
+          const double I1 = fma(dl, fma(dl, fe.BB[l], fe.A[j][l]), fe.i10);
+          const double x = (dl * cj) * fe.rdet0;
+          if (!(det > FD_DET_NEAR) || !(fabs(x) < 1e-3)) flags |= 1u << (2 * (l * D + j) + sg);
+          const double ld = fe.ld0 + log1p_small(x);
+          const double dm1 = det - 1.0;
+          W = m.C1 * ((I1 - (double)DIM) - 2.0 * ld) + m.D1 * (dm1 * dm1);
+        } else {
+          const double n2 = fmax(fma(dl, fma(dl, fe.BB[l], fe.A[j][l]), fe.base0), 0.0);
+          W = np_scalar_pow(n2, m.e_w) / m.p;
+          if (!isfinite(W)) flags |= 1u << (2 * (l * D + j) + sg);  // non-finite input
+        }
+        w[sg] = rmul(vol, W);
+      }
+      k.st[l * k.sstride + j * k.cs] = w[1] - w[0];
+    }
+  if (flags) fd_slow_states<DIM, MODEL>(flags, stage, row, nv, CAP, cl, m, k, key);
+}
+
 // Position in this CTA's chunk stream: tile t, chunk offset c0.
 template <int CT>
 struct Cursor {
@@ -337,7 +511,12 @@ struct Cursor {
 
 // HV: Hessian-vector product instead of the gradient; b then holds the
 // direction field p (full, zero on the Dirichlet dofs), there is no load term.
-template <int DIM, int MODEL, bool WJ, bool HV, int CT, int NB, int TB, int MINB>
+// FDM: the nodal-patch FD gradient (gradients.py:84-121) instead: every
+// element, computed once by its owner tile, stages for each of its nodes l and
+// components j the difference vol W(v + eps e_lj) - vol W(v - eps e_lj) of its
+// two perturbed states (fd_element); the node sums, the cross-tile exchange
+// and the finishing pass are the gradient's, and g = sum / (2 eps) - b.
+template <int DIM, int MODEL, bool WJ, bool HV, bool FDM, int CT, int NB, int TB, int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, double *__restrict__ bvpart,
@@ -442,6 +621,7 @@ __global__ void __launch_bounds__(CT, MINB)
 
   double jsum = 0.0, bvsum = 0.0;  // vol*W of own elements; b.v of the tile nodes' dofs
   bool bad_any = false;
+  unsigned long long fdkey = ~0ull;  // FDM: smallest offending (sign, j, rank, element) key
   Cursor<CT> comp{(int)blockIdx.x, 0, 0, TileMeta{}};
   comp.load(a);
   if (comp.valid(a)) {
@@ -560,9 +740,18 @@ __global__ void __launch_bounds__(CT, MINB)
 #pragma unroll
             for (int k = 0; k < D; ++k) vv[k][l] = nv[k * CAP + E.loc[l]];
           double F[D][DIM];
-          grad_F_fma<DIM, D>(vv, E.g, F);
+          if (!FDM) grad_F_fma<DIM, D>(vv, E.g, F);
           const bool own = true;
-          if (FM_DBG(mdl) & 1) {  // ablation: no constitutive work
+          if (FDM) {
+            if (has_nodes) {
+              const FdSink sink{st_at(0, tid), (int)L::slot_stride(D), CS, a.closure, a.rank_of,
+                                a.s2o, tm.clo_begin, (int64_t)tm.own_begin + c0 + tid};
+              fd_element<DIM, MODEL, D>(vv, E, mdl, sink, stg(s), tid, nv, CAP,
+                                        make_int4(E.loc[0], E.loc[1], E.loc[2],
+                                                  DIM == 3 ? E.loc[DIM] : 0),
+                                        &fdkey);
+            }
+          } else if (FM_DBG(mdl) & 1) {  // ablation: no constitutive work
 #pragma unroll
             for (int k = 0; k < D; ++k)
 #pragma unroll
@@ -589,7 +778,7 @@ __global__ void __launch_bounds__(CT, MINB)
         }
         // contributions -> staging buffer (separate from the record stages, so
         // the TMA engine never overwrites generic-proxy writes: no proxy fence)
-        if (valid && has_nodes) {
+        if (!FDM && valid && has_nodes) {
 #pragma unroll
           for (int l = 0; l < NV; ++l)
 #pragma unroll
@@ -662,9 +851,19 @@ __global__ void __launch_bounds__(CT, MINB)
       if (my_node) {
         if (cross) {
           // cross entries follow in the finishing pass: dense partial by tile node
+          // (FD: the plain difference sum; the scaling follows the cross entries)
 #pragma unroll
           for (int k = 0; k < D; ++k)
-            a.partial[(int64_t)(tm.node_begin + tid) * D + k] = acc[k] - bj[k];
+            a.partial[(int64_t)(tm.node_begin + tid) * D + k] = FDM ? acc[k] : acc[k] - bj[k];
+        } else if (FDM) {
+          int o = outw;
+          const double inv = 2.0 * mdl.eps;
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            if (fmask & (1 << k)) {
+              const double q = acc[k] / inv;
+              g[o++] = b ? q - bj[k] : q;
+            }
         } else {
           int o = outw;
 #pragma unroll
@@ -679,6 +878,7 @@ __global__ void __launch_bounds__(CT, MINB)
     }
   }
   if (bad_any) atomicOr(status, 1ull);
+  if (FDM && fdkey != ~0ull) atomicMin(status + 1, fdkey);
   if (WJ) {
     const double r = block_sum(jsum, red);
     const double r2 = block_sum(bvsum, red);
@@ -699,13 +899,22 @@ __global__ void __launch_bounds__(CT, MINB)
 // (atomic ticket) sums the tile kernel's per-CTA partials and these in index
 // order: J = sum vol W - (b.v of tile nodes + b.v of fixed nodes).  The result
 // does not depend on which block is last; the ticket is reset for the next call.
-template <int D>
+// FD (FDX): g = (partial + cross entries) / (2 eps) - b of the node (fdx.b at
+// node_desc[tile node].z), as the tile kernel's own nodes.
+struct FdFinish {
+  double inv;            // 2 eps
+  const double *b;       // load (may be null)
+  const int4 *node_desc;
+};
+
+template <int D, bool FDX>
 __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
                                                       const int4 *__restrict__ xdesc,
                                                       const int32_t *__restrict__ xinv,
                                                       const double *__restrict__ xbuf,
                                                       const double *__restrict__ partial,
-                                                      double *__restrict__ g, JFinal jf) {
+                                                      double *__restrict__ g, JFinal jf,
+                                                      FdFinish fdx) {
   // one thread per (node, component): the D threads of a node read adjacent
   // doubles of each exchange slot
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntn * D;
@@ -727,6 +936,10 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
       sum = (((sum + x0) + x1) + x2) + x3;
     }
     for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
+    if (FDX) {
+      const double q = sum / fdx.inv;
+      sum = fdx.b ? q - __ldg(fdx.b + (int64_t)__ldg(&fdx.node_desc[xd.x].z) * D + j) : q;
+    }
     g[xd.w + __popc(mask & ((1 << j) - 1))] = sum;
   }
   if (!jf.out) return;
@@ -771,16 +984,33 @@ int finish_cross_grid(int d, int64_t ntn) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((ntn * d + 255) / 256, finish_max_blocks()));
 }
 
+template <bool FDX>
+static void finish_d(int d, int grid, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
+                     const double *xbuf, const double *partial, double *g, const JFinal &jf,
+                     const FdFinish &fdx, cudaStream_t s) {
+  if (d == 3)
+    k_finish_cross<3, FDX><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf, fdx);
+  else if (d == 2)
+    k_finish_cross<2, FDX><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf, fdx);
+  else
+    k_finish_cross<1, FDX><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf, fdx);
+}
+
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
                                 const double *xbuf, const double *partial, double *g,
                                 const JFinal &jf, cudaStream_t s) {
-  const int grid = finish_cross_grid(d, ntn);
-  if (d == 3)
-    k_finish_cross<3><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
-  else if (d == 2)
-    k_finish_cross<2><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
-  else
-    k_finish_cross<1><<<grid, 256, 0, s>>>(ntn, xdesc, xinv, xbuf, partial, g, jf);
+  finish_d<false>(d, finish_cross_grid(d, ntn), ntn, xdesc, xinv, xbuf, partial, g, jf,
+                  FdFinish{0.0, nullptr, nullptr}, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish_cross_fd(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
+                                   const double *xbuf, const double *partial, double *g,
+                                   double eps, const double *b, const int4 *node_desc,
+                                   cudaStream_t s) {
+  JFinal jf{};
+  finish_d<true>(d, finish_cross_grid(d, ntn), ntn, xdesc, xinv, xbuf, partial, g, jf,
+                 FdFinish{2.0 * eps, b, node_desc}, s);
   return cudaGetLastError();
 }
 
@@ -798,12 +1028,13 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, int mode, const doubl
                               const double *b, double *g, double *jpart, double *bvpart,
                               unsigned long long *status, const ModelArgs &m, cudaStream_t s) {
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
-  constexpr int MINB = tile_exact_minb(DIM, CT);
+  constexpr int MINB = tile_exact_minb(DIM, CT), MINBF = tile_fd_minb(DIM, CT, MODEL);
   const size_t smem =
       PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB, mode == 2 ? 2 * D : D);
-  auto k = mode == 2   ? k_tile_exact<DIM, MODEL, false, true, CT, NB, TB, MINB>
-           : mode == 1 ? k_tile_exact<DIM, MODEL, true, false, CT, NB, TB, MINB>
-                       : k_tile_exact<DIM, MODEL, false, false, CT, NB, TB, MINB>;
+  auto k = mode == 3   ? k_tile_exact<DIM, MODEL, false, false, true, CT, NB, TB, MINBF>
+           : mode == 2 ? k_tile_exact<DIM, MODEL, false, true, false, CT, NB, TB, MINB>
+           : mode == 1 ? k_tile_exact<DIM, MODEL, true, false, false, CT, NB, TB, MINB>
+                       : k_tile_exact<DIM, MODEL, false, false, false, CT, NB, TB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, bvpart, status, m);
   return cudaGetLastError();

@@ -1,5 +1,6 @@
 // Energy-only streaming kernel, the descent update and the row-batch model
-// plugin (the nodal-patch finite-difference kernel is in fm_eval_fd.cu).
+// plugin (the nodal-patch finite-difference gradient is the fused tile kernel's
+// FD mode, fm_eval_exact.cu).
 // F, det, I1, W follow the reference's rounding order exactly through the
 // explicit round-to-nearest forms of fm_density.cuh (assembly.py:35-49,
 // models.py:59-126); only the libm ulps of log/pow differ from numpy.

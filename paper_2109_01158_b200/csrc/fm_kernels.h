@@ -11,7 +11,8 @@ namespace fm {
 // persistent pipelined fused J + exact gradient; grid = ctas_per_sm * #SMs, CONSUMERS threads
 // ct = threads per CTA = chunk size = max tile nodes (128 or 256); nb = node-value buffers
 // tb = table buffers (2: the next tile's descriptors / entries load a tile ahead)
-// mode 0: gradient, 1: gradient + J, 2: Hessian-vector product (b = direction)
+// mode 0: gradient, 1: gradient + J, 2: Hessian-vector product (b = direction),
+// 3: nodal-patch FD gradient (m.eps; g = sum / (2 eps) - b, partials unscaled)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
                               int ns, int mode, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,
@@ -22,6 +23,13 @@ cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, i
 // (measured: 3 CTAs 0.865 ms, 4 CTAs 0.799 ms, 5 CTAs (spills) 0.862 ms at cfg2)
 constexpr int tile_exact_minb(int dim, int ct) {
   return dim == 2 ? (ct == 128 ? 8 : 4) : (ct == 128 ? 4 : 2);
+}
+// the FD mode (mode 3) of the 2D Neo-Hookean kernel: 3 x 256 threads (<= 85
+// registers; its per-element state loop spills at 64: cfg3 FD 0.222 ms at 3
+// CTAs); p-Laplace keeps 4 (cfg2 0.94 ms at 4, 0.99 at 3)
+constexpr int tile_fd_minb(int dim, int ct, int model) {
+  return dim == 2 && model == FM_MODEL_NEOHOOKEAN ? (ct == 128 ? 6 : 3)
+                                                  : tile_exact_minb(dim, ct);
 }
 
 // J finalisation carried by the finishing pass (see k_finish_cross)
@@ -41,14 +49,14 @@ int finish_cross_grid(int d, int64_t ntn);
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
                                 const double *xbuf, const double *partial, double *g,
                                 const JFinal &jf, cudaStream_t s);
+// the FD gradient's finishing pass: g = (partial + cross entries) / (2 eps) - b
+cudaError_t launch_finish_cross_fd(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
+                                   const double *xbuf, const double *partial, double *g,
+                                   double eps, const double *b, const int4 *node_desc,
+                                   cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
                        int dn = 0);
 
-cudaError_t launch_tile_fd(int dim, int model, const TileArgs &a, int n_tiles, int ct, int ech,
-                           const double *v, const double *b, double eps, double *g,
-                           unsigned long long *badkey, const ModelArgs &m, cudaStream_t s);
-// shared memory of the FD tile kernel (ech = max node entries of one chunk)
-size_t tile_fd_smem(int dim, int model, int clo_cap, int ech, int ct);
 
 cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, int nblocks,
                           const double *v, double *part, double *dens, const ModelArgs &m,

@@ -23,5 +23,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
   > gpurun_out/${tag}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tile_exact|k_finish_cross" \
   -s 2 -c 2 -o gpurun_out/${tag}_exact python tools/exact_once.py cfg4 3 > gpurun_out/${tag}_ncu_exact.log 2>&1; echo "ncu exact rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tile_fd \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tile_exact<3, 1, 0, 0, 1" \
   -s 1 -c 1 -o gpurun_out/${tag}_fd python tools/fd_once.py cfg4 2 > gpurun_out/${tag}_ncu_fd.log 2>&1; echo "ncu fd rc=$?"

@@ -7,8 +7,8 @@ lib/libfemmin_b200.so, any other name lib/libfemmin_<name>.so (built here
 beforehand with paper_2109_01158_b200.build.build_variant).  Every variant runs
 in its own process: the fused J + exact gradient is timed (CUDA events, 50
 evaluations after warm-up, whole evaluation and the tile kernel alone) and
-checked bitwise against the first variant's gradient when the results are
-meant to agree (``--same``)."""
+compared with the first variant's gradient.  ``--op fd`` times the FD
+gradient instead (eps 1e-8, 1e-6 for scalar fields)."""
 import argparse
 import os
 import subprocess
@@ -22,8 +22,15 @@ from paper_2109_01158_b200 import problems
 pr = problems.CONFIGS[%r]()
 g = torch.empty(pr.dm.nfree_dofs, dtype=torch.float64, device="cuda")
 J = torch.empty(3, dtype=torch.float64, device="cuda")
+OP = %r
+EPS = 1e-6 if pr.dm.d == 1 else 1e-8
+def run():
+    if OP == "fd":
+        pr.dm.numeric_gradient(pr.v, pr.model, pr.b, EPS, g=g)
+    else:
+        pr.dm.exact_gradient(pr.v, pr.model, pr.b, g=g, J=J)
 for _ in range(5):
-    pr.dm.exact_gradient(pr.v, pr.model, pr.b, g=g, J=J)
+    run()
 pr.dm.check()
 torch.cuda.synchronize()
 n = %d
@@ -34,7 +41,7 @@ A, Z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 A.record()
 for a, z in ev:
     pr.dm.time_next(a, z)
-    pr.dm.exact_gradient(pr.v, pr.model, pr.b, g=g, J=J)
+    run()
 Z.record()
 torch.cuda.synchronize()
 kern = sorted(a.elapsed_time(z) for a, z in ev)[n // 2]
@@ -49,6 +56,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--n", type=int, default=50)
+    ap.add_argument("--op", default="exact", choices=["exact", "fd"])
     ap.add_argument("variants", nargs="+")
     args = ap.parse_args()
     import json
@@ -64,7 +72,7 @@ def main():
             a, b = kv.split("=", 1)
             env[a] = b
         tag = str(k)
-        code = CHILD % (ROOT, args.config, args.n, tag)
+        code = CHILD % (ROOT, args.config, args.op, args.n if args.op == "exact" else 10, tag)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         if r.returncode:
             print(f"{spec}: FAILED {r.stderr[-400:]}", flush=True)
