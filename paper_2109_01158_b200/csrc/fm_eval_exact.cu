@@ -370,7 +370,7 @@ struct FdSink {
 };
 
 // The FD states of one element that the fast path left (det near 0, or
-// |dl c / det0| >= 1e-3): both signs of every flagged (l, j) recomputed with
+// |dl c / det0| >= 1e-4): both signs of every flagged (l, j) recomputed with
 // the full rule of fd_state_w (the reference's own evaluation near det 0),
 // the difference restaged; non-finite states latch their key.  Out of line
 // and rare (flags: bit 2 (l D + j) + sg).
@@ -438,9 +438,8 @@ __device__ __noinline__ void fd_slow_states(unsigned flags, const unsigned char 
 // patch rows): per node l and component j the two perturbed states by
 // rank-one updates of the unperturbed invariants (FdElem) and
 // st[l][j] = vol W+ - vol W-.  The fast path (every state of the configs:
-// det far from 0, |dl c / det0| < 1e-3) is branch-free; other states are
-// flagged and redone by fd_slow_states.  Every state's W equals fd_state_w's
-// (the same operations in the same order).
+// det far from 0, |dl c / det0| < 1e-4) is branch-free; other states are
+// flagged and redone by fd_slow_states with the full rule of fd_state_w.
 template <int DIM, int MODEL, int D>
 __device__ __forceinline__ void fd_element(const double (&vv)[D][DIM + 1], const Elem<DIM> &E,
                                            const ModelArgs &m, const FdSink &k,
@@ -457,6 +456,8 @@ __device__ __forceinline__ void fd_element(const double (&vv)[D][DIM + 1], const
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const double vl = nv[j * CAP + c[l]];  // re-read: vv and the gradients die after fe
+      double cr = 0.0;                        // c_jl / det0
+      if constexpr (NH) cr = fe.Cc[j][l] * fe.rdet0;
       double w[2];
 #pragma unroll
       for (int sg = 0; sg < 2; ++sg) {
@@ -464,12 +465,13 @@ __device__ __forceinline__ void fd_element(const double (&vv)[D][DIM + 1], const
         const double dl = ve - vl;                     // the step it carries
         double W;
         if constexpr (NH) {
-          const double cj = fe.Cc[j][l];
-          const double det = fma(dl, cj, fe.base0);
+          const double det = fma(dl, fe.Cc[j][l], fe.base0);
           const double I1 = fma(dl, fma(dl, fe.BB[l], fe.A[j][l]), fe.i10);
-          const double x = (dl * cj) * fe.rdet0;
-          if (!(det > FD_DET_NEAR) || !(fabs(x) < 1e-3)) flags |= 1u << (2 * (l * D + j) + sg);
-          const double ld = fe.ld0 + log1p_small(x);
+          const double x = dl * cr;
+          // |x| < 1e-4 (dl ~ eps |v|: every state of the configs): log1p to x^4
+          // (truncation x^4 / 5 < 2e-17 relative); otherwise the slow path
+          if (!(det > FD_DET_NEAR) || !(fabs(x) < 1e-4)) flags |= 1u << (2 * (l * D + j) + sg);
+          const double ld = fe.ld0 + x * fma(x, fma(x, fma(x, -0.25, 1.0 / 3.0), -0.5), 1.0);
           const double dm1 = det - 1.0;
           W = m.C1 * ((I1 - (double)DIM) - 2.0 * ld) + m.D1 * (dm1 * dm1);
         } else {
