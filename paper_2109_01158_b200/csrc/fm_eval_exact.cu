@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(CT, MINB)
         outw = nd.w;
         fmask = desc_mask(nd);
         cross = ((unsigned)nd.x & CROSS_FLAG) != 0;
-        if (b && !HV) {
+        if (b && !HV && !FDM) {  // FD: loaded at the tile end (not live through the tile)
 #pragma unroll
           for (int k = 0; k < D; ++k) bj[k] = __ldg(b + (int64_t)nd.z * D + k);
         }
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(CT, MINB)
           for (int k = 0; k < D; ++k)
             if (fmask & (1 << k)) {
               const double q = acc[k] / inv;
-              g[o++] = b ? q - bj[k] : q;
+              g[o++] = b ? q - __ldg(b + (int64_t)nd.z * D + k) : q;
             }
         } else {
           int o = outw;
