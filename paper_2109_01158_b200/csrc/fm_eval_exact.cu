@@ -519,12 +519,18 @@ struct Cursor {
 
 // HV: Hessian-vector product instead of the gradient; b then holds the
 // direction field p (full, zero on the Dirichlet dofs), there is no load term.
+// EO: the energy alone (assembly.py:94-106) with WJ: each element's density in
+// the reference's operation order (einsum F, the RN density of fm_density.cuh,
+// bit for bit k_energy's values), optionally written to g as the per-element
+// densities (reference element order); no staging, node sums or exchange, one
+// barrier per chunk.
 // FDM: the nodal-patch FD gradient (gradients.py:84-121) instead: every
 // element, computed once by its owner tile, stages for each of its nodes l and
 // components j the difference vol W(v + eps e_lj) - vol W(v - eps e_lj) of its
 // two perturbed states (fd_element); the node sums, the cross-tile exchange
 // and the finishing pass are the gradient's, and g = sum / (2 eps) - b.
-template <int DIM, int MODEL, bool WJ, bool HV, bool FDM, int CT, int NB, int TB, int MINB>
+template <int DIM, int MODEL, bool WJ, bool HV, bool FDM, bool EO, int CT, int NB, int TB,
+          int MINB>
 __global__ void __launch_bounds__(CT, MINB)
     k_tile_exact(TileArgs a, const double *__restrict__ v, const double *__restrict__ b,
                  double *__restrict__ g, double *__restrict__ jpart, double *__restrict__ bvpart,
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(CT, MINB)
           xe = xch[c0 / CT + 1];
         }
         int xkey0 = 0;
-        if (xb + tid < xe) xkey0 = __ldg(a.xkey + xb + tid);
+        if (!EO && xb + tid < xe) xkey0 = __ldg(a.xkey + xb + tid);
         TRACE(0);
         mbar_wait(full + s, (q >> 1) & 1);
         TRACE(1);
@@ -748,9 +754,14 @@ __global__ void __launch_bounds__(CT, MINB)
 #pragma unroll
             for (int k = 0; k < D; ++k) vv[k][l] = nv[k * CAP + E.loc[l]];
           double F[D][DIM];
-          if (!FDM) grad_F_fma<DIM, D>(vv, E.g, F);
+          if (!FDM && !EO) grad_F_fma<DIM, D>(vv, E.g, F);
           const bool own = true;
-          if (FDM) {
+          if (EO) {
+            grad_F<DIM, D>(vv, E.g, F);
+            const double W = density<DIM, MODEL>(F, mdl);
+            if (g) g[__ldg(a.s2o + (int64_t)tm.own_begin + e)] = W;
+            jsum += E.vol * W;
+          } else if (FDM) {
             if (has_nodes) {
               const FdSink sink{st_at(0, tid), (int)L::slot_stride(D), CS, a.closure, a.rank_of,
                                 a.s2o, tm.clo_begin, (int64_t)tm.own_begin + c0 + tid};
@@ -786,7 +797,7 @@ __global__ void __launch_bounds__(CT, MINB)
         }
         // contributions -> staging buffer (separate from the record stages, so
         // the TMA engine never overwrites generic-proxy writes: no proxy fence)
-        if (!FDM && valid && has_nodes) {
+        if (!FDM && !EO && valid && has_nodes) {
 #pragma unroll
           for (int l = 0; l < NV; ++l)
 #pragma unroll
@@ -805,7 +816,7 @@ __global__ void __launch_bounds__(CT, MINB)
         __syncthreads();  // contributions staged; every record of stage s read
         TRACE(3);
         // stage s is free: records of chunk q + 2
-        if (my_node && !(FM_DBG(mdl) & 2)) {
+        if (!EO && my_node && !(FM_DBG(mdl) & 2)) {
           // this node's entries of the chunk (its slice of the chunk's entry
           // block): the loads of two entries are issued together; the order
           // (ascending tile element) is the fixed summation order
@@ -836,7 +847,7 @@ __global__ void __launch_bounds__(CT, MINB)
             }
           }
         }
-        for (int i = xb + tid; i < xe; i += CT) {
+        for (int i = xb + tid; !EO && i < xe; i += CT) {
           const int key = i == xb + tid ? xkey0 : (int)__ldg(a.xkey + i);
           const int64_t pos = i;  // item i -> exchange slot i (coalesced stores)
           const double *sp = st_at(key & 3, (key >> 2) - c0);
@@ -847,7 +858,7 @@ __global__ void __launch_bounds__(CT, MINB)
         // it; two: the next chunk's barrier already orders this consumption
         // before the write two chunks ahead
         TRACE(4);
-        __syncthreads();  // stage s consumed: records of chunk q + 2
+        if (!EO) __syncthreads();  // stage s consumed: records of chunk q + 2 (EO: barrier 1)
         TRACE(5);
         issue_records(iss, s);
         iss.advance(a);
@@ -856,7 +867,7 @@ __global__ void __launch_bounds__(CT, MINB)
 #pragma unroll
         for (int k = 0; k < D; ++k) bvsum += bj[k] * nv[k * CAP + cl];
       }
-      if (my_node) {
+      if (my_node && !EO) {
         if (cross) {
           // cross entries follow in the finishing pass: dense partial by tile node
           // (FD: the plain difference sum; the scaling follows the cross entries)
@@ -1007,7 +1018,11 @@ static void finish_d(int d, int grid, int64_t ntn, const int4 *xdesc, const int3
 cudaError_t launch_finish_cross(int d, int64_t ntn, const int4 *xdesc, const int32_t *xinv,
                                 const double *xbuf, const double *partial, double *g,
                                 const JFinal &jf, cudaStream_t s) {
-  finish_d<false>(d, finish_cross_grid(d, ntn), ntn, xdesc, xinv, xbuf, partial, g, jf,
+  // enough blocks for the cross nodes and for the b.v of the fixed nodes
+  int grid = finish_cross_grid(d, ntn);
+  if (jf.out && jf.b)
+    grid = std::max<int>(grid, (int)std::min<int64_t>((jf.nfixed + 255) / 256, finish_max_blocks()));
+  finish_d<false>(d, grid, ntn, xdesc, xinv, xbuf, partial, g, jf,
                   FdFinish{0.0, nullptr, nullptr}, s);
   return cudaGetLastError();
 }
@@ -1039,10 +1054,11 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, int mode, const doubl
   constexpr int MINB = tile_exact_minb(DIM, CT), MINBF = tile_fd_minb(DIM, CT, MODEL);
   const size_t smem =
       PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB, mode == 2 ? 2 * D : D);
-  auto k = mode == 3   ? k_tile_exact<DIM, MODEL, false, false, true, CT, NB, TB, MINBF>
-           : mode == 2 ? k_tile_exact<DIM, MODEL, false, true, false, CT, NB, TB, MINB>
-           : mode == 1 ? k_tile_exact<DIM, MODEL, true, false, false, CT, NB, TB, MINB>
-                       : k_tile_exact<DIM, MODEL, false, false, false, CT, NB, TB, MINB>;
+  auto k = mode == 4   ? k_tile_exact<DIM, MODEL, true, false, false, true, CT, NB, TB, MINB>
+           : mode == 3 ? k_tile_exact<DIM, MODEL, false, false, true, false, CT, NB, TB, MINBF>
+           : mode == 2 ? k_tile_exact<DIM, MODEL, false, true, false, false, CT, NB, TB, MINB>
+           : mode == 1 ? k_tile_exact<DIM, MODEL, true, false, false, false, CT, NB, TB, MINB>
+                       : k_tile_exact<DIM, MODEL, false, false, false, false, CT, NB, TB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, CT, smem, s>>>(a, v, b, g, jpart, bvpart, status, m);
   return cudaGetLastError();

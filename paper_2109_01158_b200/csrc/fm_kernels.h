@@ -12,7 +12,8 @@ namespace fm {
 // ct = threads per CTA = chunk size = max tile nodes (128 or 256); nb = node-value buffers
 // tb = table buffers (2: the next tile's descriptors / entries load a tile ahead)
 // mode 0: gradient, 1: gradient + J, 2: Hessian-vector product (b = direction),
-// 3: nodal-patch FD gradient (m.eps; g = sum / (2 eps) - b, partials unscaled)
+// 3: nodal-patch FD gradient (m.eps; g = sum / (2 eps) - b, partials unscaled),
+// 4: energy only (J partials; g = per-element densities or null)
 cudaError_t launch_tile_exact(int dim, int model, const TileArgs &a, int grid, int ct, int nb,
                               int ns, int mode, const double *v, const double *b, double *g,
                               double *jpart, double *bvpart, unsigned long long *status,

@@ -27,6 +27,9 @@ EPS = 1e-6 if pr.dm.d == 1 else 1e-8
 def run():
     if OP == "fd":
         pr.dm.numeric_gradient(pr.v, pr.model, pr.b, EPS, g=g)
+    elif OP == "energy":
+        pr.dm.energy(pr.v, pr.model, pr.b, out=J)
+        g[:3] = J
     else:
         pr.dm.exact_gradient(pr.v, pr.model, pr.b, g=g, J=J)
 for _ in range(5):
@@ -56,7 +59,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--n", type=int, default=50)
-    ap.add_argument("--op", default="exact", choices=["exact", "fd"])
+    ap.add_argument("--op", default="exact", choices=["exact", "fd", "energy"])
     ap.add_argument("variants", nargs="+")
     args = ap.parse_args()
     import json
@@ -72,7 +75,7 @@ def main():
             a, b = kv.split("=", 1)
             env[a] = b
         tag = str(k)
-        code = CHILD % (ROOT, args.config, args.op, args.n if args.op == "exact" else 10, tag)
+        code = CHILD % (ROOT, args.config, args.op, args.n if args.op != "fd" else 10, tag)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         if r.returncode:
             print(f"{spec}: FAILED {r.stderr[-400:]}", flush=True)
