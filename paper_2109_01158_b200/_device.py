@@ -71,7 +71,7 @@ def _copy_threads():
     global _POOL
     if _POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+        _POOL = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
     return _POOL
 
 
@@ -95,9 +95,23 @@ def to_dev(a, dtype=None) -> torch.Tensor:
     if arr.nbytes < _PINNED_MIN or arr.ndim == 0:
         return torch.from_numpy(arr).to("cuda", non_blocking=False).contiguous()
     pin = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0]).dtype, pin_memory=True)
-    _par_copyto(pin.numpy().reshape(arr.shape[0], -1), arr.reshape(arr.shape[0], -1))
-    # the caching host allocator keeps `pin` until this copy has completed
-    return pin.to("cuda", non_blocking=True)
+    out = torch.empty(arr.shape, dtype=pin.dtype, device="cuda")
+    # pipelined: the host threads copy consecutive pieces into the pinned
+    # buffer while the DMA engine uploads the pieces already copied (the
+    # copies take longer than the DMA: cfg4 field 3 + 1.9 ms serial)
+    src = arr.reshape(arr.shape[0], -1)
+    dst, dev = pin.numpy().reshape(arr.shape[0], -1), out.view(arr.shape[0], -1)
+    n, pieces = src.shape[0], 4 * _copy_threads()._max_workers
+    cuts = [n * i // pieces for i in range(pieces + 1)]
+    futs = [_copy_threads().submit(np.copyto, dst[cuts[i]:cuts[i + 1]], src[cuts[i]:cuts[i + 1]])
+            for i in range(pieces)]
+    pin_rows = pin.view(arr.shape[0], -1)
+    for i, f in enumerate(futs):
+        f.result()
+        if cuts[i + 1] > cuts[i]:
+            # the caching host allocator keeps `pin` until this copy has completed
+            dev[cuts[i]:cuts[i + 1]].copy_(pin_rows[cuts[i]:cuts[i + 1]], non_blocking=True)
+    return out
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
