@@ -215,14 +215,14 @@ __device__ __forceinline__ double np_scalar_pow(double x, double e) {
 // Tile tables (built by fm_ctx_create).
 struct TileArgs {
   const uint8_t *aos;
-  const int4 *conn4;           // global node ids per element (storage order)
+  const int4 *conn4;           // global node ids per element (storage order; 2D only)
   const int32_t *s2o;          // storage -> reference element id
   const TileMeta *meta;        // n_tiles_all
-  const int32_t *halo_ids;     // storage index of halo elements
-  const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements
+  const int32_t *halo_ids;     // storage index of halo elements (build only; null at run time)
+  const uint2 *halo_loc;       // closure indices (u16 x 4) of halo elements (build only)
   const uint2 *loc;            // closure indices (u16 x 4) w.r.t. the owner tile, storage order
   const int32_t *closure;      // node ids of the tile closures
-  const uint8_t *flags;        // owned-slot mask per tile element (own then halo)
+  const uint8_t *flags;        // owned-slot mask per tile element (build only)
   const int4 *node_desc;       // {entry_off | chunk counts, chunk counts, node id,
                                //  out offset} (see chunk_count, desc_mask)
   const uint16_t *entries;     // te_local << 2 | slot, sorted by te_local per node
@@ -244,9 +244,6 @@ struct TileArgs {
   int entry_cap;               // max entries of one tile, rounded up to 8
   int blk_cap;                 // max chunk entry block, u16 units
   int clo_cap;                 // max closure size, rounded up to 4
-  // FD items (built on the first FD call): per tile and chunk, at the chunk
-  // block's index range, the chunk's entries in ROW-major order, each
-  // p << 16 | row << 2 | slot with p its node-major position (stg slot)
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
