@@ -149,3 +149,22 @@ def test_ranks_of_stacks_reproduce_single_domain(tmp_path):
         idx = np.array([pos[int(x)] for x in z["gdof"]])
         assert np.abs(z["g"] - gg[idx]).max() / scale < 1e-13
         assert abs(z["J"][0] - Jg[0]) / abs(Jg[0]) < 1e-13
+
+
+def test_stack_mid_size_matches_single_domain():
+    """A 96x48x48 beam (1.3 M tets, many tiles per sub-slab) as 4 sub-slabs."""
+    from paper_2109_01158_b200 import problems
+    from paper_2109_01158_b200.parallel import SlabStack
+    nx, ny, nz = 96, 48, 48
+    pr = problems.beam(nx, ny, nz, seed=7, keep=True)
+    J = torch.empty(3, dtype=torch.float64, device="cuda")
+    gg = pr.dm.exact_gradient(pr.v, pr.model, pr.b, J=J).cpu().numpy()
+    Jg = J.cpu().numpy().copy()
+    pos = {int(d): k for k, d in enumerate(pr.meta["dofs_minim"].cpu().numpy())}
+    del pr
+    st = SlabStack(nx, ny, nz, 0, nx, 4, seed=7)
+    g = st.exact_gradient(st.V, st.model, st.B, J=J).cpu().numpy()
+    st.check()
+    idx = np.array([pos[int(x)] for x in _stack_gdofs(st)])
+    assert np.abs(g - gg[idx]).max() / np.abs(gg).max() < 1e-13
+    assert abs(J.cpu().numpy()[0] - Jg[0]) / abs(Jg[0]) < 1e-13

@@ -13,6 +13,7 @@ CFGS="cfg1 cfg2 cfg2_p1.8 cfg3" bash tools/cfgs.sh > gpurun_out/${tag}_cfgs.log 
 timeout 300 python tools/fd_time.py cfg1 cfg2 cfg2_p1.8 cfg3 cfg4 > gpurun_out/${tag}_fd.log 2>&1
 timeout 300 python tools/tr_time.py cfg4 10 > gpurun_out/${tag}_tr.log 2>&1
 timeout 900 python bench.py --config cfg5 --shard 1/8 --steps 20 --warmup 3 --extras --no-cpu-baseline > gpurun_out/${tag}_cfg5_8.log 2>&1; echo "cfg5/8 rc=$?"
+timeout 900 python bench.py --config cfg5 --shard 2/4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_cfg5_4.log 2>&1; echo "cfg5/4 rc=$?"
 timeout 1200 python bench.py --config cfg5 --shard 0/2 --steps 10 --warmup 3 --extras --descent-iters 20 --no-cpu-baseline > gpurun_out/${tag}_cfg5_2.log 2>&1; echo "cfg5/2 rc=$?"
 timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/${tag}_ref.log 2>&1; echo "ref rc=$?"
 # ncu: launch list of a short bench run (evaluation kernels only), then the
