@@ -944,17 +944,21 @@ __global__ void __launch_bounds__(256) k_finish_cross(int64_t ntn,
     const int mask = xd.z >> 16, lo = xd.y, hi = lo + (xd.z & 0xffff);
     if (!(mask & (1 << j))) continue;
     double sum = partial[(int64_t)xd.x * D + j];
-    // four entries per step: their slot loads, then their value loads, are
-    // issued back to back; the sum stays sequential in entry order
-    int p = lo;
-    for (; p + 4 <= hi; p += 4) {
-      const int s0 = __ldg(xinv + p), s1 = __ldg(xinv + p + 1), s2 = __ldg(xinv + p + 2),
-                s3 = __ldg(xinv + p + 3);
-      const double x0 = __ldg(xbuf + (int64_t)s0 * D + j), x1 = __ldg(xbuf + (int64_t)s1 * D + j),
-                   x2 = __ldg(xbuf + (int64_t)s2 * D + j), x3 = __ldg(xbuf + (int64_t)s3 * D + j);
-      sum = (((sum + x0) + x1) + x2) + x3;
+    // four entries per step (the last step predicated): their slot loads,
+    // then their value loads, are issued back to back; the sum stays
+    // sequential in entry order
+    constexpr int U = 4;  // 8: cfg4 finishing pass 1 % slower
+    for (int p = lo; p < hi; p += U) {
+      int sl[U];
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) sl[u] = p + u < hi ? __ldg(xinv + p + u) : -1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = sl[u] >= 0 ? __ldg(xbuf + (int64_t)sl[u] * D + j) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (p + u < hi) sum += x[u];
     }
-    for (; p < hi; ++p) sum += __ldg(xbuf + (int64_t)__ldg(xinv + p) * D + j);
     if (FDX) {
       const double q = sum / fdx.inv;
       sum = fdx.b ? q - __ldg(fdx.b + (int64_t)__ldg(&fdx.node_desc[xd.x].z) * D + j) : q;
