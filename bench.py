@@ -275,7 +275,7 @@ def main():
                     help="--impl reference: host processes (default: all cores)")
     ap.add_argument("--max-context-elems", type=int, default=1 << 28,
                     help="beams: a rank slab with more tets is held as sub-slab contexts")
-    ap.add_argument("--sub-elems", type=int, default=50_000_000,
+    ap.add_argument("--sub-elems", type=int, default=140_000_000,
                     help="beams: max tets per sub-slab context when a slab is split")
     ap.add_argument("--shard", type=str, default="",
                     help="r/w: run rank r's x1-slab of a w-way partition on this one GPU")

@@ -176,6 +176,29 @@ def stack_parts(ne: int, max_elems: int) -> int:
     return max(1, -(-int(ne) // int(max_elems)))
 
 
+def stack_ranges(ix0: int, ix1: int, parts: int) -> list[tuple[int, int]]:
+    """Cube ranges of the sub-slabs of [ix0, ix1): near-equal, each sized so
+    that its free node layers fill whole tile boxes along x1 (8 layers: n + 1
+    layers for n cubes, n for the slab at x1 = 0 whose first layer is
+    Dirichlet) — a leftover layer of thin tiles costs 5 % (cfg5 2-way share:
+    30.8 ms with 85 / 86-cube sub-slabs, 32.4 ms with 80 / 88).  The last
+    sub-slab takes the remainder."""
+    nxl = ix1 - ix0
+    parts = max(1, min(int(parts), nxl))
+    if nxl < 16 * parts:  # small slabs: an even split
+        return [(ix0 + nxl * k // parts, ix0 + nxl * (k + 1) // parts) for k in range(parts)]
+    cuts, a = [ix0], ix0
+    for k in range(parts - 1):
+        want = ix0 + round(nxl * (k + 1) / parts) - a
+        r = 0 if a == 0 else 7  # cubes mod 8 that fill whole boxes
+        n = max(1, want + ((r - want) % 8 if (r - want) % 8 <= 4 else (r - want) % 8 - 8))
+        n = min(n, ix1 - a - (parts - 1 - k))  # leave at least a cube per later part
+        a += n
+        cuts.append(a)
+    cuts.append(ix1)
+    return [(cuts[k], cuts[k + 1]) for k in range(parts)]
+
+
 class SlabStack:
     """A rank's x1-slab [ix0, ix1) of the Kuhn beam held as K sub-slab
     evaluation contexts on ONE GPU, for slabs too large for one context
@@ -204,8 +227,7 @@ class SlabStack:
         self.nx, self.ny, self.nz, self.ix0, self.ix1 = nx, ny, nz, ix0, ix1
         nxl = ix1 - ix0
         parts = max(1, min(int(parts), nxl))
-        self.ranges = [(ix0 + nxl * k // parts, ix0 + nxl * (k + 1) // parts)
-                       for k in range(parts)]
+        self.ranges = stack_ranges(ix0, ix1, parts)
         d = 3
         self.dim, self.d = 3, d
         nn_k = [(z - a + 1) * (ny + 1) * (nz + 1) for a, z in self.ranges]

@@ -90,3 +90,19 @@ def test_slab_oracle_mesh_is_a_restriction():
                       for cx in range(4, 9)])
     gel = (6 * cubes[:, None] + np.arange(6)[None]).ravel()
     np.testing.assert_array_equal(gid[s.elems2nodes], m.elems2nodes[gel])
+
+
+def test_stack_ranges_cover_and_fill_boxes():
+    """Sub-slab cuts (parallel.stack_ranges): contiguous, covering, near
+    equal; large sub-slabs fill whole 8-layer tile boxes except the last."""
+    from paper_2109_01158_b200.parallel import stack_ranges
+    for ix0, ix1, k in [(0, 512, 6), (512, 1024, 6), (0, 512, 17), (256, 512, 4),
+                        (0, 24, 3), (12, 24, 2), (0, 24, 5), (0, 8, 3), (3, 4, 1)]:
+        r = stack_ranges(ix0, ix1, k)
+        assert len(r) == min(k, ix1 - ix0) and r[0][0] == ix0 and r[-1][1] == ix1
+        assert all(a < z for a, z in r) and all(r[i][1] == r[i + 1][0] for i in range(len(r) - 1))
+        n = [z - a for a, z in r]
+        assert max(n) - min(n) <= max(12, (ix1 - ix0) // k // 4)
+        if ix1 - ix0 >= 16 * k:
+            for a, z in r[:-1]:
+                assert ((z - a) + (0 if a == 0 else 1)) % 8 == 0
