@@ -180,9 +180,10 @@ def stack_ranges(ix0: int, ix1: int, parts: int) -> list[tuple[int, int]]:
     """Cube ranges of the sub-slabs of [ix0, ix1): near-equal, each sized so
     that its free node layers fill whole tile boxes along x1 (8 layers: n + 1
     layers for n cubes, n for the slab at x1 = 0 whose first layer is
-    Dirichlet) — a leftover layer of thin tiles costs 5 % (cfg5 2-way share:
-    30.8 ms with 85 / 86-cube sub-slabs, 32.4 ms with 80 / 88).  The last
-    sub-slab takes the remainder."""
+    Dirichlet); the last sub-slab takes the remainder.  Measured on the cfg5
+    2-way share (6 sub-slabs): 30.7 ms with these cuts, 30.8 ms with an even
+    split into 85 / 86 cubes, 32.4 ms with cuts on multiples of 8 cubes (a
+    single leftover node layer per sub-slab)."""
     nxl = ix1 - ix0
     parts = max(1, min(int(parts), nxl))
     if nxl < 16 * parts:  # small slabs: an even split
