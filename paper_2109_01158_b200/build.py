@@ -29,6 +29,7 @@ UNITS = {
     "fm_prep.cu": [],
     "fm_ctx.cu": [],
     "fm_eval_exact.cu": [],
+    "fm_eval_ws.cu": [],
     "fm_eval_ref.cu": [],
     "fm_hessian.cu": [],
     "fm_cg.cu": [],

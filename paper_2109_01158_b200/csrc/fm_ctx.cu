@@ -1523,6 +1523,15 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
     if (best < 0) {
       return capacity("tile tables exceed shared memory");
     }
+#if FM_WS_KERNEL
+    // experiment builds only (tools/ws_check.sh): the warp-specialised kernel of
+    // fm_eval_ws.cu (one 896-thread CTA per SM) for FM_WS=1, 256-node tiles
+    // whose stages fit the SM's shared memory
+    c->ws = false;
+    if (const char *e = getenv("FM_WS")) c->ws = atoi(e) != 0;
+    if (c->tile_nodes != 256 || tile_ws_smem(dim, d, c->blk_cap, c->clo_cap) == 0)
+      c->ws = false;
+#endif
   }
 
   // build-only tables: the kernels read the chunk entry blocks instead of the
@@ -1690,12 +1699,19 @@ int fm_grad_exact(fm_ctx *c, const fm_model *model, const double *v, const doubl
   const bool wj = J_out != nullptr;
   TileArgs ta = c->tile_args();
   if (!wj) ta.n_tiles_all = c->n_tiles;  // J-only orphan tiles not needed
-  const int grid = std::min(c->n_sm * c->ctas_per_sm, std::max(1, ta.n_tiles_all));
+  const int grid =
+      std::min(c->n_sm * (c->ws ? 1 : c->ctas_per_sm), std::max(1, ta.n_tiles_all));
   if (ta.n_tiles_all > 0) {
     TimedLaunch tl(c, s);
-    FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
-                              c->table_bufs, wj ? 1 : 0, v, b, g, c->jpart, c->dotpart,
-                              c->status, ma, s));
+#if FM_WS_KERNEL
+    if (c->ws)
+      FM_CUDA(launch_tile_ws(c->dim, model->kind, ta, grid, wj, v, b, g, c->jpart, c->dotpart,
+                             c->status, ma, s));
+    else
+#endif
+      FM_CUDA(launch_tile_exact(c->dim, model->kind, ta, grid, c->tile_nodes, c->node_bufs,
+                                c->table_bufs, wj ? 1 : 0, v, b, g, c->jpart, c->dotpart,
+                                c->status, ma, s));
     c->launches++;
   }
   if (c->n_cross > 0 || wj) {

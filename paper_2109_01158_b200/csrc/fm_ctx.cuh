@@ -197,6 +197,11 @@ struct ModelArgs {
 #ifndef FM_ABLATE
 #define FM_ABLATE 0
 #endif
+// the warp-specialised kernel experiment (fm_eval_ws.cu) is compiled only into
+// the separate library tools/ws_check.sh builds (-DFM_WS_KERNEL=1)
+#ifndef FM_WS_KERNEL
+#define FM_WS_KERNEL 0
+#endif
 #define FM_DBG(m) (FM_ABLATE ? (m).dbg : 0)
 
 // x ** e with numpy's fast scalar cases (-1, 0, 0.5, 1, 2) and, beyond numpy,
@@ -273,6 +278,7 @@ struct fm_ctx {
   int64_t n_tile_elems = 0, n_node_entries = 0;
   int max_tile_elems = 0, max_tile_entries = 0, max_tile_nodes = 0, entry_cap = 0, clo_cap = 0;
   int n_sm = 0, ctas_per_sm = 2, node_bufs = 2, table_bufs = 2;
+  bool ws = false;  // experiment builds (FM_WS_KERNEL): fused J + gradient through fm_eval_ws.cu
   uint8_t *aos = nullptr;
   int4 *conn4 = nullptr;
   fm::TileMeta *meta = nullptr;

@@ -58,6 +58,15 @@ cudaError_t launch_finish_cross_fd(int d, int64_t ntn, const int4 *xdesc, const 
 size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
                        int dn = 0);
 
+// the warp-specialised variant of the fused J + exact gradient (fm_eval_ws.cu):
+// one 768-thread CTA per SM (a node group and two element groups), 256-node
+// tiles only; modes 0 / 1 of launch_tile_exact, bitwise the same gradient
+cudaError_t launch_tile_ws(int dim, int model, const TileArgs &a, int grid, bool wj,
+                           const double *v, const double *b, double *g, double *jpart,
+                           double *bvpart, unsigned long long *status, const ModelArgs &m,
+                           cudaStream_t s);
+size_t tile_ws_smem(int dim, int d, int blk_cap, int clo_cap);
+
 
 cudaError_t launch_energy(int dim, int model, const TileArgs &aos, int64_t ne, int nblocks,
                           const double *v, double *part, double *dens, const ModelArgs &m,
