@@ -1642,6 +1642,30 @@ int fm_ctx_stats_get(const fm_ctx *c, fm_ctx_stats *out) {
 
 int64_t fm_ctx_launches(const fm_ctx *c) { return c ? c->launches : 0; }
 
+#if FM_WS_KERNEL
+// experiment builds only (tools/bank_probe.py): one tile's metadata, the
+// closure indices of its own elements (u16 x 4 each, storage order), its
+// closure's node ids and its chunk entry blocks, copied to the host
+extern "C" int fm_debug_tile(const fm_ctx *c, int t, int *meta16, unsigned short *loc4,
+                             int *closure, unsigned short *blocks) {
+  if (!c || t < 0 || t >= c->n_tiles_all) return FM_INVALID_ARG;
+  TileMeta tm;
+  if (cudaMemcpy(&tm, c->meta + t, sizeof(tm), cudaMemcpyDeviceToHost)) return FM_CUDA_ERROR;
+  memcpy(meta16, &tm, sizeof(tm));
+  if (loc4 && cudaMemcpy(loc4, c->loc + tm.own_begin, (size_t)tm.own_count * 8,
+                         cudaMemcpyDeviceToHost))
+    return FM_CUDA_ERROR;
+  if (closure && cudaMemcpy(closure, c->closure + tm.clo_begin, (size_t)tm.clo_count * 4,
+                            cudaMemcpyDeviceToHost))
+    return FM_CUDA_ERROR;
+  const int nch = (tm.own_count + c->tile_nodes - 1) / c->tile_nodes;
+  if (blocks && cudaMemcpy(blocks, c->chunk_blocks + tm.blk_base,
+                           (size_t)nch * tm.blk_stride * 2, cudaMemcpyDeviceToHost))
+    return FM_CUDA_ERROR;
+  return FM_OK;
+}
+#endif
+
 int fm_energy(fm_ctx *c, const fm_model *model, const double *v, const double *b, double *J_out,
               double *densities, void *stream) {
   FM_NVTX("fm_energy");
