@@ -17,6 +17,9 @@ import tempfile
 sass_csv, lib, cubin, kern = sys.argv[1:5]
 lib = os.path.abspath(lib)
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 30
+# optional 6th argument: another per-instruction column to aggregate, e.g.
+# "Instructions Executed" (default: the warp-stall samples)
+column = sys.argv[6] if len(sys.argv) > 6 else "Warp Stall Sampling (All Samples)"
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", cubin, lib], cwd=tmp, check=True, capture_output=True)
 dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], capture_output=True,
@@ -35,13 +38,13 @@ for ln in dis[start + 1:]:
         a2l[int(m.group(1), 16)] = cur
 rows = list(csv.reader(open(sass_csv)))
 hdr, data = rows[1], rows[2:]
-ia, iss = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
+ia, iss = hdr.index("Address"), hdr.index(column)
 base = int(data[0][ia], 16)
 agg, tot = collections.Counter(), 0
 for r in data:
     try:
-        s = int(r[iss])
-    except ValueError:
+        s = int(float(r[iss]))
+    except (ValueError, IndexError):
         continue
     agg[a2l.get(int(r[ia], 16) - base, ("?", 0))] += s
     tot += s
