@@ -713,7 +713,7 @@ def main():
                        "tiles": {k: dm.stats[k] for k in (
                            "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
                            "ctas_per_sm", "node_bufs", "table_bufs", "entry_cap", "cross_entries",
-                           "closure_cap")}},
+                           "dict_tiles", "closure_cap")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_tile_exact<3,NH,J,256,NB=%d,TB=%d,2>" % (

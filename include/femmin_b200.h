@@ -159,6 +159,8 @@ typedef struct {
   int32_t tile_threads, ctas_per_sm, node_bufs, table_bufs;  /* tile-kernel launch shape */
   int32_t entry_cap, closure_cap;                            /* per-tile table capacities */
   int64_t cross_entries;       /* node entries whose element another tile computes */
+  int64_t dict_tiles;          /* tiles whose element records are dictionary-coded (<= 16
+                                  distinct records: 1 B per element streamed instead of 80 / 48) */
 } fm_ctx_stats;
 
 int fm_ctx_create(const fm_mesh_desc *desc, const fm_tiling *tiling, void *stream,

@@ -42,7 +42,7 @@ class FmCtxStats(C.Structure):
                 ("max_tile_entries", i64), ("bytes_device", i64), ("redundancy", dbl),
                 ("tile_threads", i32), ("ctas_per_sm", i32), ("node_bufs", i32),
                 ("table_bufs", i32), ("entry_cap", i32), ("closure_cap", i32),
-                ("cross_entries", i64)]
+                ("cross_entries", i64), ("dict_tiles", i64)]
 
 
 # name: (restype, argtypes) — every symbol declared in include/femmin_b200.h

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -522,6 +523,63 @@ __global__ void k_tile_bounds(int n_tiles, int64_t M, const uint64_t *ukeys, int
       (w ? split : ptr)[t] = (int32_t)lo;
     }
   }
+}
+
+// Record dictionaries (DICT_MAX in fm_ctx.cuh): one block per tile.  Round k
+// takes the first own element no earlier entry matched as entry k and marks
+// every element whose record has the same bits; more than DICT_MAX distinct
+// records leave the tile uncoded (dict_n = 0).  Deterministic: entries in the
+// order of first occurrence.
+template <int RB>
+__global__ void k_tile_dict(int n_tiles_all, TileMeta *meta, const uint8_t *__restrict__ aos,
+                            uint8_t *__restrict__ eidx, uint8_t *__restrict__ dict_rec) {
+  constexpr int NQ = RB / 16;
+  __shared__ int4 rep[NQ];
+  __shared__ int first;
+  const int t = blockIdx.x;
+  if (t >= n_tiles_all) return;
+  const int64_t e0 = meta[t].own_begin;
+  const int n = meta[t].own_count;
+  constexpr int PER = (MAX_TILE_ELEMS + 255) / 256;  // elements per thread (block of 256)
+  unsigned long long pending = 0;  // bit i: element threadIdx.x + 256 i is unmatched
+  for (int i = 0; i < PER; ++i)
+    if ((int)threadIdx.x + 256 * i < n) pending |= 1ull << i;
+  int k = 0;
+  for (;; ++k) {
+    if (threadIdx.x == 0) first = INT_MAX;
+    __syncthreads();
+    if (pending) atomicMin(&first, (int)threadIdx.x + 256 * (__ffsll((long long)pending) - 1));
+    __syncthreads();
+    const int f = first;
+    if (f == INT_MAX) break;  // every element matched
+    if (k == DICT_MAX) {      // too many distinct records: stream them
+      k = 0;
+      break;
+    }
+    if (threadIdx.x < NQ)
+      rep[threadIdx.x] = reinterpret_cast<const int4 *>(aos + (e0 + f) * RB)[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < NQ)
+      reinterpret_cast<int4 *>(dict_rec + ((int64_t)t * DICT_MAX + k) * RB)[threadIdx.x] =
+          rep[threadIdx.x];
+    for (unsigned long long m = pending; m; m &= m - 1) {
+      const int i = __ffsll((long long)m) - 1;
+      const int e = (int)threadIdx.x + 256 * i;
+      const int4 *r = reinterpret_cast<const int4 *>(aos + (e0 + e) * RB);
+      bool same = true;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int4 x = r[q], y = rep[q];
+        same &= x.x == y.x && x.y == y.y && x.z == y.z && x.w == y.w;
+      }
+      if (same) {
+        eidx[e0 + e] = (uint8_t)k;
+        pending &= ~(1ull << i);
+      }
+    }
+    __syncthreads();  // rep and first are rewritten next round
+  }
+  if (threadIdx.x == 0) meta[t].dict_n = k;
 }
 
 // Tile element positions ("dealt" order).  The sorted (tile, halo?, element)
@@ -1485,6 +1543,33 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
     CK(cudaStreamSynchronize(s));
   }
 
+  // record dictionaries (DICT_MAX): per tile the distinct own-element records
+  // and one slot byte per element; FM_TILE_DICT=0 streams the records of every tile
+  {
+    const char *de = getenv("FM_TILE_DICT");  // read per build (tests toggle it)
+    const bool use_dict = !de || atoi(de) != 0;
+    const int rbz = dim == 3 ? RecBytes<3>::value : RecBytes<2>::value;
+    CK(dmalloc(&c->eidx, (size_t)ne + 32, &B));
+    CK(cudaMemsetAsync(c->eidx, 0, (size_t)ne + 32, s));
+    CK(dmalloc(&c->dict_rec, (size_t)std::max(1, c->n_tiles_all) * DICT_MAX * rbz, &B));
+    c->n_dict_tiles = 0;
+    if (use_dict && c->n_tiles_all > 0) {
+      static_assert(MAX_TILE_ELEMS <= 64 * 256, "k_tile_dict: one pending bit per element");
+      if (dim == 3)
+        k_tile_dict<RecBytes<3>::value><<<c->n_tiles_all, 256, 0, s>>>(c->n_tiles_all, c->meta,
+                                                                      c->aos, c->eidx, c->dict_rec);
+      else
+        k_tile_dict<RecBytes<2>::value><<<c->n_tiles_all, 256, 0, s>>>(c->n_tiles_all, c->meta,
+                                                                      c->aos, c->eidx, c->dict_rec);
+      CK(cudaGetLastError());
+      std::vector<TileMeta> hm2(c->n_tiles_all);
+      CK(cudaMemcpyAsync(hm2.data(), c->meta, hm2.size() * sizeof(TileMeta),
+                         cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (const TileMeta &tm : hm2) c->n_dict_tiles += tm.dict_n > 0;
+    }
+  }
+
   // CTAs per SM: registers allow 4 x 128 / 2 x 256 threads (3D; 2D: 8 / 4,
   // tile_exact_minb); shared memory
   // (228 KB per SM, 1 KB reserved per CTA) decides, preferring two node-value
@@ -1578,6 +1663,7 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
   st.entry_cap = c->entry_cap;
   st.closure_cap = c->clo_cap;
   st.cross_entries = c->n_cross;
+  st.dict_tiles = c->n_dict_tiles;
   *out = c;
   return FM_OK;
 }
@@ -1627,7 +1713,7 @@ int fm_ctx_destroy(fm_ctx *c) {
                   c->dotpart,   c->status,    c->xkey,      c->xpos,      c->xchunk,
                   c->node_xbase, c->node_xn,  c->xbuf,      c->fixed_nodes, c->node_outw, c->node_fmask,
                   c->partial,   c->node_clo,  c->chunk_blocks, c->fpart, c->ticket,
-                  c->xnodes,    c->dof_pos,   c->xdesc};
+                  c->xnodes,    c->dof_pos,   c->xdesc,     c->eidx,      c->dict_rec};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1646,6 +1732,16 @@ int64_t fm_ctx_launches(const fm_ctx *c) { return c ? c->launches : 0; }
 // experiment builds only (tools/bank_probe.py): one tile's metadata, the
 // closure indices of its own elements (u16 x 4 each, storage order), its
 // closure's node ids and its chunk entry blocks, copied to the host
+extern "C" int fm_debug_tile_records(const fm_ctx *c, int t, unsigned char *rec) {
+  if (!c || t < 0 || t >= c->n_tiles_all) return FM_INVALID_ARG;
+  TileMeta tm;
+  if (cudaMemcpy(&tm, c->meta + t, sizeof(tm), cudaMemcpyDeviceToHost)) return FM_CUDA_ERROR;
+  const size_t rb = c->dim == 3 ? 80 : 48;
+  if (cudaMemcpy(rec, c->aos + (size_t)tm.own_begin * rb, (size_t)tm.own_count * rb,
+                 cudaMemcpyDeviceToHost))
+    return FM_CUDA_ERROR;
+  return FM_OK;
+}
 extern "C" int fm_debug_tile(const fm_ctx *c, int t, int *meta16, unsigned short *loc4,
                              int *closure, unsigned short *blocks) {
   if (!c || t < 0 || t >= c->n_tiles_all) return FM_INVALID_ARG;

@@ -40,6 +40,14 @@ constexpr unsigned CROSS_FLAG = 1u << 31;  // node_desc.x: the node has cross en
 constexpr int MAX_CHUNKS = 9;          // per-chunk entry counts in node_desc.x/.y (5 bits each)
 constexpr int ENTRY_OFF_MASK = (1 << 13) - 1;  // node_desc.x bits 0..12: tile-local entry offset
 constexpr int XCH_STRIDE = 12;  // ints per tile in xchunk (MAX_CHUNKS + 1, padded to 16 B)
+// Record dictionaries: a tile whose own elements share at most DICT_MAX distinct
+// records (vol, dphi — bit patterns; structured meshes have a handful) keeps
+// them as a per-tile table, and its elements as one byte each (the record's
+// table slot, TileArgs::eidx).  The tile kernel then streams 1 B instead of
+// 80 / 48 B per element and reads the record from the table in shared memory;
+// the values are the same bits.  Tiles with more distinct records (unstructured
+// meshes) stream their records as before.
+constexpr int DICT_MAX = 16;
 
 // entries of this node in chunk ch of its tile (node_desc packing, see k_node_desc)
 __device__ __forceinline__ int chunk_count(int4 nd, int ch) {
@@ -66,7 +74,8 @@ struct TileMeta {
   int clo_begin, clo_count;      // node closure (clo_begin % 4 == 0)
   int blk_stride;                // chunk entry blocks: u16 units per block (multiple of 8)
   int64_t blk_base;              // first block of the tile in chunk_blocks (u16 units)
-  int pad[2];
+  int dict_n;                    // distinct element records of the tile (0: not dictionary-coded)
+  int pad;
 };
 static_assert(sizeof(TileMeta) == 64, "TileMeta layout");
 
@@ -244,6 +253,8 @@ struct TileArgs {
   double *xbuf;
   double *partial;             // tile node x D: own-element sums of nodes with cross entries
   const uint16_t *node_clo;    // tile node -> its index in the tile's node closure
+  const uint8_t *eidx;         // dictionary slot of each element (storage order; see DICT_MAX)
+  const uint8_t *dict_rec;     // per tile DICT_MAX records (tile t at t * DICT_MAX * record bytes)
   int n_tiles;                 // node tiles
   int n_tiles_all;             // + orphan tiles (J only)
   int entry_cap;               // max entries of one tile, rounded up to 8
@@ -302,6 +313,8 @@ struct fm_ctx {
   int32_t *node_outw = nullptr;  // per tile node: output offset (finishing pass)
   uint8_t *node_fmask = nullptr;  // per tile node: free-component mask (finishing pass)
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
+  uint8_t *eidx = nullptr, *dict_rec = nullptr;  // record dictionaries (see DICT_MAX)
+  int64_t n_dict_tiles = 0;
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units
   int64_t blk_total = 0;             // size of chunk_blocks, u16 units
@@ -324,7 +337,8 @@ struct fm_ctx {
     return fm::TileArgs{aos,     conn4,   storage_to_orig, meta,      halo_ids,    halo_loc,
                         loc,     closure, flags,   node_desc,       node_entries, chunk_blocks,
                         rank_of, xkey,
-                        xpos,    xchunk,  xbuf,            partial,   node_clo,    n_tiles,
+                        xpos,    xchunk,  xbuf,            partial,   node_clo,    eidx,
+                        dict_rec, n_tiles,
                         n_tiles_all, entry_cap, blk_cap, clo_cap};
   }
 };

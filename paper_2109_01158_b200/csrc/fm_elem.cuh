@@ -22,7 +22,9 @@ struct PipeLayout {
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
   // per-tile tables: node descriptors | exchange-item chunk starts
-  __host__ __device__ static size_t tabs() { return (size_t)CT * 16 + XCH_STRIDE * 4; }
+  // (+ the tile's record dictionary, DICT_MAX records)
+  __host__ __device__ static size_t dict_off() { return (size_t)CT * 16 + XCH_STRIDE * 4; }
+  __host__ __device__ static size_t tabs() { return dict_off() + (size_t)DICT_MAX * RB; }
   // contributions staging: [slot][component][row], except D = 2 (2D
   // Neo-Hookean): [slot][row][2] (one 16-B store / load per entry; cfg3 tile
   // kernel 0.1086 -> 0.1064 ms — the same with 4 padded doubles for D = 3

@@ -345,6 +345,9 @@ __global__ void __launch_bounds__(CT, MINB)
   auto xch_of = [&](int k) {  // the tile's exchange-item chunk starts
     return reinterpret_cast<int *>(tabs0 + k * L::tabs() + (size_t)CT * 16);
   };
+  auto dict_of = [&](int k) {  // the tile's record dictionary (dictionary-coded tiles)
+    return reinterpret_cast<unsigned char *>(tabs0 + k * L::tabs() + L::dict_off());
+  };
   double *stage_d = reinterpret_cast<double *>(tabs0 + TB * L::tabs());
   double *red = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stage_d) +
                                            L::staging(D));
@@ -385,9 +388,11 @@ __global__ void __launch_bounds__(CT, MINB)
     const TileMeta tm = a.meta[t];
     const uint32_t nb = (uint32_t)tm.node_count * 16;
     const uint32_t xb_ = t < a.n_tiles ? XCH_STRIDE * 4 : 0;
-    mbar_arrive_expect_tx(tfull + k, nb + xb_);
+    const uint32_t db = (uint32_t)tm.dict_n * RB;
+    mbar_arrive_expect_tx(tfull + k, nb + xb_ + db);
     if (nb) bulk_g2s(desc_of(k), a.node_desc + tm.node_begin, nb, tfull + k);
     if (xb_) bulk_g2s(xch_of(k), a.xchunk + (int64_t)t * XCH_STRIDE, xb_, tfull + k);
+    if (db) bulk_g2s(dict_of(k), a.dict_rec + (int64_t)t * DICT_MAX * RB, db, tfull + k);
   };
   auto gather_nodev = [&](int clo_count, int k) {  // v of the closure -> nodev(k)
     double *dst = nodev(k);
@@ -412,9 +417,17 @@ __global__ void __launch_bounds__(CT, MINB)
     const int64_t l0 = r0 & ~1ll;
     const uint32_t nl = (uint32_t)((cnt + (r0 - l0) + 1) & ~1);
     const uint32_t bb = (uint32_t)x.tm.blk_stride * 2;
-    mbar_arrive_expect_tx(full + s, (uint32_t)cnt * RB + nl * 8 + bb);
+    // records, or (dictionary-coded tile) their one-byte dictionary slots: the
+    // byte range widened to 16-B alignment, row r at position r + (r0 & 15)
+    const int64_t i0 = r0 & ~15ll;
+    const uint32_t rbytes = x.tm.dict_n ? (uint32_t)((cnt + (r0 - i0) + 15) & ~15)
+                                        : (uint32_t)cnt * RB;
+    mbar_arrive_expect_tx(full + s, rbytes + nl * 8 + bb);
     if (cnt) {
-      bulk_g2s(stg(s), a.aos + r0 * RB, (uint32_t)cnt * RB, full + s);
+      if (x.tm.dict_n)
+        bulk_g2s(stg(s), a.eidx + i0, rbytes, full + s);
+      else
+        bulk_g2s(stg(s), a.aos + r0 * RB, rbytes, full + s);
       bulk_g2s(stg(s) + L::loc_off(), a.loc + l0, nl * 8, full + s);
     }
     if (bb)
@@ -534,7 +547,14 @@ __global__ void __launch_bounds__(CT, MINB)
         bool far = false;
         Elem<DIM> E;
         if (valid) {
-          load_elem_smem<DIM>(stg(s), tid, E);
+          // the record: row tid of the stage, or the dictionary entry its slot byte names
+          const unsigned char *rbase = stg(s);
+          int ridx = tid;
+          if (tm.dict_n) {
+            ridx = rbase[((tm.own_begin + c0) & 15) + tid];
+            rbase = dict_of(tb);
+          }
+          load_elem_smem<DIM>(rbase, ridx, E);
           decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + L::loc_off() +
                                                        (tid + ((tm.own_begin + c0) & 1)) * 8),
                      E.loc);
@@ -555,7 +575,7 @@ __global__ void __launch_bounds__(CT, MINB)
             if (has_nodes) {
               const FdSink sink{st_at(0, tid), (int)L::slot_stride(D), CS, a.closure, a.rank_of,
                                 a.s2o, tm.clo_begin, (int64_t)tm.own_begin + c0 + tid};
-              fd_element<DIM, MODEL, D>(vv, E, mdl, sink, stg(s), tid, nv, CAP,
+              fd_element<DIM, MODEL, D>(vv, E, mdl, sink, rbase, ridx, nv, CAP,
                                         make_int4(E.loc[0], E.loc[1], E.loc[2],
                                                   DIM == 3 ? E.loc[DIM] : 0),
                                         &fdkey);

@@ -272,7 +272,7 @@ class SlabStack:
         st = [m.stats for m in self.dms]
         self.stats = dict(st[0])
         for key in ("n_tiles", "n_orphan_tiles", "tile_elems_total", "node_entries_total",
-                    "bytes_device", "cross_entries"):
+                    "bytes_device", "cross_entries", "dict_tiles"):
             self.stats[key] = sum(x[key] for x in st)
         for key in ("max_tile_elems", "max_tile_entries", "entry_cap", "closure_cap"):
             self.stats[key] = max(x[key] for x in st)
