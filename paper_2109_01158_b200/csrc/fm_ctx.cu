@@ -1566,7 +1566,12 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
       CK(cudaMemcpyAsync(hm2.data(), c->meta, hm2.size() * sizeof(TileMeta),
                          cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      for (const TileMeta &tm : hm2) c->n_dict_tiles += tm.dict_n > 0;
+      bool all = true;
+      for (const TileMeta &tm : hm2) {
+        c->n_dict_tiles += tm.dict_n > 0;
+        all &= tm.dict_n > 0 || tm.own_count == 0;
+      }
+      c->all_coded = all;  // the stages then hold slot bytes, not records
     }
   }
 
@@ -1577,14 +1582,17 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
   {
     const int regs_cap = tile_exact_minb(dim, c->tile_nodes);
     auto fit = [&](int nb, int tb) {
-      const size_t sm = tile_exact_smem(dim, d, c->blk_cap, c->clo_cap, c->tile_nodes, nb, tb);
+      const size_t sm = tile_exact_smem(dim, d, c->blk_cap, c->clo_cap, c->tile_nodes, nb, tb, 0,
+                                        c->all_coded);
       return sm > 227 * 1024 ? 0 : std::min<int>(regs_cap, (int)(228 * 1024 / (sm + 1024)));
     };
     // most CTAs per SM first, then the next tile's tables a tile ahead
     // (tb = 2); node values a tile ahead (nb = 2) measured better in 2D (many
-    // small tiles, config 2/3) and worse in 3D (config 4: 0.874 vs 0.861 ms);
-    // FM_TILE_CFG="nb,tb" forces a variant
-    const int nb_pref = dim == 2 ? 2 : 1;
+    // small tiles, config 2/3) and, with streamed records, worse in 3D (config
+    // 4: 0.874 vs 0.861 ms: 225 KB of shared memory leave no L1); with
+    // dictionary-coded records the stages are small and nb = 2 wins there too
+    // (config 4: 0.805 vs 0.818 ms); FM_TILE_CFG="nb,tb" forces a variant
+    const int nb_pref = (dim == 2 || c->all_coded) ? 2 : 1;
     int best = -1;
     for (int nb = 2; nb >= 1; --nb)
       for (int tb = 2; tb >= 1; --tb) {
@@ -1858,7 +1866,7 @@ int fm_hvp_exact(fm_ctx *c, const fm_model *model, const double *v, const double
   TileArgs ta = c->tile_args();
   ta.n_tiles_all = c->n_tiles;  // no J: orphan tiles not needed
   if (tile_exact_smem(c->dim, c->d, c->blk_cap, c->clo_cap, c->tile_nodes, c->node_bufs,
-                      c->table_bufs, 2 * c->d) > 227 * 1024) {
+                      c->table_bufs, 2 * c->d, c->all_coded) > 227 * 1024) {
     set_error("Hessian-vector tile staging exceeds shared memory; use smaller tiles");
     return FM_INVALID_ARG;
   }

@@ -260,6 +260,8 @@ struct TileArgs {
   int entry_cap;               // max entries of one tile, rounded up to 8
   int blk_cap;                 // max chunk entry block, u16 units
   int clo_cap;                 // max closure size, rounded up to 4
+  int all_coded;               // every tile with elements is dictionary-coded: the record
+                               // area of a stage holds slot bytes only
 };
 
 // Deterministic block sum (fixed shuffle tree + fixed warp order).
@@ -315,6 +317,7 @@ struct fm_ctx {
   uint16_t *node_clo = nullptr;  // per tile node: index in its tile's closure
   uint8_t *eidx = nullptr, *dict_rec = nullptr;  // record dictionaries (see DICT_MAX)
   int64_t n_dict_tiles = 0;
+  bool all_coded = false;  // every tile with elements is coded (small record stages)
   uint16_t *chunk_blocks = nullptr;  // chunk-major entry blocks (TileMeta blk_base / blk_stride)
   int blk_cap = 0;                   // max block size, u16 units
   int64_t blk_total = 0;             // size of chunk_blocks, u16 units
@@ -339,6 +342,6 @@ struct fm_ctx {
                         rank_of, xkey,
                         xpos,    xchunk,  xbuf,            partial,   node_clo,    eidx,
                         dict_rec, n_tiles,
-                        n_tiles_all, entry_cap, blk_cap, clo_cap};
+                        n_tiles_all, entry_cap, blk_cap, clo_cap, all_coded ? 1 : 0};
   }
 };

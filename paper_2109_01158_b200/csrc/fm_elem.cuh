@@ -14,10 +14,17 @@ template <int DIM, int CT>
 struct PipeLayout {
   static constexpr int RB = RecBytes<DIM>::value;
   // stage: the chunk's records | their closure indices | its entry block
-  __host__ __device__ static size_t loc_off() { return r16((size_t)CT * RB); }
-  __host__ __device__ static size_t blk_off() { return loc_off() + (size_t)(CT + 2) * 8; }
-  __host__ __device__ static size_t stage(int blk_cap) {
-    return blk_off() + r16((size_t)blk_cap * 2);
+  // rec: bytes of the stage's record area — CT records, or only CT + 16 slot
+  // bytes when every tile of the context is dictionary-coded (rec_area)
+  __host__ __device__ static size_t rec_area(bool all_coded) {
+    return all_coded ? r16((size_t)CT + 16) : r16((size_t)CT * RB);
+  }
+  __host__ __device__ static size_t loc_off(size_t rec = rec_area(false)) { return rec; }
+  __host__ __device__ static size_t blk_off(size_t rec = rec_area(false)) {
+    return loc_off(rec) + (size_t)(CT + 2) * 8;
+  }
+  __host__ __device__ static size_t stage(int blk_cap, size_t rec = rec_area(false)) {
+    return blk_off(rec) + r16((size_t)blk_cap * 2);
   }
   __host__ __device__ static size_t nodev(int D, int clo_cap) { return r16((size_t)D * clo_cap * 8); }
   __host__ __device__ static size_t cids(int clo_cap) { return r16((size_t)clo_cap * 4); }
@@ -43,9 +50,9 @@ struct PipeLayout {
   // (dn: node-value components per node, D; 2 D for the Hessian-vector
   // product, which gathers the direction's node values too)
   __host__ __device__ static size_t total(int D, int blk_cap, int clo_cap, int nb, int tb,
-                                          int dn = 0) {
-    return 2 * stage(blk_cap) + nb * nodev(dn ? dn : D, clo_cap) + cids(clo_cap) + tb * tabs() +
-           staging(D) + 32 * 8 + 8 * 8;
+                                          int dn = 0, size_t rec = rec_area(false)) {
+    return 2 * stage(blk_cap, rec) + nb * nodev(dn ? dn : D, clo_cap) + cids(clo_cap) +
+           tb * tabs() + staging(D) + 32 * 8 + 8 * 8;
   }
 };
 

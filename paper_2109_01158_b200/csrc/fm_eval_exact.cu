@@ -333,7 +333,8 @@ __global__ void __launch_bounds__(CT, MINB)
   using L = PipeLayout<DIM, CT>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int CAP = a.clo_cap;
-  const size_t SG = L::stage(a.blk_cap);
+  const size_t REC = L::rec_area(a.all_coded != 0);  // record area of a stage
+  const size_t SG = L::stage(a.blk_cap, REC);
   // stage s at smem + s * SG; node-value buffer k at nodev0 + k * nodev()
   auto stg = [&](int s) { return smem + s * SG; };
   auto nodev = [&](int k) {
@@ -428,10 +429,10 @@ __global__ void __launch_bounds__(CT, MINB)
         bulk_g2s(stg(s), a.eidx + i0, rbytes, full + s);
       else
         bulk_g2s(stg(s), a.aos + r0 * RB, rbytes, full + s);
-      bulk_g2s(stg(s) + L::loc_off(), a.loc + l0, nl * 8, full + s);
+      bulk_g2s(stg(s) + L::loc_off(REC), a.loc + l0, nl * 8, full + s);
     }
     if (bb)
-      bulk_g2s(stg(s) + L::blk_off(),
+      bulk_g2s(stg(s) + L::blk_off(REC),
                a.chunk_blocks + x.tm.blk_base + (int64_t)(x.c0 / CT) * x.tm.blk_stride, bb,
                full + s);
   };
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(CT, MINB)
             rbase = dict_of(tb);
           }
           load_elem_smem<DIM>(rbase, ridx, E);
-          decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + L::loc_off() +
+          decode_loc(*reinterpret_cast<const uint2 *>(stg(s) + L::loc_off(REC) +
                                                        (tid + ((tm.own_begin + c0) & 1)) * 8),
                      E.loc);
           double vv[D][NV];
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(CT, MINB)
           // this node's entries of the chunk (its slice of the chunk's entry
           // block): the loads of two entries are issued together; the order
           // (ascending tile element) is the fixed summation order
-          const uint16_t *blk = reinterpret_cast<const uint16_t *>(stg(s) + L::blk_off());
+          const uint16_t *blk = reinterpret_cast<const uint16_t *>(stg(s) + L::blk_off(REC));
           const int e_beg = blk[tid], n = blk[tid + 1] - e_beg;
           const uint16_t *ents = blk + blk_header(tm.node_count) + e_beg;
           int i = 0;
@@ -851,13 +852,19 @@ cudaError_t launch_finish_cross_fd(int d, int64_t ntn, const int4 *xdesc, const 
   return cudaGetLastError();
 }
 
-size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
-                       int dn) {
+template <int DIM, int CT>
+static size_t smem_of(int d, int blk_cap, int clo_cap, int nb, int tb, int dn, bool all_coded) {
+  using L = PipeLayout<DIM, CT>;
+  return L::total(d, blk_cap, clo_cap, nb, tb, dn, L::rec_area(all_coded));
+}
+
+size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb, int dn,
+                       bool all_coded) {
   if (ct == 128)
-    return dim == 3 ? PipeLayout<3, 128>::total(d, blk_cap, clo_cap, nb, tb, dn)
-                    : PipeLayout<2, 128>::total(d, blk_cap, clo_cap, nb, tb, dn);
-  return dim == 3 ? PipeLayout<3, 256>::total(d, blk_cap, clo_cap, nb, tb, dn)
-                  : PipeLayout<2, 256>::total(d, blk_cap, clo_cap, nb, tb, dn);
+    return dim == 3 ? smem_of<3, 128>(d, blk_cap, clo_cap, nb, tb, dn, all_coded)
+                    : smem_of<2, 128>(d, blk_cap, clo_cap, nb, tb, dn, all_coded);
+  return dim == 3 ? smem_of<3, 256>(d, blk_cap, clo_cap, nb, tb, dn, all_coded)
+                  : smem_of<2, 256>(d, blk_cap, clo_cap, nb, tb, dn, all_coded);
 }
 
 template <int DIM, int MODEL, int CT, int NB, int TB>
@@ -867,7 +874,7 @@ static cudaError_t launch_cfg(const TileArgs &a, int grid, int mode, const doubl
   constexpr int D = MODEL == FM_MODEL_NEOHOOKEAN ? DIM : 1;
   constexpr int MINB = tile_exact_minb(DIM, CT), MINBF = tile_fd_minb(DIM, CT, MODEL);
   const size_t smem =
-      PipeLayout<DIM, CT>::total(D, a.blk_cap, a.clo_cap, NB, TB, mode == 2 ? 2 * D : D);
+      smem_of<DIM, CT>(D, a.blk_cap, a.clo_cap, NB, TB, mode == 2 ? 2 * D : D, a.all_coded != 0);
   auto k = mode == 4   ? k_tile_exact<DIM, MODEL, true, false, false, true, CT, NB, TB, MINB>
            : mode == 3 ? k_tile_exact<DIM, MODEL, false, false, true, false, CT, NB, TB, MINBF>
            : mode == 2 ? k_tile_exact<DIM, MODEL, false, true, false, false, CT, NB, TB, MINB>

@@ -56,7 +56,7 @@ cudaError_t launch_finish_cross_fd(int d, int64_t ntn, const int4 *xdesc, const 
                                    double eps, const double *b, const int4 *node_desc,
                                    cudaStream_t s);
 size_t tile_exact_smem(int dim, int d, int blk_cap, int clo_cap, int ct, int nb, int tb,
-                       int dn = 0);
+                       int dn = 0, bool all_coded = false);
 
 // the warp-specialised variant of the fused J + exact gradient (fm_eval_ws.cu):
 // one 768-thread CTA per SM (a node group and two element groups), 256-node
