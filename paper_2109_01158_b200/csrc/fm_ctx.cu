@@ -1572,6 +1572,15 @@ static int ctx_build(const fm_mesh_desc *m, const fm_tiling *tiling, void *strea
         all &= tm.dict_n > 0 || tm.own_count == 0;
       }
       c->all_coded = all;  // the stages then hold slot bytes, not records
+#if !FM_WS_KERNEL
+      // no kernel reads the full records of a coded 3D context any more (its
+      // energy runs through the tile pipeline too): 80 B per element back
+      if (all && dim == 3) {
+        CK(cudaFree(c->aos));
+        c->aos = nullptr;
+        B -= (size_t)ne * rbz;
+      }
+#endif
     }
   }
 
