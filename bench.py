@@ -708,8 +708,11 @@ def main():
                        "hbm_build_peak_gb": msamp.peak / 1e9,
                        "parallelism": f"x1-slabs x{world}" if world > 1 else "single GPU",
                        "step_graph": graph is not None,
-                       "l2": f"inputs ({alg / 1e9:.2f} GB per eval) larger than the 126 MB L2; "
-                             "no flush",
+                       "l2": (f"DRAM traffic per evaluation (ncu: {traffic / 1e9:.2f} GB in the "
+                              "tile kernel, plus the finishing pass) is larger than the 126 MB "
+                              "L2; no flush" if traffic else
+                              f"inputs ({alg / 1e9:.2f} GB per eval) larger than the 126 MB L2; "
+                              "no flush"),
                        "tiles": {k: dm.stats[k] for k in (
                            "n_tiles", "redundancy", "max_tile_elems", "tile_threads",
                            "ctas_per_sm", "node_bufs", "table_bufs", "entry_cap", "cross_entries",
