@@ -73,6 +73,19 @@ def test_dictionary_coded_tiles_give_the_same_bits(name, make, eps):
         assert np.array_equal(x, y), f"{name}: {what} differs between coded and streamed records"
 
 
+def test_mixed_context_gives_the_same_bits():
+    """A beam whose spacing (1/24) rounds differently from cell to cell: only a
+    few tiles have <= 16 distinct records, so coded and streamed tiles share
+    one launch (and the stages keep their full record area)."""
+    make = lambda: problems.beam(48, 24, 24, seed=11, keep=True)  # noqa: E731
+    on = _build(make, True)
+    off = _build(make, False)
+    assert 0 < on.dm.stats["dict_tiles"] < on.dm.stats["n_tiles"]
+    a, b = _all_outputs(on, 1e-8), _all_outputs(off, 1e-8)
+    for what, x, y in zip(("J", "g (with J)", "g", "J energy", "densities", "FD g", "Hp"), a, b):
+        assert np.array_equal(x, y), f"{what} differs between coded and streamed records"
+
+
 def test_unstructured_mesh_falls_back(golden):
     """The hole mesh (mesh.py:246-286): its triangles are all different, so no
     tile beyond the tiny ones can be coded; the evaluation itself is checked
